@@ -1,0 +1,107 @@
+/*
+ * kmb.h — C ABI of the B200-native exact assignment solver (KM / batched KM).
+ *
+ * Drop-in boundary for the reference's solver entry points
+ *   ot::solve_km          /root/reference/proj/include/ot/hungarian.hpp:39-40
+ *                         (impl. proj/src/hungarian.cpp:55-136)
+ *   ot::solve_batched_km  hungarian.hpp:53-56 (impl. hungarian.cpp:313-381)
+ * and of their plugin registration  ot::bench::make_solver("km" /
+ * "batched_km")  (proj/src/bench.cpp:404-422, SolverSpec bench.hpp:24-29).
+ * The reference interface is C++ (OTInstance in, SolveResult + optional
+ * DualPotentials / Matching out, exceptions on bad input); this ABI carries the
+ * same data as plain pointers and sizes so any FFI can bind it, and
+ * include/kmb.hpp rebuilds the reference's C++ signatures on top of it.
+ *
+ * Semantics (identical to the reference on the same inputs):
+ *   cost         n x n int32, row-major with leading dimension ld (>= n),
+ *                entries in [0, 2^30) (the reference only requires >= 0; the
+ *                device engine keeps reduced costs in 32 bits).
+ *   seed         KMB_SEED_KM      = u = v = 0, the start of solve_km (:63)
+ *                KMB_SEED_BATCHED = row/column reductions (:323-333), the start
+ *                                   of solve_batched_km.
+ *                Final duals are bit-identical to the reference solver with the
+ *                same start; the total cost is the optimum.
+ *   row_to_col   assignment, n entries (Matching::row_to_col, hungarian.hpp:12-14)
+ *   u, v         row / column duals, n entries each, int64
+ *                (DualPotentials, hungarian.hpp:19-22)
+ *   total_cost   sum_i cost[i][row_to_col[i]], int64 (objective_int, core.cpp:76-90)
+ *   time_budget_s  0 = none; checked once per phase on the device
+ *                (hungarian.cpp:341-346); on expiry stats->converged = 0 and the
+ *                partial matching is returned (row_to_col = -1 for free rows).
+ * Pointers may be host or device memory (detected per call).  A call whose
+ * pointers are all device memory and whose stats pointer is NULL is
+ * asynchronous on the context's stream; otherwise it returns after the result
+ * reached the caller's buffers.
+ *
+ * Return value: 0 ok; > 0 invalid input (message via kmb_last_error(), the
+ * reference's std::invalid_argument cases); < 0 CUDA / internal error.
+ * There is no CPU fallback: without a usable B200 every solve returns < 0.
+ */
+#ifndef KMB_H
+#define KMB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KMB_ABI_VERSION 1
+
+enum kmb_seed { KMB_SEED_KM = 0, KMB_SEED_BATCHED = 1 };
+
+enum kmb_status {
+  KMB_OK = 0,
+  KMB_EINVAL = 1,        /* bad argument (n <= 0, null pointer, ld < n) */
+  KMB_ENEGATIVE = 2,     /* "costs must be nonnegative" (core.cpp:144-145) */
+  KMB_ERANGE = 3,        /* a cost >= 2^30 (device range)                  */
+  KMB_ECUDA = -1,        /* CUDA runtime error                             */
+  KMB_EINTERNAL = -2,    /* engine invariant violated                      */
+  KMB_ENODEVICE = -3     /* no sm_100 device                               */
+};
+
+enum kmb_option {
+  KMB_OPT_MAX_CTAS = 1,     /* grid engine: upper bound on CTAs (0 = #SMs)      */
+  KMB_OPT_CONTINUE_BFS = 2, /* 1: exhaust the tight closure before augmenting   */
+  KMB_OPT_ENGINE = 3        /* 0 auto, 1 grid (persistent), 2 SMEM (n <= 224)   */
+};
+
+typedef struct kmb_stats {
+  int64_t phases;          /* augmentation phases (not a parity target)      */
+  int64_t dual_steps;      /* dual adjustments: equals the reference's count */
+  int64_t rows_scanned;    /* cost rows streamed by the reduced-cost scan    */
+  int64_t cost_bytes_read; /* 4*n*(rows_scanned + n) (+ reductions)          */
+  double seconds;          /* device time of the solve (CUDA events)         */
+  int32_t converged;       /* 0 when the time budget expired                 */
+  int32_t engine;          /* 1 grid, 2 SMEM                                 */
+} kmb_stats;
+
+typedef struct kmb_context kmb_context;
+
+int kmb_create(int device, kmb_context** out);
+void kmb_destroy(kmb_context* ctx);
+/* cudaStream_t passed as void* (NULL = the legacy default stream). */
+int kmb_set_stream(kmb_context* ctx, void* cuda_stream);
+int kmb_set_option(kmb_context* ctx, int option, int64_t value);
+
+/* One n x n instance (configs 1, 2, 4, 5). */
+int kmb_solve_i32(kmb_context* ctx, const int32_t* cost, int32_t n, int64_t ld, int32_t seed,
+                  double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
+                  int64_t* total_cost, kmb_stats* stats);
+
+/* `batch` independent n x n instances stored back to back (config 3).
+ * row_to_col, u, v: batch*n entries; total_cost: batch entries; stats (optional)
+ * receives the sums over the batch. */
+int kmb_solve_batch_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, int32_t n,
+                        int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
+                        int64_t* total_cost, kmb_stats* stats);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* kmb_last_error(void);
+int kmb_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KMB_H */

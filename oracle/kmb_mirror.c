@@ -1,0 +1,173 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — a step-by-step CPU mirror of the GPU engine in
+ * paper_2005_01182_b200/csrc/ (same phases, same packed-key argmin parents,
+ * same lazy dual bookkeeping, same forest augmentation), used to debug the
+ * CUDA kernels and to check, on CPU and at scale, that the engine's duals
+ * equal the reference's.  It is not the oracle: the
+ * oracle is km_oracle.c / oracle/_ref.  Only tests/ load it.
+ *
+ * Engine (one phase = one multi-source search + one batch augmentation):
+ *  - every free row is a root; D = dual shift accumulated in this phase;
+ *  - row i reached at shift Dr stores w_i = u_i - Dr; column j keeps the
+ *    packed key min_i ((C_ij - w_i + 2^30) << 32 | i) over reached rows, so
+ *    slack'_j = val(key_j) - v_j is invariant under dual steps and a column
+ *    is tight iff slack'_j == D;
+ *  - a round = relax the rows reached last round, m = min unreached slack',
+ *    if m > D it is a dual step (D = m; no tight unreached column and no
+ *    pending row, exactly hungarian.cpp:201-215), then absorb every
+ *    unreached column with slack' == D (hungarian.cpp:186-199);
+ *  - absorbing a free column claims its tree root; the search ends after the
+ *    round that found one (or, with continue_bfs, once the tight closure at
+ *    the current D is exhausted — never with another dual step);
+ *  - duals are finalised (u_i = w_i + D, v_j -= D - Dc_j), then every claimed
+ *    tree flips its parent-pointer path (vertex-disjoint: one path per tree).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define KM_BIAS (1LL << 30)
+
+static inline uint64_t pack_key(int64_t val, int32_t row) {
+  return ((uint64_t)(uint32_t)(val + KM_BIAS) << 32) | (uint32_t)row;
+}
+static inline int64_t key_val(uint64_t k) { return (int64_t)(k >> 32) - KM_BIAS; }
+static inline int32_t key_row(uint64_t k) { return (int32_t)(k & 0xffffffffu); }
+
+/* seed: 0 = u = v = 0 (solve_km start, hungarian.cpp:63),
+ *       1 = row/column reductions (hungarian.cpp:323-333).
+ * Costs must lie in [0, 2^30).  Returns 0 or a negative error. */
+int kmm_solve(const int32_t* C, int32_t n, int32_t seed, int32_t continue_bfs,
+              int64_t* u, int64_t* v, int32_t* match_row, int64_t* total_cost,
+              int64_t* phases_out, int64_t* dual_steps_out, int64_t* rows_scanned_out,
+              int64_t* trace, int64_t trace_cap) {
+  int32_t* match_col = malloc(sizeof(int32_t) * (size_t)n);
+  uint64_t* key = malloc(sizeof(uint64_t) * (size_t)n);
+  int64_t* w = malloc(sizeof(int64_t) * (size_t)n);
+  int64_t* dc = malloc(sizeof(int64_t) * (size_t)n);
+  char* rcol = malloc((size_t)n);
+  int32_t* tree_par = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* root_row = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* claim = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* list = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* found = malloc(sizeof(int32_t) * (size_t)n);
+  if (!match_col || !key || !w || !dc || !rcol || !tree_par || !root_row ||
+      !claim || !list || !found)
+    return -1;
+  int rc = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    match_row[i] = match_col[i] = -1;
+    claim[i] = -1;
+    u[i] = 0;
+    v[i] = 0;
+  }
+  if (seed == 1)
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t* row = C + (size_t)i * n;
+      int32_t lo = row[0];
+      for (int32_t j = 1; j < n; ++j) if (row[j] < lo) lo = row[j];
+      u[i] = lo;
+    }
+
+  int64_t phases = 0, dual_steps = 0, rows_scanned = 0;
+  for (int32_t phase = 0;; ++phase) {
+    int32_t tail = 0;
+    for (int32_t i = 0; i < n; ++i)
+      if (match_row[i] < 0) {
+        list[tail++] = i;
+        w[i] = u[i];
+        root_row[i] = i;
+      }
+    if (tail == 0) break;
+    const int32_t nroots = tail;
+    for (int32_t j = 0; j < n; ++j) { key[j] = UINT64_MAX; rcol[j] = 0; }
+    int64_t D = 0;
+    int32_t head = 0, nfound = 0;
+    int first = (phase == 0 && seed == 1);
+    for (;;) {
+      /* relax rows reached last round */
+      for (int32_t r = head; r < tail; ++r) {
+        const int32_t i = list[r];
+        const int32_t* row = C + (size_t)i * n;
+        for (int32_t j = 0; j < n; ++j) {
+          const uint64_t k = pack_key((int64_t)row[j] - w[i], i);
+          if (k < key[j]) key[j] = k;
+        }
+      }
+      rows_scanned += tail - head;
+      head = tail;
+      if (first) { /* column reduction is the first relax (hungarian.cpp:328-333) */
+        for (int32_t j = 0; j < n; ++j) v[j] = key_val(key[j]);
+        first = 0;
+      }
+      int64_t m = INT64_MAX;
+      for (int32_t j = 0; j < n; ++j)
+        if (!rcol[j]) {
+          const int64_t s = key_val(key[j]) - v[j];
+          if (s < m) m = s;
+        }
+      if (m == INT64_MAX) {
+        if (nfound) break; /* every column absorbed */
+        rc = -2;
+        goto done;
+      }
+      if (m > D) {
+        if (nfound) break; /* closure exhausted at this D */
+        if (trace && dual_steps < trace_cap) {
+          trace[2 * dual_steps] = m - D;
+          trace[2 * dual_steps + 1] = tail;
+        }
+        D = m;
+        ++dual_steps;
+      }
+      for (int32_t j = 0; j < n; ++j) {
+        if (rcol[j] || key_val(key[j]) - v[j] != D) continue;
+        rcol[j] = 1;
+        dc[j] = D;
+        const int32_t p = key_row(key[j]);
+        tree_par[j] = p;
+        const int32_t root = root_row[p];
+        const int32_t i2 = match_col[j];
+        if (i2 < 0) {
+          if (claim[root] != phase) {
+            claim[root] = phase;
+            found[nfound++] = j;
+          }
+        } else {
+          w[i2] = u[i2] - D;
+          root_row[i2] = root;
+          list[tail++] = i2;
+        }
+      }
+      if (nfound && (!continue_bfs || head == tail)) break;
+    }
+    /* finalise duals of this phase */
+    for (int32_t r = 0; r < tail; ++r) u[list[r]] = w[list[r]] + D;
+    for (int32_t j = 0; j < n; ++j)
+      if (rcol[j]) v[j] -= D - dc[j];
+    /* flip one parent-pointer path per claimed tree */
+    for (int32_t f = 0; f < nfound; ++f) {
+      int32_t j = found[f];
+      for (;;) {
+        const int32_t i = tree_par[j];
+        const int32_t nxt = match_row[i];
+        match_row[i] = j;
+        match_col[j] = i;
+        if (nxt < 0) break;
+        j = nxt;
+      }
+    }
+    (void)nroots;
+    ++phases;
+  }
+  int64_t tot = 0;
+  for (int32_t i = 0; i < n; ++i) tot += C[(size_t)i * n + match_row[i]];
+  *total_cost = tot;
+  *phases_out = phases;
+  *dual_steps_out = dual_steps;
+  if (rows_scanned_out) *rows_scanned_out = rows_scanned;
+done:
+  free(match_col); free(key); free(w); free(dc); free(rcol); free(tree_par);
+  free(root_row); free(claim); free(list); free(found);
+  return rc;
+}

@@ -1,0 +1,291 @@
+"""Python host mirror of the reference's solver entry points over the C ABI.
+
+``solve_km`` / ``solve_batched_km`` follow ``ot::solve_km`` (hungarian.cpp:55-136)
+and ``ot::solve_batched_km`` (hungarian.cpp:313-381): cost matrix in; assignment,
+total cost and row/column duals out; the same exceptions with the same
+messages (``ValueError`` standing in for ``std::invalid_argument``).  The C++
+mirror with the reference's exact types is ``include/kmb.hpp``; this module is
+what the tests and ``bench.py`` use.
+
+Every call goes through ``libkmb.so`` (CUDA, sm_100a).  There is no CPU path:
+if the library or a B200 is missing the call raises ``KmbUnavailable``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _build
+
+KMB_SEED_KM = 0
+KMB_SEED_BATCHED = 1
+OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE = 1, 2, 3
+
+# every symbol include/kmb.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
+               "kmb_solve_batch_i32", "kmb_last_error", "kmb_abi_version")
+
+
+class KmbUnavailable(RuntimeError):
+    """The CUDA library or an sm_100 device is missing — no fallback exists."""
+
+
+class KmbError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class Stats(C.Structure):
+    _fields_ = [("phases", C.c_int64), ("dual_steps", C.c_int64), ("rows_scanned", C.c_int64),
+                ("cost_bytes_read", C.c_int64), ("seconds", C.c_double),
+                ("converged", C.c_int32), ("engine", C.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str | None = None):
+    """Load libkmb.so (built in-tree by ``_build.build_lib``).  Fails loudly."""
+    global _lib
+    if _lib is None:
+        path = path or _build.LIB_SO
+        if not os.path.exists(path):
+            raise KmbUnavailable(f"{path} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        lib = C.CDLL(path)
+        vp = C.c_void_p
+        lib.kmb_create.argtypes = [C.c_int, C.POINTER(vp)]
+        lib.kmb_destroy.argtypes = [vp]
+        lib.kmb_destroy.restype = None
+        lib.kmb_set_stream.argtypes = [vp, vp]
+        lib.kmb_set_option.argtypes = [vp, C.c_int, C.c_int64]
+        lib.kmb_solve_i32.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32, C.c_double,
+                                      vp, vp, vp, vp, C.POINTER(Stats)]
+        lib.kmb_solve_batch_i32.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32,
+                                            vp, vp, vp, vp, C.POINTER(Stats)]
+        lib.kmb_last_error.restype = C.c_char_p
+        lib.kmb_abi_version.restype = C.c_int
+        _lib = lib
+    return _lib
+
+
+def _ptr(a) -> int | None:
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):  # torch tensor (host or device)
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+@dataclass
+class Result:
+    """Mirror of ``ot::SolveResult`` (core.hpp:90-98) + DualPotentials + Matching."""
+    row_to_col: object
+    u: object
+    v: object
+    total_cost: object
+    iterations: int = 0
+    exact: bool = True
+    converged: bool = True
+    wall_seconds: float = 0.0
+    stats: dict = field(default_factory=dict)
+
+    @property
+    def objective(self) -> float:
+        return float(self.total_cost)
+
+
+class Solver:
+    """One device context (workspace cached across calls)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        lib = load_library()
+        self._lib = lib
+        h = C.c_void_p()
+        rc = lib.kmb_create(device, C.byref(h))
+        if rc != 0:
+            raise KmbUnavailable(lib.kmb_last_error().decode())
+        self._h = h
+        if stream is not None:
+            self.set_stream(stream)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.kmb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream: int):
+        self._check(self._lib.kmb_set_stream(self._h, C.c_void_p(stream)))
+
+    def set_option(self, option: int, value: int):
+        self._check(self._lib.kmb_set_option(self._h, option, int(value)))
+
+    def _check(self, rc: int):
+        if rc != 0:
+            msg = self._lib.kmb_last_error().decode()
+            if rc > 0:
+                raise KmbError(rc, msg)
+            raise KmbError(rc, msg)
+
+    # -- raw C-ABI calls -------------------------------------------------------
+    def solve_into(self, cost, n: int, ld: int, seed: int, row_to_col, u, v, total_cost,
+                   time_budget_s: float = 0.0, stats: bool = True) -> Stats | None:
+        st = Stats() if stats else None
+        rc = self._lib.kmb_solve_i32(self._h, C.c_void_p(_ptr(cost)), n, ld, seed, time_budget_s,
+                                     C.c_void_p(_ptr(row_to_col)), C.c_void_p(_ptr(u)),
+                                     C.c_void_p(_ptr(v)), C.c_void_p(_ptr(total_cost)),
+                                     C.byref(st) if st is not None else None)
+        self._check(rc)
+        return st
+
+    def solve_batch_into(self, costs, batch: int, n: int, seed: int, row_to_col, u, v,
+                         total_cost, stats: bool = True) -> Stats | None:
+        st = Stats() if stats else None
+        rc = self._lib.kmb_solve_batch_i32(self._h, C.c_void_p(_ptr(costs)), batch, n, seed,
+                                           C.c_void_p(_ptr(row_to_col)), C.c_void_p(_ptr(u)),
+                                           C.c_void_p(_ptr(v)), C.c_void_p(_ptr(total_cost)),
+                                           C.byref(st) if st is not None else None)
+        self._check(rc)
+        return st
+
+    # -- numpy convenience -------------------------------------------------------
+    def solve(self, cost: np.ndarray, seed: int = KMB_SEED_BATCHED,
+              time_budget_s: float = 0.0) -> Result:
+        c = np.ascontiguousarray(cost, dtype=np.int32)
+        if c.ndim != 2 or c.shape[0] != c.shape[1]:
+            raise ValueError("square cost matrix required")
+        n = c.shape[0]
+        r2c = np.full(n, -1, np.int32)
+        u = np.zeros(n, np.int64)
+        v = np.zeros(n, np.int64)
+        tot = np.zeros(1, np.int64)
+        t0 = time.perf_counter()
+        st = self.solve_into(c, n, n, seed, r2c, u, v, tot, time_budget_s)
+        wall = time.perf_counter() - t0
+        return Result(r2c, u, v, int(tot[0]), iterations=int(st.phases + st.dual_steps),
+                      exact=bool(st.converged), converged=bool(st.converged), wall_seconds=wall,
+                      stats=_stats_dict(st))
+
+    def solve_batch(self, costs: np.ndarray, seed: int = KMB_SEED_BATCHED) -> Result:
+        c = np.ascontiguousarray(costs, dtype=np.int32)
+        b, n, n2 = c.shape
+        if n != n2:
+            raise ValueError("square cost matrices required")
+        r2c = np.full((b, n), -1, np.int32)
+        u = np.zeros((b, n), np.int64)
+        v = np.zeros((b, n), np.int64)
+        tot = np.zeros(b, np.int64)
+        t0 = time.perf_counter()
+        st = self.solve_batch_into(c, b, n, seed, r2c, u, v, tot)
+        wall = time.perf_counter() - t0
+        return Result(r2c, u, v, tot, iterations=int(st.phases + st.dual_steps),
+                      wall_seconds=wall, stats=_stats_dict(st))
+
+
+def _stats_dict(st: Stats) -> dict:
+    return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+
+_default: Solver | None = None
+
+
+def default_solver() -> Solver:
+    global _default
+    if _default is None:
+        _default = Solver(0)
+    return _default
+
+
+# ---- reference-shaped entry points ------------------------------------------------
+
+def _validate(cost, supplies, demands, who: str) -> np.ndarray:
+    """require_unit_square (hungarian.cpp:15-21) + validate_instance (core.cpp:30-55)
+    for the assignment case, with the reference's messages."""
+    c = np.asarray(cost)
+    if c.ndim != 2 or c.shape[0] <= 0 or c.shape[1] <= 0:
+        raise ValueError(f"{who}: dimensions must be positive")
+    n, m = c.shape
+    if supplies is not None and len(supplies) != n:
+        raise ValueError(f"{who}: supplies size does not match n")
+    if demands is not None and len(demands) != m:
+        raise ValueError(f"{who}: demands size does not match m")
+    if (supplies is not None and any(s <= 0 for s in supplies)):
+        raise ValueError(f"{who}: supplies must be positive")
+    if (demands is not None and any(d <= 0 for d in demands)):
+        raise ValueError(f"{who}: demands must be positive")
+    if supplies is not None and demands is not None and sum(supplies) != sum(demands):
+        raise ValueError(f"{who}: total supply does not equal total demand")
+    unit = n == m and (supplies is None or all(s == 1 for s in supplies)) and \
+        (demands is None or all(d == 1 for d in demands))
+    if not unit:
+        raise ValueError(f"{who}: requires a unit-capacity square instance")
+    return c
+
+
+def quantize_costs(cost, B: int):
+    """``ot::quantize_costs`` (hungarian.cpp:33-53): chat = floor(C*B/N)."""
+    if B <= 0:
+        raise ValueError("quantize_costs: B must be positive")
+    c = np.asarray(cost, dtype=np.int64)
+    N = int(c.max()) if c.size else 0
+    if N <= 0:
+        return c.copy(), 1, True
+    if B > (2**63 - 1) // N:
+        raise ValueError("quantize_costs: B * max cost overflows")
+    scaled = c * np.int64(B)
+    chat = scaled // np.int64(N)
+    return chat, N, bool(np.array_equal(chat * N, scaled))
+
+
+def solve_km(cost, supplies=None, demands=None, time_budget_s: float = 0.0,
+             solver: Solver | None = None) -> Result:
+    """Exact KM from u = v = 0; duals identical to ``ot::solve_km``."""
+    c = _validate(cost, supplies, demands, "solve_km")
+    if (c < 0).any():
+        raise ValueError("solve_km: costs must be nonnegative")
+    if c.max() >= 2**30:
+        _range_error("solve_km")
+    s = solver or default_solver()
+    r = s.solve(c.astype(np.int32, copy=False), KMB_SEED_KM, time_budget_s)
+    r.iterations = c.shape[0]  # hungarian.cpp:130: iterations = n
+    return r
+
+
+def solve_batched_km(cost, B: int | None = None, supplies=None, demands=None,
+                     time_budget_s: float = 0.0, solver: Solver | None = None,
+                     return_quantized: bool = False):
+    """``ot::solve_batched_km`` on chat = quantize_costs(cost, B); ``B=None`` is the
+    lossless B = N.  ``exact`` = lossless and converged (hungarian.cpp:374-376);
+    the total cost and objective are reported against the true costs."""
+    c = _validate(cost, supplies, demands, "solve_batched_km")
+    if (c < 0).any():
+        raise ValueError("solve_batched_km: costs must be nonnegative")
+    c64 = np.asarray(c, dtype=np.int64)
+    if B is None:
+        B = max(int(c64.max()), 1)
+    chat, N, lossless = quantize_costs(c64, int(B))
+    if chat.size and chat.max() >= 2**30:
+        _range_error("solve_batched_km")
+    s = solver or default_solver()
+    r = s.solve(chat.astype(np.int32), KMB_SEED_BATCHED, time_budget_s)
+    r.exact = bool(lossless and r.converged)
+    rows = np.arange(c64.shape[0])
+    ok = r.row_to_col >= 0
+    r.total_cost = int(c64[rows[ok], r.row_to_col[ok]].sum())
+    if return_quantized:
+        return r, (chat, int(B), N, lossless)
+    return r
+
+
+def _range_error(who: str):
+    raise ValueError(f"{who}: cost exceeds the device range [0, 2^30)")

@@ -1,0 +1,361 @@
+// C ABI of include/kmb.h: context, device workspace, engine selection, host <->
+// device staging.  Host code only; the kernels live in kmb_solver.cu (grid
+// engine) and kmb_batch.cu (SMEM engine).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "kmb.h"
+#include "kmb_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(KMB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define KMB_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t e__ = (call);                           \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct kmb_context {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t max_ctas = 0;
+  int continue_bfs = 0;
+  int engine = 0;
+  // grid-engine workspace
+  DevBuf cost, u, v, mrow, mcol, tpar, root, claim, lrow0, lrow1, lw0, lw1, found, partial,
+      ctrl, obj;
+  // batch workspace
+  DevBuf bcost, br2c, bu, bv, btot, bstat, bstatus;
+};
+
+extern "C" {
+
+const char* kmb_last_error(void) { return g_err.c_str(); }
+int kmb_abi_version(void) { return KMB_ABI_VERSION; }
+
+int kmb_create(int device, kmb_context** out) {
+  if (!out) return fail(KMB_EINVAL, "kmb_create: out is NULL");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count <= device || device < 0)
+    return fail(KMB_ENODEVICE, std::string("kmb_create: no CUDA device ") + std::to_string(device) +
+                                   (e != cudaSuccess ? std::string(" (") + cudaGetErrorString(e) + ")"
+                                                     : std::string()));
+  cudaDeviceProp prop;
+  KMB_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(KMB_ENODEVICE, std::string("kmb_create: device is sm_") + std::to_string(prop.major) +
+                                   std::to_string(prop.minor) + ", this build targets sm_100a");
+  KMB_CUDA(cudaSetDevice(device));
+  kmb_context* c = new kmb_context();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  cudaEventCreate(&c->ev0);
+  cudaEventCreate(&c->ev1);
+  *out = c;
+  return KMB_OK;
+}
+
+void kmb_destroy(kmb_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
+                    &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
+                    &c->obj, &c->bcost, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
+                    &c->bstatus})
+    b->release();
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  delete c;
+}
+
+int kmb_set_stream(kmb_context* c, void* s) {
+  if (!c) return fail(KMB_EINVAL, "kmb_set_stream: NULL context");
+  c->stream = static_cast<cudaStream_t>(s);
+  return KMB_OK;
+}
+
+int kmb_set_option(kmb_context* c, int option, int64_t value) {
+  if (!c) return fail(KMB_EINVAL, "kmb_set_option: NULL context");
+  switch (option) {
+    case KMB_OPT_MAX_CTAS: c->max_ctas = value; return KMB_OK;
+    case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
+    case KMB_OPT_ENGINE:
+      if (value < 0 || value > 2) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0, 1 or 2");
+      c->engine = static_cast<int>(value);
+      return KMB_OK;
+    default: return fail(KMB_EINVAL, "kmb_set_option: unknown option");
+  }
+}
+
+static int copy_out(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!dst || bytes == 0) return KMB_OK;
+  KMB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+  return KMB_OK;
+}
+
+static int status_message(int status, const char* who) {
+  if (status == KMB_ENEGATIVE) return fail(status, std::string(who) + ": costs must be nonnegative");
+  if (status == KMB_ERANGE)
+    return fail(status, std::string(who) + ": cost exceeds the device range [0, 2^30)");
+  return fail(KMB_EINTERNAL, std::string(who) + ": engine invariant violated (status " +
+                                 std::to_string(status) + ")");
+}
+
+static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch, int32_t n,
+                            int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
+                            int64_t* total_cost, kmb_stats* stats, const char* who) {
+  cudaStream_t st = c->stream;
+  const size_t cbytes = static_cast<size_t>(batch) * n * n * sizeof(int32_t);
+  const int32_t* dcost = costs;
+  if (!is_device_ptr(costs)) {
+    KMB_CUDA(c->bcost.ensure(cbytes));
+    KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
+    dcost = c->bcost.as<int32_t>();
+  }
+  const size_t nb = static_cast<size_t>(batch) * n;
+  int32_t* dr2c = row_to_col;
+  int64_t *du = u, *dv = v, *dtot = total_cost;
+  if (!is_device_ptr(row_to_col)) { KMB_CUDA(c->br2c.ensure(nb * 4)); dr2c = c->br2c.as<int32_t>(); }
+  if (!is_device_ptr(u)) { KMB_CUDA(c->bu.ensure(nb * 8)); du = c->bu.as<int64_t>(); }
+  if (!is_device_ptr(v)) { KMB_CUDA(c->bv.ensure(nb * 8)); dv = c->bv.as<int64_t>(); }
+  if (!is_device_ptr(total_cost)) { KMB_CUDA(c->btot.ensure(batch * 8)); dtot = c->btot.as<int64_t>(); }
+  KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * 3 * 8));
+  KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
+  kmb::BatchArgs a{};
+  a.C = dcost;
+  a.batch = batch;
+  a.n = n;
+  a.seed = seed;
+  a.continue_bfs = c->continue_bfs;
+  a.row_to_col = dr2c;
+  a.u = du;
+  a.v = dv;
+  a.total_cost = dtot;
+  a.stats = c->bstat.as<int64_t>();
+  a.status = c->bstatus.as<int32_t>();
+  KMB_CUDA(cudaEventRecord(c->ev0, st));
+  int grid = 0;
+  KMB_CUDA(kmb::launch_batch(a, c->sm_count, st, &grid));
+  KMB_CUDA(cudaEventRecord(c->ev1, st));
+  if (dr2c != row_to_col) { int r = copy_out(row_to_col, dr2c, nb * 4, st); if (r) return r; }
+  if (du != u) { int r = copy_out(u, du, nb * 8, st); if (r) return r; }
+  if (dv != v) { int r = copy_out(v, dv, nb * 8, st); if (r) return r; }
+  if (dtot != total_cost) { int r = copy_out(total_cost, dtot, batch * 8, st); if (r) return r; }
+  // status is always checked (one small copy): invalid input must not pass silently
+  int32_t* hstatus = new int32_t[batch];
+  int64_t* hstat = stats ? new int64_t[static_cast<size_t>(batch) * 3] : nullptr;
+  cudaError_t e = cudaMemcpyAsync(hstatus, c->bstatus.p, batch * 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && hstat)
+    e = cudaMemcpyAsync(hstat, c->bstat.p, static_cast<size_t>(batch) * 24, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    delete[] hstatus;
+    delete[] hstat;
+    return cuda_fail(e, who);
+  }
+  int bad = 0;
+  for (int32_t b = 0; b < batch && !bad; ++b) bad = hstatus[b];
+  delete[] hstatus;
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    for (int32_t b = 0; b < batch; ++b) {
+      stats->phases += hstat[3 * b];
+      stats->dual_steps += hstat[3 * b + 1];
+      stats->rows_scanned += hstat[3 * b + 2];
+    }
+    stats->cost_bytes_read = static_cast<int64_t>(batch) * n * n * 4;  // HBM: each matrix once
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    stats->seconds = ms * 1e-3;
+    stats->converged = 1;
+    stats->engine = 2;
+  }
+  delete[] hstat;
+  if (bad) return status_message(bad, who);
+  return KMB_OK;
+}
+
+int kmb_solve_batch_i32(kmb_context* c, const int32_t* costs, int32_t batch, int32_t n,
+                        int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
+                        int64_t* total_cost, kmb_stats* stats) {
+  const char* who = "kmb_solve_batch_i32";
+  if (!c) return fail(KMB_EINVAL, "kmb_solve_batch_i32: NULL context");
+  if (batch <= 0 || n <= 0) return fail(KMB_EINVAL, "kmb_solve_batch_i32: dimensions must be positive");
+  if (!costs) return fail(KMB_EINVAL, "kmb_solve_batch_i32: costs is NULL");
+  if (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED) return fail(KMB_EINVAL, "kmb_solve_batch_i32: bad seed");
+  if (n > kmb::batch_max_n())
+    return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > " + std::to_string(kmb::batch_max_n()) +
+                                " (use kmb_solve_i32 per instance)");
+  KMB_CUDA(cudaSetDevice(c->device));
+  return solve_batch_impl(c, costs, batch, n, seed, row_to_col, u, v, total_cost, stats, who);
+}
+
+int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, int32_t seed,
+                  double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
+                  int64_t* total_cost, kmb_stats* stats) {
+  const char* who = "kmb_solve_i32";
+  if (!c) return fail(KMB_EINVAL, "kmb_solve_i32: NULL context");
+  if (n <= 0) return fail(KMB_EINVAL, "kmb_solve_i32: dimensions must be positive");
+  if (!cost) return fail(KMB_EINVAL, "kmb_solve_i32: cost is NULL");
+  if (ld < n) return fail(KMB_EINVAL, "kmb_solve_i32: ld < n");
+  if (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED) return fail(KMB_EINVAL, "kmb_solve_i32: bad seed");
+  KMB_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+
+  int engine = c->engine;
+  if (engine == 0) engine = (n <= 128 && time_budget_s <= 0.0) ? 2 : 1;
+  if (engine == 2 && n > kmb::batch_max_n()) engine = 1;
+  if (engine == 2) {
+    if (time_budget_s > 0.0)
+      return fail(KMB_EINVAL, "kmb_solve_i32: the SMEM engine has no time budget; use engine 1");
+    const int32_t* src = cost;
+    if (ld != n) {  // compact into the batch buffer
+      KMB_CUDA(c->bcost.ensure(static_cast<size_t>(n) * n * 4));
+      KMB_CUDA(cudaMemcpy2DAsync(c->bcost.p, n * 4, cost, ld * 4, n * 4, n, cudaMemcpyDefault, st));
+      src = c->bcost.as<int32_t>();
+    }
+    return solve_batch_impl(c, src, 1, n, seed, row_to_col, u, v, total_cost, stats, who);
+  }
+
+  // ---- grid engine: choose the slab width W (power of two) and CTA count G ----
+  int64_t maxg = c->max_ctas > 0 ? c->max_ctas : c->sm_count;
+  if (maxg > c->sm_count) maxg = c->sm_count;  // cooperative: one CTA per SM
+  int W = 4;
+  while ((n + W - 1) / W > maxg) W <<= 1;
+  const int G = (n + W - 1) / W;
+  const int64_t pitch = static_cast<int64_t>(G) * W;
+  const size_t nn = static_cast<size_t>(n);
+
+  const int32_t* dC = cost;
+  const bool dev_in = is_device_ptr(cost);
+  const bool aligned = (reinterpret_cast<uintptr_t>(cost) & 15) == 0;
+  if (!(dev_in && aligned && ld == pitch)) {
+    KMB_CUDA(c->cost.ensure(nn * pitch * 4));
+    KMB_CUDA(cudaMemcpy2DAsync(c->cost.p, pitch * 4, cost, ld * 4, nn * 4, nn, cudaMemcpyDefault, st));
+    dC = c->cost.as<int32_t>();
+  }
+  KMB_CUDA(c->u.ensure(nn * 8));
+  KMB_CUDA(c->v.ensure(nn * 8));
+  KMB_CUDA(c->mrow.ensure(nn * 4));
+  KMB_CUDA(c->mcol.ensure(nn * 4));
+  KMB_CUDA(c->tpar.ensure(nn * 4));
+  KMB_CUDA(c->root.ensure(nn * 4));
+  KMB_CUDA(c->claim.ensure(nn * 8));
+  KMB_CUDA(c->lrow0.ensure(nn * 4));
+  KMB_CUDA(c->lrow1.ensure(nn * 4));
+  KMB_CUDA(c->lw0.ensure(nn * 8));
+  KMB_CUDA(c->lw1.ensure(nn * 8));
+  KMB_CUDA(c->found.ensure(nn * 4));
+  KMB_CUDA(c->partial.ensure(static_cast<size_t>(G) * 8));
+  KMB_CUDA(c->ctrl.ensure(sizeof(kmb::Ctrl)));
+  KMB_CUDA(c->obj.ensure(8));
+
+  kmb::SolverArgs a{};
+  a.C = dC;
+  a.pitch = pitch;
+  a.n = n;
+  a.W = W;
+  a.seed = seed;
+  a.continue_bfs = c->continue_bfs;
+  a.u = c->u.as<int64_t>();
+  a.v = c->v.as<int64_t>();
+  a.match_row = c->mrow.as<int32_t>();
+  a.match_col = c->mcol.as<int32_t>();
+  a.tree_par = c->tpar.as<int32_t>();
+  a.root_row = c->root.as<int32_t>();
+  a.claim = c->claim.as<uint64_t>();
+  a.list_row[0] = c->lrow0.as<int32_t>();
+  a.list_row[1] = c->lrow1.as<int32_t>();
+  a.list_w[0] = c->lw0.as<int64_t>();
+  a.list_w[1] = c->lw1.as<int64_t>();
+  a.found = c->found.as<int32_t>();
+  a.partial = c->partial.as<int64_t>();
+  a.ctrl = c->ctrl.as<kmb::Ctrl>();
+  a.deadline_ns = 0;
+  if (time_budget_s > 0.0) {
+    // relative budget (top bit set): the kernel adds it to its own %globaltimer
+    a.deadline_ns = (1ull << 63) | static_cast<unsigned long long>(time_budget_s * 1e9);
+  }
+  KMB_CUDA(cudaMemsetAsync(c->ctrl.p, 0, sizeof(kmb::Ctrl), st));
+  KMB_CUDA(cudaEventRecord(c->ev0, st));
+  KMB_CUDA(kmb::launch_solver(a, G, st));
+  KMB_CUDA(kmb::launch_objective(dC, pitch, n, a.match_row, c->obj.as<unsigned long long>(), st));
+  KMB_CUDA(cudaEventRecord(c->ev1, st));
+  int r;
+  if ((r = copy_out(row_to_col, a.match_row, nn * 4, st))) return r;
+  if ((r = copy_out(u, a.u, nn * 8, st))) return r;
+  if ((r = copy_out(v, a.v, nn * 8, st))) return r;
+  if ((r = copy_out(total_cost, c->obj.p, 8, st))) return r;
+  kmb::Ctrl h;
+  KMB_CUDA(cudaMemcpyAsync(&h, c->ctrl.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  KMB_CUDA(cudaStreamSynchronize(st));
+  if (h.status != 0) return status_message(h.status, who);
+  if (stats) {
+    stats->phases = h.phases;
+    stats->dual_steps = h.dual_steps;
+    stats->rows_scanned = h.rows_scanned;
+    stats->cost_bytes_read = 4ll * n * (h.rows_scanned + (seed == KMB_SEED_BATCHED ? n : 0));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    stats->seconds = ms * 1e-3;
+    stats->converged = h.free_rows == 0 ? 1 : 0;
+    stats->engine = 1;
+  }
+  return KMB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// Internal (non-ABI) declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace kmb {
+
+// Device control block of one single-instance solve.  Counters that are
+// recycled between phases are double-buffered by phase parity (see k_solve).
+struct Ctrl {
+  unsigned long long bar_counter;  // grid barrier (monotone)
+  int32_t tail[2];                 // row-list lengths
+  int32_t nfound[2];               // free columns absorbed this phase
+  int32_t status;                  // 0 ok, <0 internal error
+  int32_t stop;                    // time budget expired
+  int32_t free_rows;               // unmatched rows when the engine stopped
+  int32_t pad_;
+  int64_t phases;
+  int64_t dual_steps;
+  int64_t rows_scanned;
+};
+
+struct SolverArgs {
+  const int32_t* C;  // n x pitch, row-major, 16 B aligned, pitch % 4 == 0
+  int64_t pitch;
+  int32_t n;
+  int32_t W;          // column slab per CTA (power of two >= 4); G*W >= n
+  int32_t seed;       // 0: u = v = 0 (solve_km), 1: reductions (solve_batched_km)
+  int32_t continue_bfs;
+  unsigned long long deadline_ns;  // %globaltimer deadline, 0 = none
+  int64_t* u;
+  int64_t* v;
+  int32_t* match_row;
+  int32_t* match_col;
+  int32_t* tree_par;   // per column
+  int32_t* root_row;   // per row
+  uint64_t* claim;     // per row, claim_key(phase, col)
+  int32_t* list_row[2];
+  int64_t* list_w[2];
+  int32_t* found;
+  int64_t* partial;    // per CTA
+  Ctrl* ctrl;
+};
+
+cudaError_t launch_solver(const SolverArgs& a, int G, cudaStream_t st);
+cudaError_t launch_objective(const int32_t* C, int64_t pitch, int n, const int32_t* match_row,
+                             unsigned long long* out, cudaStream_t st);
+size_t solver_smem_bytes(int W);
+int solver_threads();
+
+// ---- batched small instances (one CTA per instance, cost matrix in SMEM) ----
+struct BatchArgs {
+  const int32_t* C;      // batch x n x n (contiguous instances)
+  int32_t batch;
+  int32_t n;
+  int32_t seed;
+  int32_t continue_bfs;
+  int32_t* row_to_col;   // batch x n
+  int64_t* u;            // batch x n
+  int64_t* v;            // batch x n
+  int64_t* total_cost;   // batch
+  int64_t* stats;        // batch x 3: phases, dual_steps, rows_scanned (may be null)
+  int32_t* status;       // batch (0 ok)
+};
+
+int batch_max_n();
+cudaError_t launch_batch(const BatchArgs& a, int sm_count, cudaStream_t st, int* grid_out);
+
+}  // namespace kmb

@@ -1,0 +1,395 @@
+// Single-instance exact KM / batched-KM engine for sm_100a: one persistent
+// kernel, G column-slab CTAs, software grid barriers, all state on device.
+//
+// Reference path replaced: ot::solve_batched_km (hungarian.cpp:313-381) and,
+// with seed 0, ot::solve_km (hungarian.cpp:55-136).  The engine keeps the three
+// rules that make the reference's final duals canonical:
+// same starting duals; a dual step only when the tight closure of the free rows
+// holds no free column; the step over the full closure with delta = min slack.
+// How it gets there differs from the reference:
+//
+//  * Lazy duals.  Within a phase D is the accumulated dual shift; row i reached
+//    at shift Dr stores w_i = u_i - Dr, so a column's slack' = min_i (C_ij - w_i)
+//    - v_j never changes under a dual step and column j is tight iff slack' == D.
+//    A dual step is therefore D = min unreached slack' — no O(n) update — and
+//    the duals are finalised once per phase (u_i = w_i + D, v_j -= D - Dc_j).
+//  * Relax = reduced-cost scan (hungarian.cpp:164-172).  CTA b owns columns
+//    [b*W, b*W+W) of every row; each round it streams the W-wide slab of every
+//    newly reached row with 128-bit no-allocate loads and folds them into
+//    per-column packed (value, row) keys (kmb_common.cuh): min and argmin
+//    parent in one unsigned min, reduced by warp shuffles then shared atomics.
+//  * Min-slack (hungarian.cpp:203-206): block reduce -> one partial per CTA ->
+//    every CTA reads all partials after the grid barrier (no second pass).
+//  * Absorb (hungarian.cpp:186-199): zero-slack unreached columns of the slab
+//    are reached; their matched rows are appended (warp-aggregated atomics) to
+//    the phase's row list; free columns are recorded and claim their tree root.
+//  * Augment: instead of the reference's per-phase full tight-graph rebuild
+//    (TightPhase, hungarian.cpp:233-252, 55-80% of its CPU time) the search's
+//    own argmin parents form an alternating forest of tight edges rooted at the
+//    free rows; every tree that reached a free column flips the path of its
+//    smallest such column.  Paths of distinct trees are vertex-disjoint.
+//
+// One round = relax | barrier | min + absorb | barrier.  A phase ends after
+// the round that absorbs a free column (or, with continue_bfs, when the tight
+// closure at the current D is exhausted), then finalises duals, flips paths and
+// lists the next phase's free rows behind one more barrier.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kmb_common.cuh"
+#include "kmb_internal.h"
+
+namespace kmb {
+
+constexpr int kThreads = 512;
+
+struct SlabSmem {
+  int64_t part[kThreads / 32];
+  int64_t m;
+  int32_t append_base;
+};
+
+// ---- K1: row reductions + engine state init (hungarian.cpp:323-327) -------
+// One warp per row, 128-bit loads; also seeds the phase-0 row list.
+__global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < a.n; i += nwarps) {
+    // one pass per row: validation (core.cpp:144-145 + the device range) and,
+    // for seed 1, the row minimum
+    const int32_t* row = a.C + static_cast<int64_t>(i) * a.pitch;
+    int32_t lo = 0x7fffffff, hi = 0;
+    const int n4 = a.n >> 2;
+    const int4* row4 = reinterpret_cast<const int4*>(row);
+    for (int q = lane; q < n4; q += 32) {
+      const int4 c = ld_stream(row4 + q);
+      lo = min(lo, min(min(c.x, c.y), min(c.z, c.w)));
+      hi = max(hi, max(max(c.x, c.y), max(c.z, c.w)));
+    }
+    for (int j = (n4 << 2) + lane; j < a.n; j += 32) {
+      lo = min(lo, row[j]);
+      hi = max(hi, row[j]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int64_t u0 = a.seed == 1 ? lo : 0;
+    if (lane == 0) {
+      if (lo < 0) atomicMax(&a.ctrl->status, 2);               // KMB_ENEGATIVE
+      else if (hi >= (1 << 30)) atomicMax(&a.ctrl->status, 3);  // KMB_ERANGE
+      a.u[i] = u0;
+      a.list_row[0][i] = i;
+      a.list_w[0][i] = u0;
+      a.root_row[i] = i;
+      a.claim[i] = KMB_KEY_INF;
+      a.match_row[i] = -1;
+      a.match_col[i] = -1;
+    }
+  }
+  // the rest of Ctrl was zeroed by the host (cudaMemsetAsync) before launch
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->tail[0] = a.n;
+}
+
+// ---- K3: reduced-cost scan of rows list[head, tail) over one column slab ----
+// Thread (g, s): segment s = 4 consecutive columns, row group g.  W = 4*S is a
+// power of two, so lanes sharing a segment differ only in their high lane bits
+// (S < 32) and a xor-shuffle tree merges them before the shared atomics.
+__device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* list,
+                                           const int64_t* listw, int head, int tail,
+                                           int c0, int W, uint64_t* skey) {
+  const int S = W >> 2;
+  const int R = kThreads / S > 0 ? kThreads / S : 1;
+  const int tid = threadIdx.x;
+  const int Sreal = S < kThreads ? S : kThreads;
+  const int lane = tid & 31;
+  for (int sbase = 0; sbase < S; sbase += Sreal) {
+    const int s = sbase + (tid % Sreal);
+    const int g = tid / Sreal;
+    uint64_t best0 = KMB_KEY_INF, best1 = KMB_KEY_INF, best2 = KMB_KEY_INF, best3 = KMB_KEY_INF;
+    if (g < R) {
+      const int32_t* base = a.C + c0 + 4 * s;
+      int r = head + g;
+      // 4 rows in flight per thread
+      for (; r + 3 * R < tail; r += 4 * R) {
+        int i[4];
+        uint32_t b[4];
+        int4 c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          i[k] = ldcg(list + r + k * R);
+          b[k] = row_bias(ldcg(listw + r + k * R));
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          c[k] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[k]) * a.pitch));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          best0 = umin64(best0, pack_key(static_cast<uint32_t>(c[k].x) + b[k], i[k]));
+          best1 = umin64(best1, pack_key(static_cast<uint32_t>(c[k].y) + b[k], i[k]));
+          best2 = umin64(best2, pack_key(static_cast<uint32_t>(c[k].z) + b[k], i[k]));
+          best3 = umin64(best3, pack_key(static_cast<uint32_t>(c[k].w) + b[k], i[k]));
+        }
+      }
+      for (; r < tail; r += R) {
+        const int i = ldcg(list + r);
+        const uint32_t b = row_bias(ldcg(listw + r));
+        const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * a.pitch));
+        best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
+        best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
+        best2 = umin64(best2, pack_key(static_cast<uint32_t>(c.z) + b, i));
+        best3 = umin64(best3, pack_key(static_cast<uint32_t>(c.w) + b, i));
+      }
+    }
+    // merge lanes of the same segment inside the warp
+    if (Sreal < 32) {
+      for (int o = Sreal; o < 32; o <<= 1) {
+        best0 = umin64(best0, __shfl_xor_sync(0xffffffffu, best0, o));
+        best1 = umin64(best1, __shfl_xor_sync(0xffffffffu, best1, o));
+        best2 = umin64(best2, __shfl_xor_sync(0xffffffffu, best2, o));
+        best3 = umin64(best3, __shfl_xor_sync(0xffffffffu, best3, o));
+      }
+    }
+    const bool writer = (g < R) && (Sreal >= 32 || lane < Sreal);
+    if (writer && best0 != KMB_KEY_INF) {
+      unsigned long long* k4 = reinterpret_cast<unsigned long long*>(skey + 4 * s);
+      atomicMin(k4 + 0, best0);
+      atomicMin(k4 + 1, best1);
+      atomicMin(k4 + 2, best2);
+      atomicMin(k4 + 3, best3);
+    }
+  }
+}
+
+// ---- the persistent engine ---------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  const int W = a.W;
+  uint64_t* skey = reinterpret_cast<uint64_t*>(dyn);
+  int64_t* vloc = reinterpret_cast<int64_t*>(skey + W);
+  int64_t* dcol = vloc + W;
+  unsigned char* rch = reinterpret_cast<unsigned char*>(dcol + W);
+  __shared__ SlabSmem sm;
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = gridDim.x;
+  const int c0 = blockIdx.x * W;
+  const bool leader = (blockIdx.x == 0 && tid == 0);
+  GridBarrier bar{&a.ctrl->bar_counter, 0ull, static_cast<unsigned>(G)};
+  Ctrl* ctrl = a.ctrl;
+
+  if (ldcg(&ctrl->status) != 0) return;  // invalid input (k_init_rows), all CTAs agree
+  for (int c = tid; c < W; c += kThreads) vloc[c] = 0;  // seed 0: v = 0
+  int64_t dual_steps = 0, rows_scanned = 0;
+  unsigned long long deadline = a.deadline_ns;
+  if (deadline >> 63) deadline = globaltimer_ns() + (deadline & ~(1ull << 63));  // relative budget
+
+  for (int phase = 0;; ++phase) {
+    const int p = phase & 1;
+    const int nroots = ldcg(&ctrl->tail[p]);
+    if (nroots == 0 || ldcg(&ctrl->stop) != 0) {
+      if (leader) ctrl->free_rows = nroots;
+      break;
+    }
+    const int32_t* list = a.list_row[p];
+    const int64_t* listw = a.list_w[p];
+    for (int c = tid; c < W; c += kThreads) {
+      skey[c] = KMB_KEY_INF;
+      rch[c] = (c0 + c < a.n) ? 0 : 1;  // padding columns never count
+    }
+    __syncthreads();
+
+    int64_t D = 0;
+    int head = 0, tail = nroots, nfound = 0;
+    bool fatal = false;  // identical in every CTA (all see the same m)
+    for (int round = 0;; ++round) {
+      relax_slab(a, list, listw, head, tail, c0, W, skey);
+      rows_scanned += tail - head;
+      __syncthreads();
+      if (phase == 0 && round == 0 && a.seed == 1)  // column reduction, hungarian.cpp:328-333
+        for (int c = tid; c < W; c += kThreads)
+          if (c0 + c < a.n) vloc[c] = key_val(skey[c]);
+      // local min of unreached slack'
+      int64_t lm = KMB_I64_INF;
+      for (int c = tid; c < W; c += kThreads)
+        if (!rch[c]) {
+          const int64_t s = key_val(skey[c]) - vloc[c];
+          lm = s < lm ? s : lm;
+        }
+      lm = warp_min_i64(lm);
+      if (lane == 0) sm.part[wid] = lm;
+      __syncthreads();
+      if (wid == 0) {
+        int64_t x = lane < kThreads / 32 ? sm.part[lane] : KMB_I64_INF;
+        x = warp_min_i64(x);
+        if (lane == 0) a.partial[blockIdx.x] = x;
+      }
+      bar.sync();  // ---------------------------------------------- B1
+      if (round == 0 && leader) {  // recycle the previous phase's counters
+        ctrl->tail[p ^ 1] = 0;
+        ctrl->nfound[p ^ 1] = 0;
+      }
+      if (wid == 0) {
+        int64_t x = KMB_I64_INF;
+        for (int b = lane; b < G; b += 32) {
+          const int64_t y = ldcg(a.partial + b);
+          x = y < x ? y : x;
+        }
+        x = warp_min_i64(x);
+        if (lane == 0) sm.m = x;
+      }
+      __syncthreads();
+      const int64_t m = sm.m;
+      if (m > D) {
+        if (nfound > 0) break;  // closure exhausted at this D (continue_bfs)
+        if (m == KMB_I64_INF) {  // no unreached column: cannot happen on valid input
+          if (leader) ctrl->status = -2;
+          fatal = true;
+          break;
+        }
+        D = m;  // dual step: no tight unreached column, no pending row
+        ++dual_steps;
+      }
+      // absorb zero-slack columns of the slab
+      for (int cb = 0; cb < W; cb += kThreads) {
+        const int c = cb + tid;
+        bool newrow = false, newfree = false;
+        int32_t i2 = -1, col = c0 + c;
+        int64_t w2 = 0;
+        int32_t root = 0;
+        if (c < W && !rch[c] && key_val(skey[c]) - vloc[c] == D) {
+          rch[c] = 1;
+          dcol[c] = D;
+          const int32_t par = key_row(skey[c]);
+          a.tree_par[col] = par;
+          root = ldcg(a.root_row + par);
+          i2 = ldcg(a.match_col + col);
+          if (i2 < 0) {
+            newfree = true;
+            atomicMin(reinterpret_cast<unsigned long long*>(a.claim + root), claim_key(phase, col));
+          } else {
+            newrow = true;
+            w2 = ldcg(a.u + i2) - D;
+            a.root_row[i2] = root;
+          }
+        }
+        // warp-aggregated appends
+        const unsigned rowmask = __ballot_sync(0xffffffffu, newrow);
+        if (rowmask) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&ctrl->tail[p], __popc(rowmask));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (newrow) {
+            const int pos = base + __popc(rowmask & ((1u << lane) - 1));
+            a.list_row[p][pos] = i2;
+            a.list_w[p][pos] = w2;
+          }
+        }
+        const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
+        if (fmask) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&ctrl->nfound[p], __popc(fmask));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (newfree) a.found[base + __popc(fmask & ((1u << lane) - 1))] = col;
+        }
+      }
+      bar.sync();  // ---------------------------------------------- B2
+      head = tail;
+      tail = ldcg(&ctrl->tail[p]);
+      nfound = ldcg(&ctrl->nfound[p]);
+      if (nfound > 0 && (!a.continue_bfs || head == tail)) break;
+    }
+    if (fatal) break;
+
+    // ---- end of phase: finalise duals, flip paths, list next free rows -------
+    const int gtid = blockIdx.x * kThreads + tid;
+    const int gthreads = G * kThreads;
+    for (int r = gtid; r < tail; r += gthreads) {
+      const int32_t i = ldcg(list + r);
+      const int64_t un = ldcg(listw + r) + D;
+      a.u[i] = un;
+      if (r < nroots && !claimed_in(ldcg(a.claim + i), phase)) {  // still free
+        const int pos = atomicAdd(&ctrl->tail[p ^ 1], 1);
+        a.list_row[p ^ 1][pos] = i;
+        a.list_w[p ^ 1][pos] = un;
+        a.root_row[i] = i;
+      }
+    }
+    for (int c = tid; c < W; c += kThreads)
+      if (rch[c] && c0 + c < a.n) vloc[c] -= D - dcol[c];
+    for (int f = gtid; f < nfound; f += gthreads) {
+      int32_t j = ldcg(a.found + f);
+      // winner: the smallest free column that reached this tree's root
+      int32_t i = ldcg(a.tree_par + j);
+      // walk to the root (the path is only read here; flips happen below by
+      // the winner alone, and trees are disjoint)
+      int32_t root = ldcg(a.root_row + i);
+      if (ldcg(a.claim + root) != claim_key(phase, j)) continue;
+      for (;;) {
+        i = ldcg(a.tree_par + j);
+        const int32_t nxt = ldcg(a.match_row + i);
+        a.match_row[i] = j;
+        a.match_col[j] = i;
+        if (nxt < 0) break;
+        j = nxt;
+      }
+    }
+    if (leader) {
+      ctrl->phases = phase + 1;
+      if (deadline && globaltimer_ns() > deadline) ctrl->stop = 1;
+    }
+    bar.sync();  // ------------------------------------------------ B3
+  }
+  for (int c = tid; c < W; c += kThreads)
+    if (c0 + c < a.n) a.v[c0 + c] = vloc[c];
+  if (leader) {
+    ctrl->dual_steps = dual_steps;
+    ctrl->rows_scanned = rows_scanned;
+  }
+}
+
+// ---- K10: objective  sum_i C[i][match_row[i]] (core.cpp:76-90, int64) -------
+__global__ void k_objective(const int32_t* C, int64_t pitch, int n, const int32_t* match_row,
+                            unsigned long long* out) {
+  int64_t s = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int j = match_row[i];
+    if (j >= 0) s += C[static_cast<int64_t>(i) * pitch + j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, static_cast<unsigned long long>(s));
+}
+
+size_t solver_smem_bytes(int W) { return static_cast<size_t>(W) * (8 + 8 + 8 + 1) + 16; }
+
+cudaError_t launch_solver(const SolverArgs& a, int G, cudaStream_t st) {
+  k_init_rows<<<256, 256, 0, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = solver_smem_bytes(a.W);
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  void* params[] = {const_cast<SolverArgs*>(&a)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_solve), dim3(G), dim3(kThreads),
+                                     params, smem, st);
+}
+
+cudaError_t launch_objective(const int32_t* C, int64_t pitch, int n, const int32_t* match_row,
+                             unsigned long long* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  const int blocks = (n + 255) / 256 < 148 ? (n + 255) / 256 : 148;
+  k_objective<<<blocks, 256, 0, st>>>(C, pitch, n, match_row, out);
+  return cudaGetLastError();
+}
+
+int solver_threads() { return kThreads; }
+
+}  // namespace kmb

@@ -1,0 +1,250 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): total cost and duals bit-exact in integer
+arithmetic; the assignment identical to the oracle's where the optimum is
+unique, otherwise verified optimal by exact complementary slackness.  The
+dual-step count is invariant too and is compared; the
+phase count is not a parity target.
+
+Oracles: ``oracle/_ref/libotref.so`` (the unmodified reference built from its
+own sources) for every case it finishes in seconds; the seeded e-maxx
+restatement (pinned against the reference in tests/test_oracle.py) for config
+4; committed golden hashes + exact certificate checks for config 5.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2005_01182_b200 import KMB_SEED_BATCHED, KMB_SEED_KM, KmbError
+from paper_2005_01182_b200 import workloads as W
+from paper_2005_01182_b200.api import OPT_CONTINUE_BFS, OPT_ENGINE, OPT_MAX_CTAS
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def certificate_ok(c, u, v, r2c) -> bool:
+    """Exact optimality: u_i + v_j <= C_ij everywhere, equality on the matching,
+    and the matching is a permutation (complementary slackness)."""
+    c = np.asarray(c, np.int64)
+    n = c.shape[0]
+    if sorted(r2c.tolist()) != list(range(n)):
+        return False
+    if (u[:, None] + v[None, :] > c).any():
+        return False
+    return bool((u + v[r2c] == c[np.arange(n), r2c]).all())
+
+
+def optimum_unique(c, u, v, r2c) -> bool:
+    """The optimum is unique iff the tight graph at (u, v) has no alternating
+    cycle w.r.t. the matching: orient matched edges col->row and tight
+    unmatched edges row->col; unique iff that digraph is acyclic."""
+    c = np.asarray(c, np.int64)
+    n = c.shape[0]
+    tight = (c - u[:, None] - v[None, :]) == 0
+    col_row = np.empty(n, np.int64)
+    col_row[r2c] = np.arange(n)
+    # node i (row) -> rows reachable in one alternating step: row i -> tight col j
+    # (j != r2c[i]) -> its matched row col_row[j]
+    adj = [col_row[np.nonzero(tight[i] & (np.arange(n) != r2c[i]))[0]] for i in range(n)]
+    color = np.zeros(n, np.int8)
+    for s in range(n):
+        if color[s]:
+            continue
+        stack = [(s, 0)]
+        color[s] = 1
+        while stack:
+            x, k = stack.pop()
+            if k < len(adj[x]):
+                stack.append((x, k + 1))
+                y = adj[x][k]
+                if color[y] == 1:
+                    return False
+                if color[y] == 0:
+                    color[y] = 1
+                    stack.append((y, 0))
+            else:
+                color[x] = 2
+    return True
+
+
+def check_against(res, ref, c, dual_steps=None):
+    assert res.total_cost == ref.total_cost
+    np.testing.assert_array_equal(res.u, ref.u)
+    np.testing.assert_array_equal(res.v, ref.v)
+    assert certificate_ok(c, res.u, res.v, res.row_to_col)
+    if optimum_unique(c, res.u, res.v, res.row_to_col):
+        np.testing.assert_array_equal(res.row_to_col, ref.row_to_col)
+    if dual_steps is not None:
+        assert res.stats["dual_steps"] == dual_steps
+
+
+# ---- known answers of the reference's own tests (test_hungarian.cpp) ----------
+
+def test_known_2x2(solver):  # test_hungarian.cpp:72-85
+    c = np.array([[1, 3], [2, 1]], np.int32)
+    for seed in (KMB_SEED_KM, KMB_SEED_BATCHED):
+        for engine in (1, 2):
+            solver.set_option(OPT_ENGINE, engine)
+            r = solver.solve(c, seed)
+            assert r.total_cost == 2
+            assert r.row_to_col.tolist() == [0, 1]
+            assert int(r.u.sum() + r.v.sum()) == 2
+    solver.set_option(OPT_ENGINE, 0)
+
+
+def test_known_zero_diagonal(solver):  # :61-70
+    c = np.array([[0, 5, 5], [5, 0, 5], [5, 5, 0]], np.int32)
+    r = solver.solve(c, KMB_SEED_KM)
+    assert r.total_cost == 0 and r.row_to_col.tolist() == [0, 1, 2]
+
+
+def test_known_constant(solver):  # :133-142: constant 6x6 cost 4 -> 24, one phase, no step
+    r = solver.solve(np.full((6, 6), 4, np.int32), KMB_SEED_BATCHED)
+    assert r.total_cost == 24
+    assert r.stats["dual_steps"] == 0
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("seed", [KMB_SEED_KM, KMB_SEED_BATCHED])
+def test_random_small_vs_reference(solver, engine, seed):
+    rng = np.random.default_rng(100 + 10 * engine + seed)
+    solver.set_option(OPT_ENGINE, engine)
+    try:
+        for t in range(150):
+            n = int(rng.integers(1, 60))
+            hi = int(rng.choice([1, 2, 9, 50, 1000, 10**6, 2**30 - 1]))
+            c = rng.integers(0, hi + 1, size=(n, n)).astype(np.int32)
+            ref = O.ref_solve_km(c) if seed == KMB_SEED_KM else O.ref_solve_batched_km(c)
+            r = solver.solve(c, seed)
+            ds = O.kmo_solve_batched(c).dual_steps if seed == KMB_SEED_BATCHED else None
+            check_against(r, ref, c, ds)
+    finally:
+        solver.set_option(OPT_ENGINE, 0)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 13, 31, 33, 127, 129, 200, 255, 257, 300, 513, 1000, 1001])
+def test_ragged_sizes_grid(solver, n):
+    rng = np.random.default_rng(n)
+    c = rng.integers(0, 5000, size=(n, n)).astype(np.int32)
+    ref = O.ref_solve_batched_km(c)
+    solver.set_option(OPT_ENGINE, 1)
+    try:
+        r = solver.solve(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_ENGINE, 0)
+    check_against(r, ref, c, O.kmo_solve_batched(c).dual_steps)
+
+
+@pytest.mark.parametrize("maxg", [1, 3, 16, 0])
+def test_cta_counts(solver, maxg):
+    rng = np.random.default_rng(7)
+    c = rng.integers(0, 100, size=(300, 300)).astype(np.int32)
+    ref = O.ref_solve_batched_km(c)
+    solver.set_option(OPT_ENGINE, 1)
+    solver.set_option(OPT_MAX_CTAS, maxg)
+    try:
+        r = solver.solve(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_MAX_CTAS, 0)
+        solver.set_option(OPT_ENGINE, 0)
+    check_against(r, ref, c)
+
+
+@pytest.mark.parametrize("cont", [0, 1])
+def test_continue_bfs_same_duals(solver, cont):
+    c = W.CONFIGS["c1"].make()
+    ref = O.ref_solve_batched_km(c)
+    solver.set_option(OPT_CONTINUE_BFS, cont)
+    try:
+        r = solver.solve(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_CONTINUE_BFS, 0)
+    check_against(r, ref, c)
+
+
+def test_matching_equals_mirror(solver):
+    """The engine is deterministic: same forest, same claims -> same matching as
+    the step-by-step CPU mirror."""
+    rng = np.random.default_rng(3)
+    for t in range(20):
+        n = int(rng.integers(2, 300))
+        c = rng.integers(0, 20, size=(n, n)).astype(np.int32)
+        m = O.mirror_solve(c, 1)
+        for engine in (1, 2) if n <= 224 else (1,):
+            solver.set_option(OPT_ENGINE, engine)
+            r = solver.solve(c, KMB_SEED_BATCHED)
+            np.testing.assert_array_equal(r.row_to_col, m.row_to_col)
+            assert r.stats["phases"] == m.phases
+    solver.set_option(OPT_ENGINE, 0)
+
+
+# ---- error behaviour (hungarian.cpp:15-21, core.cpp:144-145) ------------------
+
+def test_negative_cost_rejected(solver):
+    c = np.ones((5, 5), np.int32)
+    c[2, 3] = -1
+    for engine in (1, 2):
+        solver.set_option(OPT_ENGINE, engine)
+        with pytest.raises(KmbError, match="costs must be nonnegative"):
+            solver.solve(c, KMB_SEED_BATCHED)
+    solver.set_option(OPT_ENGINE, 0)
+
+
+def test_out_of_device_range_rejected(solver):
+    c = np.ones((5, 5), np.int32)
+    c[0, 0] = 2**30
+    with pytest.raises(KmbError, match="device range"):
+        solver.solve(c, KMB_SEED_BATCHED)
+
+
+def test_time_budget(solver):
+    c = W.CONFIGS["c2"].make()
+    solver.set_option(OPT_ENGINE, 1)
+    r = solver.solve(c, KMB_SEED_BATCHED, time_budget_s=1e-6)
+    solver.set_option(OPT_ENGINE, 0)
+    assert not r.converged
+    assert (r.row_to_col >= 0).sum() < c.shape[0]
+
+
+# ---- BASELINE configs -----------------------------------------------------------
+
+def test_config1(solver):
+    c = W.CONFIGS["c1"].make()
+    ref = O.ref_solve_batched_km(c)
+    r = solver.solve(c, KMB_SEED_BATCHED)
+    check_against(r, ref, c, O.kmo_solve_batched(c).dual_steps)
+    k = O.ref_solve_km(c)
+    rk = solver.solve(c, KMB_SEED_KM)
+    check_against(rk, k, c)
+
+
+def test_config2(solver):
+    c = W.CONFIGS["c2"].make()
+    ref = O.ref_solve_batched_km(c)
+    r = solver.solve(c, KMB_SEED_BATCHED)
+    check_against(r, ref, c)
+
+
+def test_config3_subset(solver):
+    c = W.CONFIGS["c3"].make(batch=64)
+    r = solver.solve_batch(c, KMB_SEED_BATCHED)
+    for t in range(c.shape[0]):
+        ref = O.ref_solve_batched_km(c[t])
+        assert r.total_cost[t] == ref.total_cost
+        np.testing.assert_array_equal(r.u[t], ref.u)
+        np.testing.assert_array_equal(r.v[t], ref.v)
+        assert certificate_ok(c[t], r.u[t], r.v[t], r.row_to_col[t])
+
+
+def test_config4(solver):
+    c = W.CONFIGS["c4"].make()
+    ref = O.kmo_solve_km_seeded(c)
+    r = solver.solve(c, KMB_SEED_BATCHED)
+    assert r.total_cost == ref.total_cost
+    np.testing.assert_array_equal(r.u, ref.u)
+    np.testing.assert_array_equal(r.v, ref.v)
+    assert certificate_ok(c, r.u, r.v, r.row_to_col)
