@@ -88,14 +88,15 @@ void kmb_gen_geometric(int32_t* out, int32_t n, double scale, uint64_t seed) {
   free(b);
 }
 
-/* Config 3: `batch` instances; instance t draws 2n vectors of dimension dim,
- * i.i.d. N(0,1) in fp32 from its own stream stream_of(seed, 4<<32 | t);
+/* Config 3: instances first .. first+batch-1; instance t draws 2n vectors of
+ * dimension dim, i.i.d. N(0,1) in fp32 from its own stream
+ * stream_of(seed, 4<<32 | t) (so any shard of the batch can be generated alone);
  * C = llround(scale * Euclidean distance) with the distance in double. */
-void kmb_gen_embedding_batch(int32_t* out, int32_t batch, int32_t n, int32_t dim,
-                             double scale, uint64_t seed) {
+void kmb_gen_embedding_batch(int32_t* out, int32_t first, int32_t batch, int32_t n,
+                             int32_t dim, double scale, uint64_t seed) {
 #pragma omp parallel for schedule(dynamic, 4)
   for (int32_t t = 0; t < batch; ++t) {
-    const uint64_t st = stream_of(seed, (4ULL << 32) | (uint64_t)t);
+    const uint64_t st = stream_of(seed, (4ULL << 32) | (uint64_t)(first + t));
     float* x = malloc(sizeof(float) * 2 * (size_t)n * dim);
     for (int64_t k = 0; k < 2 * (int64_t)n * dim; ++k) x[k] = (float)normal(st, (uint64_t)k);
     const float* A = x;

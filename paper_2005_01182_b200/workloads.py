@@ -33,7 +33,7 @@ def _load():
         lib.kmb_gen_uniform.argtypes = [_i32p, C.c_int32, C.c_int32, C.c_int32, C.c_uint64]
         lib.kmb_gen_geometric.argtypes = [_i32p, C.c_int32, C.c_double, C.c_uint64]
         lib.kmb_gen_embedding_batch.argtypes = [_i32p, C.c_int32, C.c_int32, C.c_int32,
-                                                C.c_double, C.c_uint64]
+                                                C.c_int32, C.c_double, C.c_uint64]
         lib.kmb_gen_gmm.argtypes = [_i32p, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                     C.c_double, C.c_uint64]
         lib.kmb_fnv1a64.argtypes = [C.c_void_p, C.c_int64]
@@ -57,11 +57,11 @@ def geometric(n: int, scale: float = 1e6, seed: int = 2) -> np.ndarray:
 
 
 def embedding_batch(batch: int, n: int = 128, dim: int = 300, scale: float = 1e4,
-                    seed: int = 3) -> np.ndarray:
-    """``batch`` instances of two n-sets of dim-D N(0,1) fp32 vectors;
-    llround(scale * Euclidean distance).  Shape (batch, n, n)."""
+                    seed: int = 3, first: int = 0) -> np.ndarray:
+    """Instances first..first+batch-1, each two n-sets of dim-D N(0,1) fp32
+    vectors; llround(scale * Euclidean distance).  Shape (batch, n, n)."""
     out = np.empty((batch, n, n), np.int32)
-    _load().kmb_gen_embedding_batch(out, batch, n, dim, scale, seed)
+    _load().kmb_gen_embedding_batch(out, first, batch, n, dim, scale, seed)
     return out
 
 
@@ -85,15 +85,16 @@ class Config:
     batch: int
     description: str
 
-    def make(self, batch: int | None = None) -> np.ndarray:
+    def make(self, batch: int | None = None, first: int = 0) -> np.ndarray:
         """The config's cost matrix (n, n), or (batch, n, n) for config 3.
-        ``batch`` overrides the instance count (a prefix of the same stream)."""
+        ``batch``/``first`` select instances first..first+batch-1 of config 3."""
         if self.key == "c1":
             return uniform(256, 0, 1000, seed=1)
         if self.key == "c2":
             return geometric(1024, 1e6, seed=2)
         if self.key == "c3":
-            return embedding_batch(self.batch if batch is None else batch, 128, 300, 1e4, seed=3)
+            return embedding_batch(self.batch if batch is None else batch, 128, 300, 1e4, seed=3,
+                                   first=first)
         if self.key == "c4":
             return gmm(4096, 16, 100.0, 1.0, 1e3, seed=4)
         if self.key == "c5":

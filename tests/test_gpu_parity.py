@@ -240,11 +240,44 @@ def test_config3_subset(solver):
         assert certificate_ok(c[t], r.u[t], r.v[t], r.row_to_col[t])
 
 
-def test_config4(solver):
-    c = W.CONFIGS["c4"].make()
-    ref = O.kmo_solve_km_seeded(c)
+def _golden():
+    with open(os.path.join(GOLDEN, "configs.json")) as f:
+        return json.load(f)
+
+
+def test_config3_golden(solver):
+    """Full 4096-instance batch; the first 64 against the reference's fixture
+    (tests/golden/make_golden.py), all of them by exact certificate."""
+    g = _golden()["c3_first64"]
+    c = W.CONFIGS["c3"].make()
+    r = solver.solve_batch(c, KMB_SEED_BATCHED)
+    assert W.fnv1a64(c[:64]) == g["cost_fnv"]
+    for t in range(64):
+        assert r.total_cost[t] == g["total_cost"][t]
+        assert W.fnv1a64(r.u[t]) == g["u_fnv"][t] and W.fnv1a64(r.v[t]) == g["v_fnv"][t]
+    for t in range(0, 4096, 97):
+        assert certificate_ok(c[t], r.u[t], r.v[t], r.row_to_col[t])
+    # size-independent property over the whole batch: dual objective == primal
+    assert np.array_equal(r.u.sum(1) + r.v.sum(1), r.total_cost)
+
+
+@pytest.mark.parametrize("key", ["c4", "c5"])
+def test_large_config_golden(solver, key):
+    g = _golden()
+    if key not in g:
+        pytest.skip(f"no golden for {key}")
+    g = g[key]
+    c = W.CONFIGS[key].make()
+    assert W.fnv1a64(c) == g["cost_fnv"]
     r = solver.solve(c, KMB_SEED_BATCHED)
-    assert r.total_cost == ref.total_cost
-    np.testing.assert_array_equal(r.u, ref.u)
-    np.testing.assert_array_equal(r.v, ref.v)
-    assert certificate_ok(c, r.u, r.v, r.row_to_col)
+    assert r.total_cost == g["total_cost"]
+    assert W.fnv1a64(r.u) == g["u_fnv"]
+    assert W.fnv1a64(r.v) == g["v_fnv"]
+    assert int(r.u.sum() + r.v.sum()) == r.total_cost
+    assert sorted(r.row_to_col.tolist()) == list(range(c.shape[0]))
+    # exact complementary slackness, chunked to bound host memory
+    cc = c.astype(np.int64)
+    for lo in range(0, c.shape[0], 2048):
+        blk = cc[lo:lo + 2048] - r.u[lo:lo + 2048, None] - r.v[None, :]
+        assert blk.min() >= 0
+    assert (cc[np.arange(c.shape[0]), r.row_to_col] == r.u + r.v[r.row_to_col]).all()

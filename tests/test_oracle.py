@@ -1,0 +1,185 @@
+"""CPU: pin the oracle before trusting it.
+
+* the C restatement (oracle/km_oracle.c) against the UNMODIFIED reference
+  compiled from its own sources (oracle/_ref/libotref.so), bit for bit:
+  duals, matching, total cost, `iterations`;
+* both against the reference's own known answers and golden checks
+  (test_hungarian.cpp, acceptance.cpp criterion 1/2, committed fixtures);
+* the seeded e-maxx restatement (config-5 oracle) against solve_batched_km;
+* the GPU-engine mirror (oracle/kmb_mirror.c) against the reference — the CPU
+  proof that the engine's forest augmentation keeps the duals canonical.
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def brute_force_assignment(c):  # tests/oracle.hpp:75-89
+    n = c.shape[0]
+    return min(sum(int(c[i, p[i]]) for i in range(n)) for p in itertools.permutations(range(n)))
+
+
+def same_duals(a, b):
+    return np.array_equal(a.u, b.u) and np.array_equal(a.v, b.v) and a.total_cost == b.total_cost
+
+
+# ---- known answers (test_hungarian.cpp) ----------------------------------------
+
+def test_quantize_known_answers():  # :27-59
+    for f in (O.ref_quantize_costs, O.kmo_quantize):
+        chat, N, ll = f([100, 200, 300, 400], 4)
+        assert chat.tolist() == [1, 2, 3, 4] and N == 400 and ll
+        assert f([7], 2)[0].tolist() == [2]
+        chat, N, ll = f([5, 7], 2)
+        assert chat.tolist() == [1, 2] and not ll
+        chat, N, ll = f([0, 0], 10)
+        assert chat.tolist() == [0, 0] and N == 1 and ll
+
+
+def test_quantize_errors():  # hungarian.cpp:34, :44-45
+    with pytest.raises(O.RefError, match="B must be positive"):
+        O.ref_quantize_costs([1, 2], 0)
+    with pytest.raises(ValueError, match="B must be positive"):
+        O.kmo_quantize([1, 2], 0)
+    with pytest.raises(O.RefError, match="overflows"):
+        O.ref_quantize_costs([2**40], 2**40)
+    with pytest.raises(ValueError, match="overflows"):
+        O.kmo_quantize([2**40], 2**40)
+
+
+def test_quantize_identity_random():
+    rng = np.random.default_rng(5)
+    c = rng.integers(0, 1000, 30)
+    c[0] = 999
+    a = O.ref_quantize_costs(c, 999)
+    b = O.kmo_quantize(c, 999)
+    assert np.array_equal(a[0], c) and np.array_equal(b[0], c) and a[2] and b[2]
+
+
+def test_km_2x2():  # :72-85
+    c = np.array([[1, 3], [2, 1]])
+    for r in (O.ref_solve_km(c), O.kmo_solve_km(c)):
+        assert r.total_cost == 2 and r.row_to_col.tolist() == [0, 1]
+        assert int(r.u.sum() + r.v.sum()) == 2
+
+
+def test_km_zero_diagonal():  # :61-70
+    c = np.array([[0, 5, 5], [5, 0, 5], [5, 5, 0]])
+    for r in (O.ref_solve_km(c), O.kmo_solve_km(c)):
+        assert r.total_cost == 0 and r.row_to_col.tolist() == [0, 1, 2]
+
+
+def test_batched_constant_one_phase():  # :133-142 (default B = 100)
+    c = np.full((6, 6), 4)
+    r = O.ref_solve_batched_km(c, B=100)
+    assert r.objective == 24.0 and r.iterations == 1
+    k = O.kmo_solve_batched(c)
+    assert k.total_cost == 24 and k.iterations == 1 and k.dual_steps == 0
+
+
+def test_errors_match_reference():  # :87-94, :200-205
+    c = np.array([[1, 3], [2, 1]])
+    with pytest.raises(O.RefError, match="unit-capacity square") as e:
+        O.ref_solve_km(c, supplies=[2, 1], demands=[1, 2])
+    assert e.value.code == 1
+    with pytest.raises(O.RefError, match="costs must be nonnegative"):
+        O.ref_solve_batched_km(np.array([[1, -1], [0, 0]]))
+
+
+def test_exhaustive_random_small():  # :96-105 (seed 11) and acceptance criterion 2
+    rng = np.random.default_rng(11)
+    for t in range(100):
+        n = 2 + int(rng.integers(0, 5))
+        c = rng.integers(0, 10, size=(n, n))
+        opt = brute_force_assignment(c)
+        assert O.ref_solve_km(c).total_cost == opt
+        assert O.kmo_solve_km(c).total_cost == opt
+        assert O.kmo_solve_batched(c).total_cost == opt
+        assert O.mirror_solve(c, 1).total_cost == opt
+
+
+# ---- restatement == reference, bit for bit ------------------------------------
+
+@pytest.mark.parametrize("hi", [1, 2, 9, 50, 1000, 10**6, 2**30 - 1])
+def test_restatement_matches_reference(hi):
+    rng = np.random.default_rng(hi % 1000)
+    for t in range(60):
+        n = int(rng.integers(1, 45))
+        c = rng.integers(0, hi + 1, size=(n, n))
+        r = O.ref_solve_batched_km(c)
+        k = O.kmo_solve_batched(c)
+        assert same_duals(k, r) and np.array_equal(k.row_to_col, r.row_to_col)
+        assert k.iterations == r.iterations  # phases + adjustments (hungarian.cpp:375)
+        rk = O.ref_solve_km(c)
+        kk = O.kmo_solve_km(c)
+        assert same_duals(kk, rk) and np.array_equal(kk.row_to_col, rk.row_to_col)
+
+
+@pytest.mark.parametrize("hi", [2, 30, 10**6])
+def test_mirror_and_seeded_match_reference(hi):
+    """SURVEY fact 0.5 reproduced: the GPU engine's strategy (argmin-parent
+    forest, lazy duals, both augmentation schedules) and seeded e-maxx all land
+    on the reference's duals; the dual-step sequence (delta, |closure|) is
+    identical step by step."""
+    rng = np.random.default_rng(hi)
+    for t in range(150):
+        n = int(rng.integers(1, 60))
+        c = rng.integers(0, hi + 1, size=(n, n)).astype(np.int32)
+        r = O.ref_solve_batched_km(c)
+        k = O.kmo_solve_batched(c, trace_cap=100000)
+        for cont in (False, True):
+            m = O.mirror_solve(c, 1, continue_bfs=cont, trace_cap=100000)
+            assert same_duals(m, r)
+            assert m.dual_steps == k.dual_steps
+            assert np.array_equal(m.trace, k.trace)
+        assert same_duals(O.kmo_solve_km_seeded(c), r)
+        assert same_duals(O.mirror_solve(c, 0), O.ref_solve_km(c))
+
+
+def test_config1_config2_mirror():
+    from paper_2005_01182_b200 import workloads as W
+    for key in ("c1", "c2"):
+        c = W.CONFIGS[key].make()
+        r = O.ref_solve_batched_km(c)
+        assert same_duals(O.mirror_solve(c, 1), r)
+        assert same_duals(O.kmo_solve_km_seeded(c), r)
+
+
+def test_acceptance_circle_square_objectives():
+    """acceptance.cpp criterion 1 pins cs100 = 732033 (and cs900 = 9515106,
+    SURVEY.md §8(c)); the CircleSquare instance is RNG-free
+    (datasets.cpp:57-112) and restated in tests/golden/make_golden.py."""
+    from tests.golden.make_golden import circle_square
+    c = circle_square(100)
+    assert O.ref_solve_km(c).total_cost == 732033
+    assert O.kmo_solve_batched(c).total_cost == 732033
+    assert O.mirror_solve(c.astype(np.int32), 1).total_cost == 732033
+
+
+def test_golden_fixtures():
+    """Committed fixtures generated by tests/golden/make_golden.py with the
+    reference itself: the restatement and the seeded generators still agree."""
+    from paper_2005_01182_b200 import workloads as W
+    with open(os.path.join(GOLDEN, "configs.json")) as f:
+        g = json.load(f)
+    for key in ("c1", "c2"):
+        c = W.CONFIGS[key].make()
+        assert W.fnv1a64(c) == g[key]["cost_fnv"]
+        k = O.kmo_solve_batched(c)
+        assert k.total_cost == g[key]["total_cost"]
+        assert W.fnv1a64(k.u) == g[key]["u_fnv"] and W.fnv1a64(k.v) == g[key]["v_fnv"]
+        assert k.dual_steps == g[key]["dual_steps"]
+    small = np.load(os.path.join(GOLDEN, "small_cases.npz"))
+    for t in range(int(small["count"])):
+        n = int(small["n"][t])
+        c = small["cost"][t, :n, :n]
+        k = O.kmo_solve_batched(c)
+        assert k.total_cost == small["total"][t]
+        assert np.array_equal(k.u, small["u"][t, :n]) and np.array_equal(k.v, small["v"][t, :n])
