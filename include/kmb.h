@@ -14,7 +14,7 @@
  *
  * Semantics (identical to the reference on the same inputs):
  *   cost         n x n int32, row-major with leading dimension ld (>= n),
- *                entries in [0, 2^30) (the reference only requires >= 0; the
+ *                entries in [0, 2^29) (the reference only requires >= 0; the
  *                device engine keeps reduced costs in 32 bits).
  *   seed         KMB_SEED_KM      = u = v = 0, the start of solve_km (:63)
  *                KMB_SEED_BATCHED = row/column reductions (:323-333), the start
@@ -54,7 +54,7 @@ enum kmb_status {
   KMB_OK = 0,
   KMB_EINVAL = 1,        /* bad argument (n <= 0, null pointer, ld < n) */
   KMB_ENEGATIVE = 2,     /* "costs must be nonnegative" (core.cpp:144-145) */
-  KMB_ERANGE = 3,        /* a cost >= 2^30 (device range)                  */
+  KMB_ERANGE = 3,        /* a cost >= 2^29 (device range)                  */
   KMB_ECUDA = -1,        /* CUDA runtime error                             */
   KMB_EINTERNAL = -2,    /* engine invariant violated                      */
   KMB_ENODEVICE = -3     /* no sm_100 device                               */
@@ -63,7 +63,8 @@ enum kmb_status {
 enum kmb_option {
   KMB_OPT_MAX_CTAS = 1,     /* grid engine: upper bound on CTAs (0 = #SMs)      */
   KMB_OPT_CONTINUE_BFS = 2, /* 1: exhaust the tight closure before augmenting   */
-  KMB_OPT_ENGINE = 3        /* 0 auto, 1 grid (persistent), 2 SMEM (n <= 224)   */
+  KMB_OPT_ENGINE = 3        /* 0 auto, 1 grid (persistent), 2 CTA/SMEM (n<=224),
+                               3 warp/SMEM, 4 warp/L2 (n <= 256)                */
 };
 
 typedef struct kmb_stats {
@@ -74,6 +75,9 @@ typedef struct kmb_stats {
   double seconds;          /* device time of the solve (CUDA events)         */
   int32_t converged;       /* 0 when the time budget expired                 */
   int32_t engine;          /* 1 grid, 2 SMEM                                 */
+  int64_t rounds;          /* search rounds (relax | min | absorb)           */
+  int64_t stage_ns[6];     /* grid engine, CTA 0's clock: relax, barrier 1,
+                              absorb, barrier 2, phase end, barrier 3        */
 } kmb_stats;
 
 typedef struct kmb_context kmb_context;

@@ -51,6 +51,7 @@ int kmm_solve(const int32_t* C, int32_t n, int32_t seed, int32_t continue_bfs,
   int32_t* claim = malloc(sizeof(int32_t) * (size_t)n);
   int32_t* list = malloc(sizeof(int32_t) * (size_t)n);
   int32_t* found = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* dead_round = malloc(sizeof(int32_t) * (size_t)n);
   if (!match_col || !key || !w || !dc || !rcol || !tree_par || !root_row ||
       !claim || !list || !found)
     return -1;
@@ -84,7 +85,7 @@ int kmm_solve(const int32_t* C, int32_t n, int32_t seed, int32_t continue_bfs,
     int64_t D = 0;
     int32_t head = 0, nfound = 0;
     int first = (phase == 0 && seed == 1);
-    for (;;) {
+    for (int32_t round = 0;; ++round) {
       /* relax rows reached last round */
       for (int32_t r = head; r < tail; ++r) {
         const int32_t i = list[r];
@@ -131,8 +132,11 @@ int kmm_solve(const int32_t* C, int32_t n, int32_t seed, int32_t continue_bfs,
         if (i2 < 0) {
           if (claim[root] != phase) {
             claim[root] = phase;
+            dead_round[root] = round;
             found[nfound++] = j;
           }
+        } else if (continue_bfs == 2 && claim[root] == phase && dead_round[root] < round) {
+          /* harvest mode: a tree that already owns a free column stops growing */
         } else {
           w[i2] = u[i2] - D;
           root_row[i2] = root;
@@ -168,6 +172,6 @@ int kmm_solve(const int32_t* C, int32_t n, int32_t seed, int32_t continue_bfs,
   if (rows_scanned_out) *rows_scanned_out = rows_scanned;
 done:
   free(match_col); free(key); free(w); free(dc); free(rcol); free(tree_par);
-  free(root_row); free(claim); free(list); free(found);
+  free(root_row); free(claim); free(list); free(found); free(dead_round);
   return rc;
 }

@@ -43,7 +43,8 @@ class KmbError(RuntimeError):
 class Stats(C.Structure):
     _fields_ = [("phases", C.c_int64), ("dual_steps", C.c_int64), ("rows_scanned", C.c_int64),
                 ("cost_bytes_read", C.c_int64), ("seconds", C.c_double),
-                ("converged", C.c_int32), ("engine", C.c_int32)]
+                ("converged", C.c_int32), ("engine", C.c_int32), ("rounds", C.c_int64),
+                ("stage_ns", C.c_int64 * 6)]
 
 
 _lib = None
@@ -193,7 +194,9 @@ class Solver:
 
 
 def _stats_dict(st: Stats) -> dict:
-    return {k: getattr(st, k) for k, _ in Stats._fields_}
+    d = {k: getattr(st, k) for k, _ in Stats._fields_}
+    d["stage_ns"] = list(d["stage_ns"])
+    return d
 
 
 _default: Solver | None = None
@@ -253,7 +256,7 @@ def solve_km(cost, supplies=None, demands=None, time_budget_s: float = 0.0,
     c = _validate(cost, supplies, demands, "solve_km")
     if (c < 0).any():
         raise ValueError("solve_km: costs must be nonnegative")
-    if c.max() >= 2**30:
+    if c.max() >= 2**29:
         _range_error("solve_km")
     s = solver or default_solver()
     r = s.solve(c.astype(np.int32, copy=False), KMB_SEED_KM, time_budget_s)
@@ -274,7 +277,7 @@ def solve_batched_km(cost, B: int | None = None, supplies=None, demands=None,
     if B is None:
         B = max(int(c64.max()), 1)
     chat, N, lossless = quantize_costs(c64, int(B))
-    if chat.size and chat.max() >= 2**30:
+    if chat.size and chat.max() >= 2**29:
         _range_error("solve_batched_km")
     s = solver or default_solver()
     r = s.solve(chat.astype(np.int32), KMB_SEED_BATCHED, time_budget_s)
@@ -288,4 +291,4 @@ def solve_batched_km(cost, B: int | None = None, supplies=None, demands=None,
 
 
 def _range_error(who: str):
-    raise ValueError(f"{who}: cost exceeds the device range [0, 2^30)")
+    raise ValueError(f"{who}: cost exceeds the device range [0, 2^29)")

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) k_batch_solve(BatchArgs a) {
       const int64_t u0 = a.seed == 1 ? lo : 0;
       if (lane == 0) {
         if (lo < 0) atomicMax(&sm.status, 2);
-        else if (hi >= (1 << 30)) atomicMax(&sm.status, 3);
+        else if (hi >= (1 << 29)) atomicMax(&sm.status, 3);
         u[i] = u0;
         w[i] = u0;
       }

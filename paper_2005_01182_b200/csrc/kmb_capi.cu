@@ -77,7 +77,7 @@ struct kmb_context {
   DevBuf cost, u, v, mrow, mcol, tpar, root, claim, lrow0, lrow1, lw0, lw1, found, partial,
       ctrl, obj;
   // batch workspace
-  DevBuf bcost, br2c, bu, bv, btot, bstat, bstatus;
+  DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus;
 };
 
 extern "C" {
@@ -114,7 +114,7 @@ void kmb_destroy(kmb_context* c) {
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
-                    &c->obj, &c->bcost, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
+                    &c->obj, &c->bcost, &c->bpad, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
                     &c->bstatus})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -134,7 +134,7 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
     case KMB_OPT_MAX_CTAS: c->max_ctas = value; return KMB_OK;
     case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_ENGINE:
-      if (value < 0 || value > 2) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0, 1 or 2");
+      if (value < 0 || value > 4) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..4");
       c->engine = static_cast<int>(value);
       return KMB_OK;
     default: return fail(KMB_EINVAL, "kmb_set_option: unknown option");
@@ -150,14 +150,14 @@ static int copy_out(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 static int status_message(int status, const char* who) {
   if (status == KMB_ENEGATIVE) return fail(status, std::string(who) + ": costs must be nonnegative");
   if (status == KMB_ERANGE)
-    return fail(status, std::string(who) + ": cost exceeds the device range [0, 2^30)");
+    return fail(status, std::string(who) + ": cost exceeds the device range [0, 2^29)");
   return fail(KMB_EINTERNAL, std::string(who) + ": engine invariant violated (status " +
                                  std::to_string(status) + ")");
 }
 
 static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch, int32_t n,
                             int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
-                            int64_t* total_cost, kmb_stats* stats, const char* who) {
+                            int64_t* total_cost, kmb_stats* stats, const char* who, int engine) {
   cudaStream_t st = c->stream;
   const size_t cbytes = static_cast<size_t>(batch) * n * n * sizeof(int32_t);
   const int32_t* dcost = costs;
@@ -175,21 +175,49 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   if (!is_device_ptr(total_cost)) { KMB_CUDA(c->btot.ensure(batch * 8)); dtot = c->btot.as<int64_t>(); }
   KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * 3 * 8));
   KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
-  kmb::BatchArgs a{};
-  a.C = dcost;
-  a.batch = batch;
-  a.n = n;
-  a.seed = seed;
-  a.continue_bfs = c->continue_bfs;
-  a.row_to_col = dr2c;
-  a.u = du;
-  a.v = dv;
-  a.total_cost = dtot;
-  a.stats = c->bstat.as<int64_t>();
-  a.status = c->bstatus.as<int32_t>();
-  KMB_CUDA(cudaEventRecord(c->ev0, st));
+  if (engine == 0 || engine == 1) engine = 4;  // auto: warp engine, costs from L2
+  if (engine == 2 && n > kmb::batch_max_n()) engine = 4;
   int grid = 0;
-  KMB_CUDA(kmb::launch_batch(a, c->sm_count, st, &grid));
+  if (engine == 2) {
+    kmb::BatchArgs a{};
+    a.C = dcost;
+    a.batch = batch;
+    a.n = n;
+    a.seed = seed;
+    a.continue_bfs = c->continue_bfs;
+    a.row_to_col = dr2c;
+    a.u = du;
+    a.v = dv;
+    a.total_cost = dtot;
+    a.stats = c->bstat.as<int64_t>();
+    a.status = c->bstatus.as<int32_t>();
+    KMB_CUDA(cudaEventRecord(c->ev0, st));
+    KMB_CUDA(kmb::launch_batch(a, c->sm_count, st, &grid));
+  } else {
+    const int np = (n + 3) & ~3;
+    const int32_t* src = dcost;
+    if (np != n) {  // 16 B row alignment for 128-bit loads / TMA: pad once
+      KMB_CUDA(c->bpad.ensure(static_cast<size_t>(batch) * n * np * 4));
+      KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4,
+                                 static_cast<size_t>(batch) * n, cudaMemcpyDeviceToDevice, st));
+      src = c->bpad.as<int32_t>();
+    }
+    kmb::WarpArgs a{};
+    a.C = src;
+    a.batch = batch;
+    a.n = n;
+    a.pitch = np;
+    a.seed = seed;
+    a.continue_bfs = c->continue_bfs;
+    a.row_to_col = dr2c;
+    a.u = du;
+    a.v = dv;
+    a.total_cost = dtot;
+    a.stats = c->bstat.as<int64_t>();
+    a.status = c->bstatus.as<int32_t>();
+    KMB_CUDA(cudaEventRecord(c->ev0, st));
+    KMB_CUDA(kmb::launch_warp_batch(a, c->sm_count, engine == 3, st, &grid));
+  }
   KMB_CUDA(cudaEventRecord(c->ev1, st));
   if (dr2c != row_to_col) { int r = copy_out(row_to_col, dr2c, nb * 4, st); if (r) return r; }
   if (du != u) { int r = copy_out(u, du, nb * 8, st); if (r) return r; }
@@ -222,7 +250,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     stats->seconds = ms * 1e-3;
     stats->converged = 1;
-    stats->engine = 2;
+    stats->engine = engine;
   }
   delete[] hstat;
   if (bad) return status_message(bad, who);
@@ -237,11 +265,12 @@ int kmb_solve_batch_i32(kmb_context* c, const int32_t* costs, int32_t batch, int
   if (batch <= 0 || n <= 0) return fail(KMB_EINVAL, "kmb_solve_batch_i32: dimensions must be positive");
   if (!costs) return fail(KMB_EINVAL, "kmb_solve_batch_i32: costs is NULL");
   if (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED) return fail(KMB_EINVAL, "kmb_solve_batch_i32: bad seed");
-  if (n > kmb::batch_max_n())
-    return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > " + std::to_string(kmb::batch_max_n()) +
+  if (n > kmb::warp_max_n())
+    return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > " + std::to_string(kmb::warp_max_n()) +
                                 " (use kmb_solve_i32 per instance)");
   KMB_CUDA(cudaSetDevice(c->device));
-  return solve_batch_impl(c, costs, batch, n, seed, row_to_col, u, v, total_cost, stats, who);
+  return solve_batch_impl(c, costs, batch, n, seed, row_to_col, u, v, total_cost, stats, who,
+                          c->engine);
 }
 
 int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, int32_t seed,
@@ -257,18 +286,19 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   cudaStream_t st = c->stream;
 
   int engine = c->engine;
-  if (engine == 0) engine = (n <= 128 && time_budget_s <= 0.0) ? 2 : 1;
+  if (engine == 0) engine = (n <= 128 && time_budget_s <= 0.0) ? 4 : 1;
   if (engine == 2 && n > kmb::batch_max_n()) engine = 1;
-  if (engine == 2) {
+  if (engine >= 3 && n > kmb::warp_max_n()) engine = 1;
+  if (engine >= 2) {
     if (time_budget_s > 0.0)
-      return fail(KMB_EINVAL, "kmb_solve_i32: the SMEM engine has no time budget; use engine 1");
+      return fail(KMB_EINVAL, "kmb_solve_i32: the per-instance engines have no time budget; use engine 1");
     const int32_t* src = cost;
     if (ld != n) {  // compact into the batch buffer
       KMB_CUDA(c->bcost.ensure(static_cast<size_t>(n) * n * 4));
       KMB_CUDA(cudaMemcpy2DAsync(c->bcost.p, n * 4, cost, ld * 4, n * 4, n, cudaMemcpyDefault, st));
       src = c->bcost.as<int32_t>();
     }
-    return solve_batch_impl(c, src, 1, n, seed, row_to_col, u, v, total_cost, stats, who);
+    return solve_batch_impl(c, src, 1, n, seed, row_to_col, u, v, total_cost, stats, who, engine);
   }
 
   // ---- grid engine: choose the slab width W (power of two) and CTA count G ----
@@ -354,6 +384,8 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
     stats->seconds = ms * 1e-3;
     stats->converged = h.free_rows == 0 ? 1 : 0;
     stats->engine = 1;
+    stats->rounds = h.rounds;
+    for (int k = 0; k < 6; ++k) stats->stage_ns[k] = h.stage_ns[k];
   }
   return KMB_OK;
 }

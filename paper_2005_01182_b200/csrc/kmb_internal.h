@@ -20,6 +20,8 @@ struct Ctrl {
   int64_t phases;
   int64_t dual_steps;
   int64_t rows_scanned;
+  int64_t rounds;
+  int64_t stage_ns[6];
 };
 
 struct SolverArgs {
@@ -68,4 +70,25 @@ struct BatchArgs {
 int batch_max_n();
 cudaError_t launch_batch(const BatchArgs& a, int sm_count, cudaStream_t st, int* grid_out);
 
+}  // namespace kmb
+
+namespace kmb {
+// ---- warp engine (one warp per instance, n <= 256) -----------------------------
+struct WarpArgs {
+  const int32_t* C;      // batch x n x pitch (pitch % 4 == 0), instances back to back
+  int32_t batch;
+  int32_t n;
+  int32_t pitch;
+  int32_t seed;
+  int32_t continue_bfs;
+  int32_t* row_to_col;   // batch x n
+  int64_t* u;            // batch x n
+  int64_t* v;            // batch x n
+  int64_t* total_cost;   // batch
+  int64_t* stats;        // batch x 3 (may be null)
+  int32_t* status;       // batch
+};
+int warp_max_n();
+cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, cudaStream_t st,
+                              int* grid_out);
 }  // namespace kmb

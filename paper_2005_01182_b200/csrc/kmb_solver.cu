@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
     const int64_t u0 = a.seed == 1 ? lo : 0;
     if (lane == 0) {
       if (lo < 0) atomicMax(&a.ctrl->status, 2);               // KMB_ENEGATIVE
-      else if (hi >= (1 << 30)) atomicMax(&a.ctrl->status, 3);  // KMB_ERANGE
+      else if (hi >= (1 << 29)) atomicMax(&a.ctrl->status, 3);  // KMB_ERANGE
       a.u[i] = u0;
       a.list_row[0][i] = i;
       a.list_w[0][i] = u0;
@@ -184,6 +184,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   if (ldcg(&ctrl->status) != 0) return;  // invalid input (k_init_rows), all CTAs agree
   for (int c = tid; c < W; c += kThreads) vloc[c] = 0;  // seed 0: v = 0
   int64_t dual_steps = 0, rows_scanned = 0;
+  // stage clock (leader only): 0 relax+local min, 1 B1, 2 absorb, 3 B2, 4 phase end, 5 B3
+  long long prof[6] = {0, 0, 0, 0, 0, 0};
+  long long rounds_total = 0;
+  unsigned long long tprev = leader ? globaltimer_ns() : 0ull;
+#define KMB_STAGE(k)                                   \
+  do {                                                 \
+    if (leader) {                                      \
+      const unsigned long long t_ = globaltimer_ns();  \
+      prof[k] += static_cast<long long>(t_ - tprev);   \
+      tprev = t_;                                      \
+    }                                                  \
+  } while (0)
   unsigned long long deadline = a.deadline_ns;
   if (deadline >> 63) deadline = globaltimer_ns() + (deadline & ~(1ull << 63));  // relative budget
 
@@ -208,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     for (int round = 0;; ++round) {
       relax_slab(a, list, listw, head, tail, c0, W, skey);
       rows_scanned += tail - head;
+      ++rounds_total;
       __syncthreads();
       if (phase == 0 && round == 0 && a.seed == 1)  // column reduction, hungarian.cpp:328-333
         for (int c = tid; c < W; c += kThreads)
@@ -227,7 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
         x = warp_min_i64(x);
         if (lane == 0) a.partial[blockIdx.x] = x;
       }
+      KMB_STAGE(0);
       bar.sync();  // ---------------------------------------------- B1
+      KMB_STAGE(1);
       if (round == 0 && leader) {  // recycle the previous phase's counters
         ctrl->tail[p ^ 1] = 0;
         ctrl->nfound[p ^ 1] = 0;
@@ -296,7 +311,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
           if (newfree) a.found[base + __popc(fmask & ((1u << lane) - 1))] = col;
         }
       }
+      KMB_STAGE(2);
       bar.sync();  // ---------------------------------------------- B2
+      KMB_STAGE(3);
       head = tail;
       tail = ldcg(&ctrl->tail[p]);
       nfound = ldcg(&ctrl->nfound[p]);
@@ -341,13 +358,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       ctrl->phases = phase + 1;
       if (deadline && globaltimer_ns() > deadline) ctrl->stop = 1;
     }
+    KMB_STAGE(4);
     bar.sync();  // ------------------------------------------------ B3
+    KMB_STAGE(5);
   }
   for (int c = tid; c < W; c += kThreads)
     if (c0 + c < a.n) a.v[c0 + c] = vloc[c];
   if (leader) {
     ctrl->dual_steps = dual_steps;
     ctrl->rows_scanned = rows_scanned;
+    ctrl->rounds = rounds_total;
+    for (int k = 0; k < 6; ++k) ctrl->stage_ns[k] = prof[k];
   }
 }
 
