@@ -78,6 +78,8 @@ typedef struct kmb_stats {
   int64_t rounds;          /* search rounds (relax | min | absorb)           */
   int64_t stage_ns[6];     /* grid engine, CTA 0's clock: relax, barrier 1,
                               absorb, barrier 2, phase end, barrier 3        */
+  int64_t max_instance_cycles; /* batch engines: slowest instance (SM clocks) */
+  int64_t sum_instance_cycles; /* batch engines: sum over instances          */
 } kmb_stats;
 
 typedef struct kmb_context kmb_context;

@@ -175,3 +175,175 @@ done:
   free(root_row); free(claim); free(list); free(found); free(dead_round);
   return rc;
 }
+
+/*
+ * Incremental variant (the engine's "epoch" schedule): the multi-source search
+ * is never restarted.  When a round absorbs free columns, the trees that own
+ * one are augmented and dissolved — their rows and columns are finalised
+ * (u = w + D, v -= D - Dc) and become unreached — while every other tree
+ * stays reached with its lazy duals.  Columns whose argmin row belonged to a
+ * dissolved tree are reset and all surviving rows are relaxed once more, which
+ * restores key_j = min over the surviving reached rows for every unreached
+ * column; the search then continues at the same D.  Surviving trees are tight
+ * alternating trees from free roots, so the explored set is still exactly the
+ * tight closure of the free rows and dual steps still happen only when it
+ * holds no free column.
+ */
+int kmm_solve_incr(const int32_t* C, int32_t n, int32_t seed, int64_t* u, int64_t* v,
+                   int32_t* match_row, int64_t* total_cost, int64_t* epochs_out,
+                   int64_t* dual_steps_out, int64_t* rows_scanned_out, int64_t* rounds_out,
+                   int64_t* trace, int64_t trace_cap) {
+  int32_t* match_col = malloc(sizeof(int32_t) * (size_t)n);
+  uint64_t* key = malloc(sizeof(uint64_t) * (size_t)n);
+  int64_t* w = malloc(sizeof(int64_t) * (size_t)n);
+  int64_t* dc = malloc(sizeof(int64_t) * (size_t)n);
+  char* rcol = malloc((size_t)n);
+  char* rrow = malloc((size_t)n);
+  int32_t* tree_par = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* root_row = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* claim = malloc(sizeof(int32_t) * (size_t)n); /* epoch stamp */
+  int32_t* claim_col = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* rows = malloc(sizeof(int32_t) * (size_t)n);  /* reached rows */
+  int32_t* nxt_rows = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* found = malloc(sizeof(int32_t) * (size_t)n);
+  if (!match_col || !key || !w || !dc || !rcol || !rrow || !tree_par || !root_row || !claim ||
+      !claim_col || !rows || !nxt_rows || !found)
+    return -1;
+  for (int32_t i = 0; i < n; ++i) {
+    match_row[i] = match_col[i] = -1;
+    claim[i] = -1;
+    u[i] = 0;
+    v[i] = 0;
+    key[i] = UINT64_MAX;
+    rcol[i] = 0;
+  }
+  if (seed == 1)
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t* row = C + (size_t)i * n;
+      int32_t lo = row[0];
+      for (int32_t j = 1; j < n; ++j) if (row[j] < lo) lo = row[j];
+      u[i] = lo;
+    }
+  /* every row starts free and reached */
+  int32_t nrows = n;
+  for (int32_t i = 0; i < n; ++i) {
+    rows[i] = i;
+    rrow[i] = 1;
+    w[i] = u[i];
+    root_row[i] = i;
+  }
+  int32_t head = 0; /* rows[head, nrows) still to relax */
+  int64_t D = 0, dual_steps = 0, rows_scanned = 0, rounds = 0, epochs = 0;
+  int first = (seed == 1);
+  int32_t nfree = n;
+  int rc = 0;
+  while (nfree > 0) {
+    ++rounds;
+    for (int32_t r = head; r < nrows; ++r) {
+      const int32_t i = rows[r];
+      const int32_t* row = C + (size_t)i * n;
+      for (int32_t j = 0; j < n; ++j) {
+        const uint64_t k = pack_key((int64_t)row[j] - w[i], i);
+        if (k < key[j]) key[j] = k;
+      }
+    }
+    rows_scanned += nrows - head;
+    head = nrows;
+    if (first) {
+      for (int32_t j = 0; j < n; ++j) v[j] = key_val(key[j]);
+      first = 0;
+    }
+    int64_t m = INT64_MAX;
+    for (int32_t j = 0; j < n; ++j)
+      if (!rcol[j]) {
+        const int64_t s = key_val(key[j]) - v[j];
+        if (s < m) m = s;
+      }
+    if (m == INT64_MAX) { rc = -2; goto done; }
+    if (m > D) {
+      if (trace && dual_steps < trace_cap) {
+        trace[2 * dual_steps] = m - D;
+        trace[2 * dual_steps + 1] = nrows;
+      }
+      D = m;
+      ++dual_steps;
+    }
+    int32_t nfound = 0;
+    const int32_t ep = (int32_t)epochs;
+    for (int32_t j = 0; j < n; ++j) {
+      if (rcol[j] || key_val(key[j]) - v[j] != D) continue;
+      rcol[j] = 1;
+      dc[j] = D;
+      const int32_t p = key_row(key[j]);
+      tree_par[j] = p;
+      const int32_t root = root_row[p];
+      const int32_t i2 = match_col[j];
+      if (i2 < 0) {
+        if (claim[root] != ep || j < claim_col[root]) {
+          claim[root] = ep;
+          claim_col[root] = j;
+        }
+        found[nfound++] = j;
+      } else {
+        w[i2] = u[i2] - D;
+        root_row[i2] = root;
+        rrow[i2] = 1;
+        rows[nrows++] = i2;
+      }
+    }
+    if (!nfound) continue;
+    /* ---- epoch end: dissolve claimed trees ---- */
+    for (int32_t j = 0; j < n; ++j) {
+      if (rcol[j]) {
+        if (claim[root_row[tree_par[j]]] == ep) {
+          v[j] -= D - dc[j];
+          rcol[j] = 0;
+          key[j] = UINT64_MAX;
+        }
+      } else if (key[j] != UINT64_MAX && claim[root_row[key_row(key[j])]] == ep) {
+        key[j] = UINT64_MAX; /* dirty: argmin row leaves the search */
+      }
+    }
+    int32_t ns = 0;
+    for (int32_t r = 0; r < nrows; ++r) {
+      const int32_t i = rows[r];
+      if (claim[root_row[i]] == ep) {
+        u[i] = w[i] + D;
+        rrow[i] = 0;
+      } else {
+        nxt_rows[ns++] = i;
+      }
+    }
+    for (int32_t f = 0; f < nfound; ++f) {
+      int32_t j = found[f];
+      const int32_t root = root_row[tree_par[j]];
+      if (claim_col[root] != j) continue;
+      --nfree;
+      for (;;) {
+        const int32_t i = tree_par[j];
+        const int32_t nx = match_row[i];
+        match_row[i] = j;
+        match_col[j] = i;
+        if (nx < 0) break;
+        j = nx;
+      }
+    }
+    memcpy(rows, nxt_rows, sizeof(int32_t) * (size_t)ns);
+    nrows = ns;
+    head = 0; /* survivors relax once more for the reset columns */
+    ++epochs;
+  }
+  {
+    int64_t tot = 0;
+    for (int32_t i = 0; i < n; ++i) tot += C[(size_t)i * n + match_row[i]];
+    *total_cost = tot;
+  }
+  *epochs_out = epochs;
+  *dual_steps_out = dual_steps;
+  if (rows_scanned_out) *rows_scanned_out = rows_scanned;
+  if (rounds_out) *rounds_out = rounds;
+done:
+  free(match_col); free(key); free(w); free(dc); free(rcol); free(rrow); free(tree_par);
+  free(root_row); free(claim); free(claim_col); free(rows); free(nxt_rows); free(found);
+  return rc;
+}

@@ -44,7 +44,8 @@ class Stats(C.Structure):
     _fields_ = [("phases", C.c_int64), ("dual_steps", C.c_int64), ("rows_scanned", C.c_int64),
                 ("cost_bytes_read", C.c_int64), ("seconds", C.c_double),
                 ("converged", C.c_int32), ("engine", C.c_int32), ("rounds", C.c_int64),
-                ("stage_ns", C.c_int64 * 6)]
+                ("stage_ns", C.c_int64 * 6), ("max_instance_cycles", C.c_int64),
+                ("sum_instance_cycles", C.c_int64)]
 
 
 _lib = None

@@ -299,9 +299,12 @@ __global__ void __launch_bounds__(256) k_batch_solve(BatchArgs a) {
       a.total_cost[inst] = t;
       a.status[inst] = fatal ? -2 : 0;  // KMB_EINTERNAL
       if (a.stats) {
-        a.stats[3 * static_cast<int64_t>(inst) + 0] = phases;
-        a.stats[3 * static_cast<int64_t>(inst) + 1] = dual_steps;
-        a.stats[3 * static_cast<int64_t>(inst) + 2] = rows_scanned;
+        int64_t* o = a.stats + KMB_ISTATS * static_cast<int64_t>(inst);
+        o[0] = phases;
+        o[1] = dual_steps;
+        o[2] = rows_scanned;
+        o[3] = 0;
+        o[4] = 0;
       }
     }
     __syncthreads();

@@ -173,7 +173,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   if (!is_device_ptr(u)) { KMB_CUDA(c->bu.ensure(nb * 8)); du = c->bu.as<int64_t>(); }
   if (!is_device_ptr(v)) { KMB_CUDA(c->bv.ensure(nb * 8)); dv = c->bv.as<int64_t>(); }
   if (!is_device_ptr(total_cost)) { KMB_CUDA(c->btot.ensure(batch * 8)); dtot = c->btot.as<int64_t>(); }
-  KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * 3 * 8));
+  KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8));
   KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
   if (engine == 0 || engine == 1) engine = 4;  // auto: warp engine, costs from L2
   if (engine == 2 && n > kmb::batch_max_n()) engine = 4;
@@ -225,10 +225,11 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   if (dtot != total_cost) { int r = copy_out(total_cost, dtot, batch * 8, st); if (r) return r; }
   // status is always checked (one small copy): invalid input must not pass silently
   int32_t* hstatus = new int32_t[batch];
-  int64_t* hstat = stats ? new int64_t[static_cast<size_t>(batch) * 3] : nullptr;
+  int64_t* hstat = stats ? new int64_t[static_cast<size_t>(batch) * kmb::KMB_ISTATS] : nullptr;
   cudaError_t e = cudaMemcpyAsync(hstatus, c->bstatus.p, batch * 4, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess && hstat)
-    e = cudaMemcpyAsync(hstat, c->bstat.p, static_cast<size_t>(batch) * 24, cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(hstat, c->bstat.p, static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8,
+                        cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     delete[] hstatus;
@@ -241,9 +242,13 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
     for (int32_t b = 0; b < batch; ++b) {
-      stats->phases += hstat[3 * b];
-      stats->dual_steps += hstat[3 * b + 1];
-      stats->rows_scanned += hstat[3 * b + 2];
+      const int64_t* o = hstat + kmb::KMB_ISTATS * static_cast<size_t>(b);
+      stats->phases += o[0];
+      stats->dual_steps += o[1];
+      stats->rows_scanned += o[2];
+      stats->rounds += o[3];
+      stats->sum_instance_cycles += o[4];
+      if (o[4] > stats->max_instance_cycles) stats->max_instance_cycles = o[4];
     }
     stats->cost_bytes_read = static_cast<int64_t>(batch) * n * n * 4;  // HBM: each matrix once
     float ms = 0.f;

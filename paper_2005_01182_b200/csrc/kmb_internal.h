@@ -7,6 +7,10 @@
 
 namespace kmb {
 
+// per-instance stats of the batch engines: phases/epochs, dual steps, rows
+// scanned, rounds, SM cycles
+constexpr int KMB_ISTATS = 5;
+
 // Device control block of one single-instance solve.  Counters that are
 // recycled between phases are double-buffered by phase parity (see k_solve).
 struct Ctrl {
@@ -63,7 +67,7 @@ struct BatchArgs {
   int64_t* u;            // batch x n
   int64_t* v;            // batch x n
   int64_t* total_cost;   // batch
-  int64_t* stats;        // batch x 3: phases, dual_steps, rows_scanned (may be null)
+  int64_t* stats;        // batch x KMB_ISTATS (may be null)
   int32_t* status;       // batch (0 ok)
 };
 
@@ -85,7 +89,7 @@ struct WarpArgs {
   int64_t* u;            // batch x n
   int64_t* v;            // batch x n
   int64_t* total_cost;   // batch
-  int64_t* stats;        // batch x 3 (may be null)
+  int64_t* stats;        // batch x KMB_ISTATS (may be null)
   int32_t* status;       // batch
 };
 int warp_max_n();

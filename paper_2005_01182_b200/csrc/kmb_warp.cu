@@ -64,7 +64,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
       : "memory");
 }
 
-// claim word for n <= 256: smaller is better; stamp decreases with the phase
+// claim word for n <= 256: smaller is better; stamp decreases with the epoch
 __device__ __forceinline__ uint32_t wclaim(int phase, int col) {
   return (static_cast<uint32_t>(0xFFFFFE - phase) << 8) | static_cast<uint32_t>(col);
 }
@@ -77,41 +77,307 @@ struct RowVec {
   int32_t x[CPL];
 };
 
+// Loads the lane's CPL columns of one row; `avail` = pitch - c0 (elements left
+// in the padded row), chunks past it read as 0 (padding columns are masked).
 template <int CPL, bool SMEM_C>
-__device__ __forceinline__ RowVec<CPL> load_row(const int32_t* base) {
+__device__ __forceinline__ RowVec<CPL> load_row(const int32_t* base, int avail) {
   RowVec<CPL> r;
-  if constexpr (CPL == 4) {
-    int4 t;
-    if constexpr (SMEM_C) t = *reinterpret_cast<const int4*>(base);
-    else t = __ldg(reinterpret_cast<const int4*>(base));
-    r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
-  } else if constexpr (CPL == 8) {
-    int4 t0, t1;
-    if constexpr (SMEM_C) {
-      t0 = reinterpret_cast<const int4*>(base)[0];
-      t1 = reinterpret_cast<const int4*>(base)[1];
-    } else {
-      t0 = __ldg(reinterpret_cast<const int4*>(base));
-      t1 = __ldg(reinterpret_cast<const int4*>(base) + 1);
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) r.x[q] = 0;
+  if constexpr (CPL >= 4) {
+#pragma unroll
+    for (int h = 0; h < CPL / 4; ++h) {
+      if (4 * h < avail) {
+        const int4* p = reinterpret_cast<const int4*>(base) + h;
+        const int4 t = SMEM_C ? *p : __ldg(p);
+        r.x[4 * h + 0] = t.x; r.x[4 * h + 1] = t.y; r.x[4 * h + 2] = t.z; r.x[4 * h + 3] = t.w;
+      }
     }
-    r.x[0] = t0.x; r.x[1] = t0.y; r.x[2] = t0.z; r.x[3] = t0.w;
-    r.x[4] = t1.x; r.x[5] = t1.y; r.x[6] = t1.z; r.x[7] = t1.w;
   } else if constexpr (CPL == 2) {
-    int2 t;
-    if constexpr (SMEM_C) t = *reinterpret_cast<const int2*>(base);
-    else t = __ldg(reinterpret_cast<const int2*>(base));
-    r.x[0] = t.x; r.x[1] = t.y;
+    if (avail > 0) {
+      const int2* p = reinterpret_cast<const int2*>(base);
+      const int2 t = SMEM_C ? *p : __ldg(p);
+      r.x[0] = t.x; r.x[1] = t.y;
+    }
   } else {
-    r.x[0] = SMEM_C ? *base : __ldg(base);
+    if (avail > 0) r.x[0] = SMEM_C ? *base : __ldg(base);
   }
   return r;
 }
 
 }  // namespace
 
-// Per-warp shared state (n <= 256): u, w, root_row, match_row, match_col,
-// tree_par, claim, found, list[2]  -> 10 * n int32.
-__host__ __device__ constexpr int warp_state_words(int n) { return 10 * n; }
+// Per-warp shared state (n <= 256), in 32-bit words: u, w, root_row,
+// match_row, match_col, tree_par, claim, found (8n) + two row lists of
+// (row, tag) pairs (4n).
+__host__ __device__ constexpr int warp_state_words(int n) { return 12 * n; }
+
+// Column keys.  Wide: ((c - w + 2^30) << 32) | row (any n, costs < 2^29).
+// Narrow (n <= 256, costs < 2^21): ((c - w + 2^22) << 8) | row in 32 bits, so a
+// relaxation is one shift-add and one unsigned min.  A row's tag is fixed when
+// it is reached (w is constant while it stays reached): wide tag = 2^30 - w,
+// narrow tag = ((2^22 - w) << 8) | row.  Both orders are (value, row): the
+// same argmin and tie-breaking.
+template <bool NARROW>
+struct Keys;
+template <>
+struct Keys<false> {
+  using K = uint64_t;
+  static constexpr K INF = ~0ull;
+  __device__ static uint32_t tag(int32_t w, int32_t) {
+    return static_cast<uint32_t>(static_cast<int32_t>(KMB_BIAS) - w);
+  }
+  __device__ static K make(int32_t c, uint32_t tag, int32_t row) {
+    return (static_cast<uint64_t>(static_cast<uint32_t>(c) + tag) << 32) | static_cast<uint32_t>(row);
+  }
+  __device__ static int32_t val(K k) { return static_cast<int32_t>(static_cast<int64_t>(k >> 32) - KMB_BIAS); }
+  __device__ static int32_t row(K k) { return static_cast<int32_t>(static_cast<uint32_t>(k)); }
+  __device__ static K kmin(K a, K b) { return a < b ? a : b; }
+};
+template <>
+struct Keys<true> {
+  using K = uint32_t;
+  static constexpr K INF = 0xffffffffu;
+  static constexpr int32_t NB = 1 << 22;
+  __device__ static uint32_t tag(int32_t w, int32_t row) {
+    return (static_cast<uint32_t>(NB - w) << 8) | static_cast<uint32_t>(row);
+  }
+  __device__ static K make(int32_t c, uint32_t tag, int32_t) {
+    return (static_cast<uint32_t>(c) << 8) + tag;
+  }
+  __device__ static int32_t val(K k) { return static_cast<int32_t>(k >> 8) - NB; }
+  __device__ static int32_t row(K k) { return static_cast<int32_t>(k & 0xffu); }
+  __device__ static K kmin(K a, K b) { return min(a, b); }
+};
+
+struct WarpSmem {
+  int32_t *u, *w, *root_row, *match_row, *match_col, *tree_par, *found;
+  int32_t* ctr;  // [0] rows tail, [1] free columns found this epoch
+  uint32_t* claim;
+  int2 *rows, *spare;  // (row, tag)
+};
+
+// One instance, whole warp.  Returns the status (0 ok, -2 internal).
+template <int CPL, bool SMEM_C, bool NARROW>
+__device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* Cm, int inst,
+                                              const WarpSmem& S, int lane) {
+  using KO = Keys<NARROW>;
+  using K = typename KO::K;
+  constexpr uint32_t FULL = 0xffffffffu;
+  const int n = a.n, np = a.pitch;
+  const int c0 = CPL * lane;
+  const int avail = np - c0;
+  int32_t* const u = S.u;
+  int32_t* const w = S.w;
+  int32_t* const root_row = S.root_row;
+  int32_t* const match_row = S.match_row;
+  int32_t* const match_col = S.match_col;
+  int32_t* const tree_par = S.tree_par;
+  uint32_t* const claim = S.claim;
+  int32_t* const found = S.found;
+  int2* rows = S.rows;
+  int2* spare = S.spare;
+
+  for (int k = lane; k < n; k += 32) rows[k] = make_int2(k, KO::tag(w[k], k));
+  if (lane == 0) {
+    S.ctr[0] = n;
+    S.ctr[1] = 0;
+  }
+  K key[CPL];
+  int32_t v[CPL], dc[CPL];
+  uint32_t pad = 0;
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    v[q] = 0;
+    dc[q] = 0;
+    key[q] = KO::INF;
+    if (c0 + q >= n) pad |= 1u << q;
+  }
+  uint32_t rch = pad;  // bit q: column c0+q reached (padding counts as reached)
+  int nrows = n, head = 0, nfree = n;  // rows[0, nrows) reached; [head, nrows) to relax
+  int32_t D = 0;
+  int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
+  int status = 0;
+  const long long t_start = clock64();
+  __syncwarp();
+
+  while (nfree > 0) {
+    ++rounds;
+    // ---- relax rows[head, nrows)  (hungarian.cpp:164-172) ----
+    int r = head;
+    for (; r + 3 < nrows; r += 4) {
+      int2 e[4];
+      RowVec<CPL> cv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) e[k] = rows[r + k];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        cv[k] = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(e[k].x) * np + c0, avail);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), e[k].x));
+    }
+    for (; r < nrows; ++r) {
+      const int2 e = rows[r];
+      const RowVec<CPL> cv = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(e.x) * np + c0, avail);
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+        key[q] = KO::kmin(key[q], KO::make(cv.x[q], static_cast<uint32_t>(e.y), e.x));
+    }
+    rows_scanned += nrows - head;
+    head = nrows;
+    if (epochs == 0 && rounds == 1 && a.seed == 1) {  // column reduction, :328-333
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+        if (!((pad >> q) & 1)) v[q] = KO::val(key[q]);
+    }
+    // ---- min unreached slack' (hungarian.cpp:203-206) ----
+    int32_t s[CPL];
+    int32_t lm = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      s[q] = KO::val(key[q]) - v[q];
+      if (!((rch >> q) & 1)) lm = min(lm, s[q]);
+    }
+    const int32_t m = __reduce_min_sync(FULL, lm);
+    if (m > D) {
+      if (m == 0x7fffffff) {
+        status = -2;
+        break;
+      }
+      D = m;  // dual step (hungarian.cpp:207-215), applied lazily
+      ++dual_steps;
+    }
+    // ---- absorb zero-slack columns (hungarian.cpp:186-199) ----
+    // Usually one column per round turns tight: only its lane branches in, and
+    // appends go through warp-private shared counters (no per-column ballots).
+    uint32_t tm = 0;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+      if (!((rch >> q) & 1) && s[q] == D) tm |= 1u << q;
+    if (tm) {
+      rch |= tm;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        if (!((tm >> q) & 1)) continue;
+        const int col = c0 + q;
+        dc[q] = D;
+        const int32_t par = KO::row(key[q]);
+        tree_par[col] = par;
+        const int32_t root = root_row[par];
+        const int32_t i2 = match_col[col];
+        if (i2 < 0) {
+          atomicMin(claim + root, wclaim(epochs, col));
+          found[atomicAdd(S.ctr + 1, 1)] = col;
+        } else {
+          const int32_t w2 = u[i2] - D;
+          w[i2] = w2;
+          root_row[i2] = root;
+          rows[atomicAdd(S.ctr, 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
+        }
+      }
+    }
+    __syncwarp();
+    nrows = S.ctr[0];
+    const int nfound = S.ctr[1];
+    if (nfound == 0) continue;
+
+    // ---- epoch end: augment and dissolve the trees that reached a free column.
+    // Columns (lane-owned): finalise dissolved ones; reset keys whose argmin row
+    // leaves the search.
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      if ((pad >> q) & 1) continue;
+      const int col = c0 + q;
+      if ((rch >> q) & 1) {
+        if (wclaimed_in(claim[root_row[tree_par[col]]], epochs)) {
+          v[q] -= D - dc[q];
+          rch &= ~(1u << q);
+          key[q] = KO::INF;
+        }
+      } else if (key[q] != KO::INF && wclaimed_in(claim[root_row[KO::row(key[q])]], epochs)) {
+        key[q] = KO::INF;
+      }
+    }
+    // rows: finalise dissolved ones (u = w + D), compact the survivors
+    int ns = 0;
+    for (int rb = 0; rb < nrows; rb += 32) {
+      const int rr = rb + lane;
+      bool keep = false;
+      int2 e = make_int2(0, 0);
+      if (rr < nrows) {
+        e = rows[rr];
+        if (wclaimed_in(claim[root_row[e.x]], epochs)) u[e.x] = w[e.x] + D;
+        else keep = true;
+      }
+      const uint32_t km = __ballot_sync(FULL, keep);
+      if (keep) spare[ns + __popc(km & ((1u << lane) - 1))] = e;
+      ns += __popc(km);
+    }
+    __syncwarp();
+    // flip one parent-pointer path per claimed tree (its smallest free column)
+    int won = 0;
+    for (int fb = 0; fb < nfound; fb += 32) {
+      const int f = fb + lane;
+      bool winner = false;
+      if (f < nfound) {
+        int32_t j = found[f];
+        if (claim[root_row[tree_par[j]]] == wclaim(epochs, j)) {
+          winner = true;
+          for (;;) {
+            const int32_t i = tree_par[j];
+            const int32_t nx = match_row[i];
+            match_row[i] = j;
+            match_col[j] = i;
+            if (nx < 0) break;
+            j = nx;
+          }
+        }
+      }
+      won += __popc(__ballot_sync(FULL, winner));
+    }
+    if (lane == 0) {
+      S.ctr[0] = ns;
+      S.ctr[1] = 0;
+    }
+    __syncwarp();
+    nfree -= won;
+    int2* t = rows;
+    rows = spare;
+    spare = t;
+    nrows = ns;
+    head = 0;  // survivors relax once more for the reset columns
+    ++epochs;
+  }
+  const long long cycles = clock64() - t_start;
+  // ---- outputs ----
+  int64_t tot = 0;
+  for (int k = lane; k < n; k += 32) {
+    const int32_t mr = match_row[k];
+    a.row_to_col[static_cast<int64_t>(inst) * n + k] = mr;
+    a.u[static_cast<int64_t>(inst) * n + k] = u[k];
+    if (mr >= 0) tot += SMEM_C ? Cm[static_cast<int64_t>(k) * np + mr] : __ldg(Cm + static_cast<int64_t>(k) * np + mr);
+  }
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+    if (c0 + q < n) a.v[static_cast<int64_t>(inst) * n + c0 + q] = v[q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+  if (lane == 0) {
+    a.total_cost[inst] = tot;
+    if (a.stats) {
+      int64_t* o = a.stats + KMB_ISTATS * static_cast<int64_t>(inst);
+      o[0] = epochs;
+      o[1] = dual_steps;
+      o[2] = rows_scanned;
+      o[3] = rounds;
+      o[4] = cycles;
+    }
+  }
+  return status;
+}
 
 template <int CPL, bool SMEM_C>
 __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
@@ -122,27 +388,32 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
   const int n = a.n, np = a.pitch;
   constexpr uint32_t FULL = 0xffffffffu;
 
-  // carve this warp's slice
+  // carve this warp's slice: [mbarrier | C (SMEM_C) | state]
   const size_t cbytes = SMEM_C ? static_cast<size_t>(n) * np * 4 : 0;
   const size_t wbytes = cbytes + static_cast<size_t>(warp_state_words(n)) * 4 + 16;
   unsigned char* base = dyn + wib * ((wbytes + 15) & ~static_cast<size_t>(15));
   uint64_t* bar = reinterpret_cast<uint64_t*>(base);
+  int32_t* ctr = reinterpret_cast<int32_t*>(base + 8);  // 2 counters after the mbarrier
   int32_t* Cs = reinterpret_cast<int32_t*>(base + 16);
   int32_t* st = reinterpret_cast<int32_t*>(base + 16 + cbytes);
-  int32_t* u = st;
-  int32_t* w = u + n;
-  int32_t* root_row = w + n;
-  int32_t* match_row = root_row + n;
-  int32_t* match_col = match_row + n;
-  int32_t* tree_par = match_col + n;
-  uint32_t* claim = reinterpret_cast<uint32_t*>(tree_par + n);
-  int32_t* found = reinterpret_cast<int32_t*>(claim + n);
-  int32_t* lists = found + n;
+  WarpSmem S;
+  S.rows = reinterpret_cast<int2*>(st);  // 8-byte aligned first
+  S.spare = S.rows + n;
+  S.u = reinterpret_cast<int32_t*>(S.spare + n);
+  S.w = S.u + n;
+  S.root_row = S.w + n;
+  S.match_row = S.root_row + n;
+  S.match_col = S.match_row + n;
+  S.tree_par = S.match_col + n;
+  S.claim = reinterpret_cast<uint32_t*>(S.tree_par + n);
+  S.found = reinterpret_cast<int32_t*>(S.claim + n);
+  S.ctr = ctr;
 
   if (SMEM_C && lane == 0) mbar_init1(bar);
   __syncwarp();
   uint32_t parity = 0;
-  const int c0 = CPL * lane;  // first owned column
+  const int c0 = CPL * lane;
+  const int avail = np - c0;
 
   for (int inst = blockIdx.x * wpb + wib; inst < a.batch; inst += gridDim.x * wpb) {
     const int32_t* Cg = a.C + static_cast<int64_t>(inst) * n * np;
@@ -161,11 +432,10 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
       Cm = Cs;
     }
     for (int k = lane; k < n; k += 32) {
-      match_row[k] = -1;
-      match_col[k] = -1;
-      claim[k] = 0xFFFFFFFFu;
-      root_row[k] = k;
-      lists[k] = k;
+      S.match_row[k] = -1;
+      S.match_col[k] = -1;
+      S.claim[k] = 0xFFFFFFFFu;
+      S.root_row[k] = k;
     }
     if constexpr (SMEM_C) {
       mbar_wait_parity(bar, parity);
@@ -176,7 +446,7 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
     // (hungarian.cpp:323-327): the warp walks the rows, lanes across columns
     int32_t lo_all = 0x7fffffff, hi_all = 0;
     for (int i = 0; i < n; ++i) {
-      const RowVec<CPL> cv = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(i) * np + c0);
+      const RowVec<CPL> cv = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(i) * np + c0, avail);
       int32_t lo = 0x7fffffff, hi = 0;
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
@@ -189,198 +459,21 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
       hi_all = max(hi_all, hi);
       if (lane == (i & 31)) {
         const int32_t u0 = a.seed == 1 ? lo : 0;
-        u[i] = u0;
-        w[i] = u0;
+        S.u[i] = u0;
+        S.w[i] = u0;
       }
     }
     hi_all = __reduce_max_sync(FULL, hi_all);
-    const int32_t bad = lo_all < 0 ? 2 : (hi_all >= (1 << 29) ? 3 : 0);
-    if (bad) {
-      for (int k = lane; k < n; k += 32) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
-      if (lane == 0) {
-        a.status[inst] = bad;
-        a.total_cost[inst] = 0;
-      }
-      __syncwarp();
-      continue;
-    }
+    int status = lo_all < 0 ? 2 : (hi_all >= (1 << 29) ? 3 : 0);
     __syncwarp();
-
-    uint64_t key[CPL];
-    int32_t v[CPL], dc[CPL];
-    uint32_t rch = 0;  // bit q: column c0+q reached (or padding)
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) v[q] = 0;
-    int32_t* list = lists;
-    int32_t* next = lists + n;
-    int nroots = n;
-    int phases = 0, dual_steps = 0, rows_scanned = 0;
-    bool fatal = false;
-
-    for (int phase = 0; nroots > 0; ++phase) {
-      uint32_t pad = 0;
-#pragma unroll
-      for (int q = 0; q < CPL; ++q) {
-        key[q] = KMB_KEY_INF;
-        if (c0 + q >= n) pad |= 1u << q;
-      }
-      rch = pad;
-      int32_t D = 0;
-      int head = 0, tail = nroots, nfound = 0;
-      for (int round = 0;; ++round) {
-        // ---- relax rows list[head, tail)  (hungarian.cpp:164-172) ----
-        int r = head;
-        for (; r + 3 < tail; r += 4) {
-          int32_t ii[4];
-          uint32_t bb[4];
-          RowVec<CPL> cv[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            ii[k] = list[r + k];
-            bb[k] = static_cast<uint32_t>(static_cast<int32_t>(KMB_BIAS) - w[ii[k]]);
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            cv[k] = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(ii[k]) * np + c0);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int q = 0; q < CPL; ++q)
-              key[q] = umin64(key[q], pack_key(static_cast<uint32_t>(cv[k].x[q]) + bb[k], ii[k]));
-        }
-        for (; r < tail; ++r) {
-          const int32_t i = list[r];
-          const uint32_t b = static_cast<uint32_t>(static_cast<int32_t>(KMB_BIAS) - w[i]);
-          const RowVec<CPL> cv = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(i) * np + c0);
-#pragma unroll
-          for (int q = 0; q < CPL; ++q)
-            key[q] = umin64(key[q], pack_key(static_cast<uint32_t>(cv.x[q]) + b, i));
-        }
-        rows_scanned += tail - head;
-        if (phase == 0 && round == 0 && a.seed == 1) {  // column reduction, :328-333
-#pragma unroll
-          for (int q = 0; q < CPL; ++q)
-            if (!((pad >> q) & 1)) v[q] = static_cast<int32_t>(key_val(key[q]));
-        }
-        // ---- min unreached slack' (hungarian.cpp:203-206) ----
-        int32_t s[CPL];
-        int32_t lm = 0x7fffffff;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          s[q] = static_cast<int32_t>(key_val(key[q])) - v[q];
-          if (!((rch >> q) & 1)) lm = min(lm, s[q]);
-        }
-        const int32_t m = __reduce_min_sync(FULL, lm);
-        if (m > D) {
-          if (nfound > 0) break;  // closure exhausted (continue_bfs)
-          if (m == 0x7fffffff) {
-            fatal = true;
-            break;
-          }
-          D = m;  // dual step (hungarian.cpp:207-215), applied lazily
-          ++dual_steps;
-        }
-        // ---- absorb zero-slack columns (hungarian.cpp:186-199) ----
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          const bool tight = !((rch >> q) & 1) && s[q] == D;
-          bool newrow = false, newfree = false;
-          int32_t i2 = -1;
-          const int col = c0 + q;
-          if (tight) {
-            rch |= 1u << q;
-            dc[q] = D;
-            const int32_t par = key_row(key[q]);
-            tree_par[col] = par;
-            const int32_t root = root_row[par];
-            i2 = match_col[col];
-            if (i2 < 0) {
-              newfree = true;
-              atomicMin(claim + root, wclaim(phase, col));
-            } else {
-              newrow = true;
-              w[i2] = u[i2] - D;
-              root_row[i2] = root;
-            }
-          }
-          const uint32_t rm = __ballot_sync(FULL, newrow);
-          if (newrow) list[tail + __popc(rm & ((1u << lane) - 1))] = i2;
-          tail += __popc(rm);
-          const uint32_t fm = __ballot_sync(FULL, newfree);
-          if (newfree) found[nfound + __popc(fm & ((1u << lane) - 1))] = col;
-          nfound += __popc(fm);
-        }
-        __syncwarp();
-        head = r;  // == old tail
-        if (nfound > 0 && (!a.continue_bfs || head == tail)) break;
-      }
-      if (fatal) break;
-      // ---- end of phase: finalise duals, next free rows, flips ----
-      int nnext = 0;
-      for (int rb = 0; rb < tail; rb += 32) {
-        const int rr = rb + lane;
-        bool keep = false;
-        int32_t i = 0;
-        if (rr < tail) {
-          i = list[rr];
-          const int32_t un = w[i] + D;
-          u[i] = un;
-          if (rr < nroots && !wclaimed_in(claim[i], phase)) {
-            keep = true;
-            w[i] = un;
-            root_row[i] = i;
-          }
-        }
-        const uint32_t km = __ballot_sync(FULL, keep);
-        if (keep) next[nnext + __popc(km & ((1u << lane) - 1))] = i;
-        nnext += __popc(km);
-      }
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-        if (((rch >> q) & 1) && !((pad >> q) & 1)) v[q] -= D - dc[q];
-      __syncwarp();
-      for (int f = lane; f < nfound; f += 32) {
-        int32_t j = found[f];
-        const int32_t root = root_row[tree_par[j]];
-        if (claim[root] != wclaim(phase, j)) continue;
-        for (;;) {
-          const int32_t i = tree_par[j];
-          const int32_t nx = match_row[i];
-          match_row[i] = j;
-          match_col[j] = i;
-          if (nx < 0) break;
-          j = nx;
-        }
-      }
-      __syncwarp();
-      int32_t* t = list;
-      list = next;
-      next = t;
-      nroots = nnext;
-      ++phases;
+    if (status == 0) {
+      status = hi_all < (1 << 21) ? solve_instance<CPL, SMEM_C, true>(a, Cm, inst, S, lane)
+                                  : solve_instance<CPL, SMEM_C, false>(a, Cm, inst, S, lane);
+    } else {
+      for (int k = lane; k < n; k += 32) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
+      if (lane == 0) a.total_cost[inst] = 0;
     }
-    // ---- outputs ----
-    int64_t tot = 0;
-    for (int k = lane; k < n; k += 32) {
-      const int32_t mr = match_row[k];
-      a.row_to_col[static_cast<int64_t>(inst) * n + k] = mr;
-      a.u[static_cast<int64_t>(inst) * n + k] = u[k];
-      if (mr >= 0) tot += SMEM_C ? Cs[static_cast<int64_t>(k) * np + mr] : __ldg(Cg + static_cast<int64_t>(k) * np + mr);
-    }
-#pragma unroll
-    for (int q = 0; q < CPL; ++q)
-      if (c0 + q < n) a.v[static_cast<int64_t>(inst) * n + c0 + q] = v[q];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
-    if (lane == 0) {
-      a.total_cost[inst] = tot;
-      a.status[inst] = fatal ? -2 : 0;
-      if (a.stats) {
-        a.stats[3 * static_cast<int64_t>(inst) + 0] = phases;
-        a.stats[3 * static_cast<int64_t>(inst) + 1] = dual_steps;
-        a.stats[3 * static_cast<int64_t>(inst) + 2] = rows_scanned;
-      }
-    }
+    if (lane == 0) a.status[inst] = status;
     __syncwarp();
   }
 }
