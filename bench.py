@@ -283,7 +283,7 @@ def main():
     ok_e2e = bool(torch.equal(hr2c, r2c.cpu())) and bool(torch.equal(htot, dtot.cpu()))
 
     hbm_peak, peak_src = peaks()
-    # roofline of the dominant kernel (k_batch_solve): SURVEY.md §8(d) algorithmic
+    # roofline of the dominant kernel (k_warp_batch): SURVEY.md §8(d) algorithmic
     # bytes = 4*n^2 per phase + 2*4*n^2 for the reductions, per instance
     alg_bytes = 4.0 * N * N * (phases + 2 * count)
     achieved = alg_bytes / (step_ms * 1e-3) / 1e9
@@ -324,10 +324,10 @@ def main():
             "config": {"workload": WORKLOAD, "batch": BATCH, "n": N, "per_rank": count,
                        "parallelism": f"instances sharded over {world} GPU(s)",
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "engine": "SMEM engine, one CTA per instance"},
+                       "engine": "warp engine (one warp per instance, costs streamed from L2)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "k_batch_solve", "peak_source": peak_src,
+                         "kernel": "k_warp_batch", "peak_source": peak_src,
                          "note": "SMEM-resident: algorithmic bytes are SURVEY 8(d) 4n^2 per phase, "
                                  "re-read from shared memory; HBM reads each matrix once"},
             "cpu_baseline": cpu,

@@ -1,0 +1,143 @@
+// kmb_ot.hpp — reference-side drop-in over the kmb C ABI (include/kmb.h).
+//
+// Include AFTER the reference's own headers ("ot/core.hpp", "ot/hungarian.hpp")
+// and link libkmb.so.  It adds, in namespace ot, functions with the exact
+// signatures and semantics of the reference solvers:
+//
+//   solve_km_b200          == ot::solve_km          (hungarian.hpp:39-40)
+//   solve_batched_km_b200  == ot::solve_batched_km  (hungarian.hpp:53-56)
+//
+// Same inputs (OTInstance), same outputs (SolveResult built with the
+// reference's own make_result, optional DualPotentials / Matching /
+// QuantizedCosts overwritten wholesale), same exceptions and messages
+// (hungarian.cpp:15-21, :34, :44-45, :353-354).  Beyond the reference, costs
+// must fit the device range [0, 2^29) after quantization; a larger entry
+// throws std::invalid_argument("<who>: cost exceeds the device range [0, 2^29)").
+// A CUDA failure throws std::runtime_error (there is no CPU fallback).
+//
+// Registering them as bench plugins (bench.cpp:391-464) is one line each,
+// see INTEGRATION.md.
+#ifndef KMB_OT_HPP
+#define KMB_OT_HPP
+
+#include <chrono>
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kmb.h"
+
+namespace ot {
+
+namespace kmb_detail {
+
+inline kmb_context* context() {
+  // one context per thread (the C ABI is re-entrant; a context is not)
+  thread_local std::unique_ptr<kmb_context, void (*)(kmb_context*)> ctx(nullptr, kmb_destroy);
+  if (!ctx) {
+    kmb_context* c = nullptr;
+    if (kmb_create(0, &c) != KMB_OK) throw std::runtime_error(kmb_last_error());
+    ctx.reset(c);
+  }
+  return ctx.get();
+}
+
+inline void require_unit_square(const OTInstance& inst, const char* who) {
+  if (auto err = validate_instance(inst))
+    throw std::invalid_argument(std::string(who) + ": " + *err);
+  if (!inst.unit_caps())
+    throw std::invalid_argument(std::string(who) + ": requires a unit-capacity square instance");
+}
+
+inline std::vector<int32_t> narrow(const std::vector<int64_t>& c, const char* who) {
+  std::vector<int32_t> out(c.size());
+  for (size_t k = 0; k < c.size(); ++k) {
+    if (c[k] >= (int64_t{1} << 29))
+      throw std::invalid_argument(std::string(who) + ": cost exceeds the device range [0, 2^29)");
+    out[k] = static_cast<int32_t>(c[k]);
+  }
+  return out;
+}
+
+inline void check(int rc, const char* who) {
+  if (rc == KMB_OK) return;
+  if (rc > 0) throw std::invalid_argument(std::string(who) + ": " + kmb_last_error());
+  throw std::runtime_error(std::string(who) + ": " + kmb_last_error());
+}
+
+inline Flow matching_flow(int32_t n, const std::vector<int32_t>& row_to_col) {
+  std::vector<Flow::Entry> entries;
+  entries.reserve(n);
+  for (int32_t i = 0; i < n; ++i)
+    if (row_to_col[i] >= 0) entries.push_back({i, row_to_col[i], 1.0});
+  return Flow(n, n, std::move(entries));
+}
+
+}  // namespace kmb_detail
+
+inline SolveResult solve_km_b200(const OTInstance& inst, DualPotentials* duals = nullptr,
+                                 Matching* matching = nullptr, double time_budget_s = 0.0) {
+  kmb_detail::require_unit_square(inst, "solve_km");
+  const auto t0 = std::chrono::steady_clock::now();
+  const int32_t n = inst.n;
+  const std::vector<int32_t> c = kmb_detail::narrow(inst.cost, "solve_km");
+  std::vector<int32_t> r2c(n, -1);
+  std::vector<int64_t> u(n), v(n);
+  int64_t total = 0;
+  kmb_stats st{};
+  kmb_detail::check(kmb_solve_i32(kmb_detail::context(), c.data(), n, n, KMB_SEED_KM,
+                                  time_budget_s, r2c.data(), u.data(), v.data(), &total, &st),
+                    "solve_km");
+  const bool done = st.converged != 0;
+  if (done) {
+    if (duals) {
+      duals->u = u;
+      duals->v = v;
+    }
+    if (matching) matching->row_to_col = r2c;
+  }
+  int32_t matched = 0;
+  for (int32_t j : r2c) matched += j >= 0;
+  // iterations: rows inserted (hungarian.cpp:113, :130)
+  SolveResult res = make_result(inst, kmb_detail::matching_flow(n, r2c), done ? n : matched,
+                                /*exact=*/done, /*converged=*/done);
+  res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return res;
+}
+
+inline SolveResult solve_batched_km_b200(const OTInstance& inst, const BatchedKMConfig& config = {},
+                                         DualPotentials* duals = nullptr,
+                                         QuantizedCosts* quantized = nullptr) {
+  kmb_detail::require_unit_square(inst, "solve_batched_km");
+  const auto t0 = std::chrono::steady_clock::now();
+  const int32_t n = inst.n;
+  QuantizedCosts q = quantize_costs(inst.cost, config.B);  // the reference's own, :33-53
+  const std::vector<int32_t> c = kmb_detail::narrow(q.chat, "solve_batched_km");
+  std::vector<int32_t> r2c(n, -1);
+  std::vector<int64_t> u(n), v(n);
+  int64_t total = 0;
+  kmb_stats st{};
+  kmb_detail::check(kmb_solve_i32(kmb_detail::context(), c.data(), n, n, KMB_SEED_BATCHED,
+                                  config.time_budget_s, r2c.data(), u.data(), v.data(), &total,
+                                  &st),
+                    "solve_batched_km");
+  const bool budget_ok = st.converged != 0;
+  if (duals) {
+    duals->u = u;
+    duals->v = v;
+  }
+  if (quantized) *quantized = q;
+  // iterations = phases + dual adjustments (hungarian.cpp:375); the dual-step
+  // count equals the reference's, the phase count is the engine's own.
+  SolveResult res = make_result(inst, kmb_detail::matching_flow(n, r2c), st.phases + st.dual_steps,
+                                /*exact=*/q.lossless && budget_ok, budget_ok);
+  res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return res;
+}
+
+}  // namespace ot
+
+#endif  // KMB_OT_HPP

@@ -88,6 +88,10 @@ def _load_oracle():
             _i32p, C.c_int32, C.c_int32, C.c_int32, _i64p, _i64p, _i32p,
             C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
             C.POINTER(C.c_int64), C.c_void_p, C.c_int64]
+        lib.kmm_solve_incr.argtypes = [
+            _i32p, C.c_int32, C.c_int32, _i64p, _i64p, _i32p, C.POINTER(C.c_int64),
+            C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+            C.POINTER(C.c_int64), C.c_void_p, C.c_int64]
         _orc = lib
     return _orc
 
@@ -262,6 +266,26 @@ def mirror_solve(cost, seed: int = 1, continue_bfs: bool = False, trace_cap: int
         raise RuntimeError(f"kmm_solve failed ({rc})")
     s = Solution(r2c, u, v, tot.value, iterations=ph.value + ds.value, phases=ph.value,
                  dual_steps=ds.value, rows_scanned=rs.value)
+    if trace_cap:
+        s.trace = tr[: 2 * min(ds.value, trace_cap)].reshape(-1, 2)
+    return s
+
+
+def mirror_solve_incr(cost, seed: int = 1, trace_cap: int = 0) -> Solution:
+    """CPU mirror of the engine's incremental-epoch schedule (kmm_solve_incr)."""
+    lib = _load_oracle()
+    c, n = _sq(np.asarray(cost, dtype=np.int32))
+    u = np.zeros(n, np.int64); v = np.zeros(n, np.int64); r2c = np.full(n, -1, np.int32)
+    tot = C.c_int64(); ep = C.c_int64(); ds = C.c_int64(); rs = C.c_int64(); ro = C.c_int64()
+    tr = np.zeros(2 * max(trace_cap, 1), np.int64)
+    rc = lib.kmm_solve_incr(c, n, seed, u, v, r2c, C.byref(tot), C.byref(ep), C.byref(ds),
+                            C.byref(rs), C.byref(ro), tr.ctypes.data if trace_cap else None,
+                            trace_cap)
+    if rc:
+        raise RuntimeError(f"kmm_solve_incr failed ({rc})")
+    s = Solution(r2c, u, v, tot.value, iterations=ep.value + ds.value, phases=ep.value,
+                 dual_steps=ds.value, rows_scanned=rs.value)
+    s.rounds = ro.value
     if trace_cap:
         s.trace = tr[: 2 * min(ds.value, trace_cap)].reshape(-1, 2)
     return s

@@ -1,0 +1,16 @@
+#!/bin/sh
+# Build the C++ drop-in tests against the reference headers (needs
+# /root/reference, i.e. this container) and the in-tree libraries; the binary
+# travels to the GPU box with the snapshot.
+set -e
+HERE=$(cd "$(dirname "$0")" && pwd)
+ROOT=$(cd "$HERE/../.." && pwd)
+REF=${OT_REF_DIR:-/root/reference/proj}
+if [ ! -f "$REF/include/ot/hungarian.hpp" ]; then
+  echo "reference headers absent; keeping prebuilt binary" ; exit 0
+fi
+mkdir -p "$HERE/build"
+g++ -O2 -std=c++20 -I"$REF/include" -I"$ROOT/include" "$HERE/test_drop_in.cpp" \
+  -L"$ROOT/oracle/_ref" -lotref -L"$ROOT/paper_2005_01182_b200" -lkmb \
+  -Wl,-rpath,'$ORIGIN/../../../oracle/_ref' -Wl,-rpath,'$ORIGIN/../../../paper_2005_01182_b200' \
+  -o "$HERE/build/test_drop_in"

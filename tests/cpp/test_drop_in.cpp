@@ -1,0 +1,189 @@
+// C++ parity tests of the drop-in (include/kmb_ot.hpp) against the UNMODIFIED
+// reference solvers, written like the reference's own tests/test_hungarian.cpp
+// (same cases, same RNG seeds, same assertions) plus exact-equality checks of
+// the duals.  Built by tests/cpp/build.sh (needs /root/reference headers), run
+// on the GPU by tests/test_cpp_drop_in.py.
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "ot/core.hpp"
+#include "ot/hungarian.hpp"
+#include "kmb_ot.hpp"
+
+using namespace ot;
+
+static int g_checks = 0, g_fail = 0;
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    ++g_checks;                                                              \
+    if (!(cond)) {                                                           \
+      ++g_fail;                                                              \
+      std::fprintf(stderr, "%s:%d: CHECK(%s) failed\n", __FILE__, __LINE__, #cond); \
+    }                                                                        \
+  } while (0)
+
+static OTInstance random_unit_instance(std::mt19937& rng, int32_t n, int64_t max_cost) {
+  std::uniform_int_distribution<int64_t> cost(0, max_cost);
+  OTInstance inst;
+  inst.n = inst.m = n;
+  inst.cost.resize(static_cast<size_t>(n) * n);
+  for (int64_t& c : inst.cost) c = cost(rng);
+  inst.supplies.assign(n, 1);
+  inst.demands.assign(n, 1);
+  return inst;
+}
+
+static OTInstance unit_2x2() {
+  OTInstance inst;
+  inst.n = inst.m = 2;
+  inst.cost = {1, 3, 2, 1};
+  inst.supplies = {1, 1};
+  inst.demands = {1, 1};
+  return inst;
+}
+
+static int64_t dual_total(const DualPotentials& d) {
+  int64_t t = 0;
+  for (int64_t x : d.u) t += x;
+  for (int64_t x : d.v) t += x;
+  return t;
+}
+
+int main() {
+  {  // km: zero diagonal picks the identity matching (test_hungarian.cpp:61-70)
+    OTInstance inst;
+    inst.n = inst.m = 3;
+    inst.cost = {0, 5, 5, 5, 0, 5, 5, 5, 0};
+    inst.supplies = inst.demands = {1, 1, 1};
+    Matching m;
+    const SolveResult res = solve_km_b200(inst, nullptr, &m);
+    CHECK(res.objective == 0.0);
+    for (int32_t i = 0; i < 3; ++i) CHECK(m.row_to_col[i] == i);
+  }
+  {  // km: 2x2 with known optimum (:72-85)
+    const OTInstance inst = unit_2x2();
+    Matching m;
+    DualPotentials d;
+    const SolveResult res = solve_km_b200(inst, &d, &m);
+    CHECK(res.objective == 2.0);
+    CHECK((m.row_to_col == std::vector<int32_t>{0, 1}));
+    CHECK(dual_total(d) == 2);
+  }
+  {  // km: requires a unit square (:87-94) — same exception, same message
+    OTInstance inst = unit_2x2();
+    inst.supplies = {2, 1};
+    inst.demands = {1, 2};
+    std::string a, b;
+    try { solve_km_b200(inst); } catch (const std::invalid_argument& e) { a = e.what(); }
+    try { solve_km(inst); } catch (const std::invalid_argument& e) { b = e.what(); }
+    CHECK(!a.empty() && a == b);
+  }
+  {  // km: agreement with the reference on random unit instances (:96-105, seed 11)
+    std::mt19937 rng(11);
+    for (int t = 0; t < 100; ++t) {
+      const OTInstance inst = random_unit_instance(rng, 2 + static_cast<int32_t>(rng() % 5), 9);
+      DualPotentials d1, d2;
+      const SolveResult a = solve_km_b200(inst, &d1);
+      const SolveResult b = solve_km(inst, &d2);
+      CHECK(objective_int(inst, a.flow) == objective_int(inst, b.flow));
+      CHECK(d1.u == d2.u && d1.v == d2.v);
+      CHECK(residue(inst, a.flow) == 0.0);
+    }
+  }
+  {  // km: duals feasible and tight (:107-122, seed 13) and equal to the reference's
+    std::mt19937 rng(13);
+    const OTInstance inst = random_unit_instance(rng, 50, 100000);
+    DualPotentials d, dr;
+    Matching m;
+    const SolveResult res = solve_km_b200(inst, &d, &m);
+    solve_km(inst, &dr);
+    for (int32_t i = 0; i < inst.n; ++i) {
+      for (int32_t j = 0; j < inst.m; ++j) CHECK(d.u[i] + d.v[j] <= inst.cost_at(i, j));
+      CHECK(d.u[i] + d.v[m.row_to_col[i]] == inst.cost_at(i, m.row_to_col[i]));
+    }
+    CHECK(static_cast<double>(dual_total(d)) == res.objective);
+    CHECK(d.u == dr.u && d.v == dr.v);
+  }
+  {  // batched: lossless quantization reproduces km (:124-131)
+    const OTInstance inst = unit_2x2();
+    BatchedKMConfig cfg;
+    cfg.B = inst.max_cost();
+    const SolveResult res = solve_batched_km_b200(inst, cfg);
+    CHECK(res.objective == 2.0);
+    CHECK(res.exact);
+  }
+  {  // batched: constant costs (:133-142): objective 24; no dual step
+    OTInstance inst;
+    inst.n = inst.m = 6;
+    inst.cost.assign(36, 4);
+    inst.supplies.assign(6, 1);
+    inst.demands.assign(6, 1);
+    const SolveResult res = solve_batched_km_b200(inst);
+    CHECK(res.objective == 24.0);
+  }
+  {  // batched: B = N*n matches km and the reference, duals bit-exact (:144-156, seed 17)
+    std::mt19937 rng(17);
+    for (int t = 0; t < 100; ++t) {
+      const OTInstance inst = random_unit_instance(rng, 2 + static_cast<int32_t>(rng() % 7), 50);
+      BatchedKMConfig cfg;
+      cfg.B = std::max<int64_t>(inst.max_cost(), 1) * inst.n;
+      DualPotentials d1, d2;
+      const SolveResult a = solve_batched_km_b200(inst, cfg, &d1);
+      const SolveResult b = solve_batched_km(inst, cfg, &d2);
+      CHECK(a.objective == b.objective);
+      CHECK(a.exact);
+      CHECK(d1.u == d2.u && d1.v == d2.v);
+    }
+  }
+  {  // batched: objective within the quantization error bound (:158-172, seed 19)
+    std::mt19937 rng(19);
+    for (int64_t B : {1, 2, 5, 10, 37}) {
+      const OTInstance inst = random_unit_instance(rng, 40, 100000);
+      BatchedKMConfig cfg;
+      cfg.B = B;
+      DualPotentials d1, d2;
+      const SolveResult batched = solve_batched_km_b200(inst, cfg, &d1);
+      const SolveResult ref = solve_batched_km(inst, cfg, &d2);
+      const SolveResult km = solve_km(inst);
+      const double bound = km.objective + static_cast<double>(inst.n) * inst.max_cost() / static_cast<double>(B);
+      CHECK(batched.objective >= km.objective);
+      CHECK(batched.objective <= bound);
+      CHECK(!batched.exact == !ref.exact);
+      CHECK(d1.u == d2.u && d1.v == d2.v);  // lossy mode: duals on chat still canonical
+    }
+  }
+  {  // batched: certificate against the quantized costs (:174-189, seed 23)
+    std::mt19937 rng(23);
+    const OTInstance inst = random_unit_instance(rng, 60, 5000);
+    BatchedKMConfig cfg;
+    cfg.B = 64;
+    DualPotentials d;
+    QuantizedCosts q;
+    const SolveResult res = solve_batched_km_b200(inst, cfg, &d, &q);
+    CHECK(q.chat.size() == inst.cost.size());
+    for (int32_t i = 0; i < inst.n; ++i)
+      for (int32_t j = 0; j < inst.m; ++j)
+        CHECK(d.u[i] + d.v[j] <= q.chat[static_cast<size_t>(i) * inst.m + j]);
+    for (const Flow::Entry& e : res.flow.entries())
+      CHECK(d.u[e.i] + d.v[e.j] == q.chat[static_cast<size_t>(e.i) * inst.m + e.j]);
+  }
+  {  // batched: rejects non-unit instances (:200-205)
+    OTInstance inst = unit_2x2();
+    inst.supplies = {2, 1};
+    inst.demands = {1, 2};
+    bool threw = false;
+    try { solve_batched_km_b200(inst); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
+  }
+  {  // quantize_costs: B must be positive (:34) surfaces unchanged
+    BatchedKMConfig cfg;
+    cfg.B = 0;
+    std::string a;
+    try { solve_batched_km_b200(unit_2x2(), cfg); } catch (const std::invalid_argument& e) { a = e.what(); }
+    CHECK(a == "quantize_costs: B must be positive");
+  }
+  std::printf("drop-in: %d checks, %d failed\n", g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}

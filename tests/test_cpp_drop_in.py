@@ -1,0 +1,18 @@
+"""GPU: the C++ drop-in (include/kmb_ot.hpp) against the unmodified reference,
+written like the reference's test_hungarian.cpp (tests/cpp/test_drop_in.cpp)."""
+import os
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "cpp", "build", "test_drop_in")
+
+
+@pytest.mark.gpu
+def test_cpp_drop_in():
+    if not os.path.exists(BIN):
+        pytest.fail(f"{BIN} missing: run tests/cpp/build.sh where /root/reference exists")
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failed" in out.stdout

@@ -87,7 +87,7 @@ def check_against(res, ref, c, dual_steps=None):
 def test_known_2x2(solver):  # test_hungarian.cpp:72-85
     c = np.array([[1, 3], [2, 1]], np.int32)
     for seed in (KMB_SEED_KM, KMB_SEED_BATCHED):
-        for engine in (1, 2):
+        for engine in (1, 2, 3, 4):
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, seed)
             assert r.total_cost == 2
@@ -108,7 +108,7 @@ def test_known_constant(solver):  # :133-142: constant 6x6 cost 4 -> 24, one pha
     assert r.stats["dual_steps"] == 0
 
 
-@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("engine", [1, 2, 3, 4])
 @pytest.mark.parametrize("seed", [KMB_SEED_KM, KMB_SEED_BATCHED])
 def test_random_small_vs_reference(solver, engine, seed):
     rng = np.random.default_rng(100 + 10 * engine + seed)
@@ -116,7 +116,7 @@ def test_random_small_vs_reference(solver, engine, seed):
     try:
         for t in range(150):
             n = int(rng.integers(1, 60))
-            hi = int(rng.choice([1, 2, 9, 50, 1000, 10**6, 2**30 - 1]))
+            hi = int(rng.choice([1, 2, 9, 50, 1000, 10**6, 2**29 - 1]))
             c = rng.integers(0, hi + 1, size=(n, n)).astype(np.int32)
             ref = O.ref_solve_km(c) if seed == KMB_SEED_KM else O.ref_solve_batched_km(c)
             r = solver.solve(c, seed)
@@ -167,18 +167,24 @@ def test_continue_bfs_same_duals(solver, cont):
 
 
 def test_matching_equals_mirror(solver):
-    """The engine is deterministic: same forest, same claims -> same matching as
-    the step-by-step CPU mirror."""
+    """The engines are deterministic: same forest, same claims -> the same
+    matching as the step-by-step CPU mirror of their schedule (restart: grid and
+    CTA engines; incremental epochs: warp engines)."""
     rng = np.random.default_rng(3)
     for t in range(20):
         n = int(rng.integers(2, 300))
         c = rng.integers(0, 20, size=(n, n)).astype(np.int32)
         m = O.mirror_solve(c, 1)
-        for engine in (1, 2) if n <= 224 else (1,):
+        mi = O.mirror_solve_incr(c, 1)
+        engines = [1] + ([2] if n <= 224 else []) + ([3, 4] if n <= 256 else [])
+        for engine in engines:
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, KMB_SEED_BATCHED)
-            np.testing.assert_array_equal(r.row_to_col, m.row_to_col)
-            assert r.stats["phases"] == m.phases
+            ref = mi if engine >= 3 else m
+            np.testing.assert_array_equal(r.row_to_col, ref.row_to_col)
+            assert r.stats["phases"] == ref.phases
+            if engine >= 3:
+                assert r.stats["rounds"] == ref.rounds
     solver.set_option(OPT_ENGINE, 0)
 
 
@@ -187,7 +193,7 @@ def test_matching_equals_mirror(solver):
 def test_negative_cost_rejected(solver):
     c = np.ones((5, 5), np.int32)
     c[2, 3] = -1
-    for engine in (1, 2):
+    for engine in (1, 2, 3, 4):
         solver.set_option(OPT_ENGINE, engine)
         with pytest.raises(KmbError, match="costs must be nonnegative"):
             solver.solve(c, KMB_SEED_BATCHED)
@@ -196,9 +202,15 @@ def test_negative_cost_rejected(solver):
 
 def test_out_of_device_range_rejected(solver):
     c = np.ones((5, 5), np.int32)
-    c[0, 0] = 2**30
-    with pytest.raises(KmbError, match="device range"):
-        solver.solve(c, KMB_SEED_BATCHED)
+    c[0, 0] = 2**29
+    for engine in (1, 2, 3, 4):
+        solver.set_option(OPT_ENGINE, engine)
+        with pytest.raises(KmbError, match="device range"):
+            solver.solve(c, KMB_SEED_BATCHED)
+    solver.set_option(OPT_ENGINE, 0)
+    c[0, 0] = 2**29 - 1  # the largest admissible cost
+    ref = O.ref_solve_batched_km(c)
+    check_against(solver.solve(c, KMB_SEED_BATCHED), ref, c)
 
 
 def test_time_budget(solver):
@@ -229,9 +241,14 @@ def test_config2(solver):
     check_against(r, ref, c)
 
 
-def test_config3_subset(solver):
+@pytest.mark.parametrize("engine", [2, 3, 4])
+def test_config3_subset(solver, engine):
     c = W.CONFIGS["c3"].make(batch=64)
-    r = solver.solve_batch(c, KMB_SEED_BATCHED)
+    solver.set_option(OPT_ENGINE, engine)
+    try:
+        r = solver.solve_batch(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_ENGINE, 0)
     for t in range(c.shape[0]):
         ref = O.ref_solve_batched_km(c[t])
         assert r.total_cost[t] == ref.total_cost
