@@ -102,6 +102,12 @@ int kmb_solve_batch_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, i
                         int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
                         int64_t* total_cost, kmb_stats* stats);
 
+/* Diagnostics: the grid engine's reduced-cost scan with every row in the
+ * frontier (one full pass over the matrix per iteration), averaged over
+ * `iters` passes; bytes counted = 4*n*n per pass. */
+int kmb_bench_scan(kmb_context* ctx, const int32_t* cost, int32_t n, int64_t ld, int32_t iters,
+                   double* seconds_per_pass, double* gbytes_per_s);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* kmb_last_error(void);
 int kmb_abi_version(void);

@@ -27,7 +27,7 @@ OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE = 1, 2, 3
 
 # every symbol include/kmb.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
-               "kmb_solve_batch_i32", "kmb_last_error", "kmb_abi_version")
+               "kmb_solve_batch_i32", "kmb_bench_scan", "kmb_last_error", "kmb_abi_version")
 
 
 class KmbUnavailable(RuntimeError):
@@ -69,6 +69,8 @@ def load_library(path: str | None = None):
                                       vp, vp, vp, vp, C.POINTER(Stats)]
         lib.kmb_solve_batch_i32.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32,
                                             vp, vp, vp, vp, C.POINTER(Stats)]
+        lib.kmb_bench_scan.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
         lib.kmb_last_error.restype = C.c_char_p
         lib.kmb_abi_version.restype = C.c_int
         _lib = lib
@@ -159,6 +161,14 @@ class Solver:
                                            C.byref(st) if st is not None else None)
         self._check(rc)
         return st
+
+    def bench_scan(self, cost, n: int, ld: int, iters: int = 5) -> tuple[float, float]:
+        """Full-frontier scan microbenchmark: (seconds per pass, GB/s)."""
+        t = C.c_double()
+        g = C.c_double()
+        self._check(self._lib.kmb_bench_scan(self._h, C.c_void_p(_ptr(cost)), n, ld, iters,
+                                             C.byref(t), C.byref(g)))
+        return t.value, g.value
 
     # -- numpy convenience -------------------------------------------------------
     def solve(self, cost: np.ndarray, seed: int = KMB_SEED_BATCHED,

@@ -278,6 +278,66 @@ int kmb_solve_batch_i32(kmb_context* c, const int32_t* costs, int32_t batch, int
                           c->engine);
 }
 
+// Grid engine staging: slab width W (power of two) and CTA count G, pitched
+// cost copy when the caller's buffer is not already in that layout, workspace.
+static int prepare_grid(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, int32_t seed,
+                        kmb::SolverArgs* out, int* G_out) {
+  cudaStream_t st = c->stream;
+  int64_t maxg = c->max_ctas > 0 ? c->max_ctas : c->sm_count;
+  if (maxg > c->sm_count) maxg = c->sm_count;  // cooperative: one CTA per SM
+  int W = 4;
+  while ((n + W - 1) / W > maxg) W <<= 1;
+  const int G = (n + W - 1) / W;
+  const int64_t pitch = static_cast<int64_t>(G) * W;
+  const size_t nn = static_cast<size_t>(n);
+  const int32_t* dC = cost;
+  const bool dev_in = is_device_ptr(cost);
+  const bool aligned = (reinterpret_cast<uintptr_t>(cost) & 15) == 0;
+  if (!(dev_in && aligned && ld == pitch)) {
+    KMB_CUDA(c->cost.ensure(nn * pitch * 4));
+    KMB_CUDA(cudaMemcpy2DAsync(c->cost.p, pitch * 4, cost, ld * 4, nn * 4, nn, cudaMemcpyDefault, st));
+    dC = c->cost.as<int32_t>();
+  }
+  KMB_CUDA(c->u.ensure(nn * 8));
+  KMB_CUDA(c->v.ensure(nn * 8));
+  KMB_CUDA(c->mrow.ensure(nn * 4));
+  KMB_CUDA(c->mcol.ensure(nn * 4));
+  KMB_CUDA(c->tpar.ensure(nn * 4));
+  KMB_CUDA(c->root.ensure(nn * 4));
+  KMB_CUDA(c->claim.ensure(nn * 8));
+  KMB_CUDA(c->lrow0.ensure(nn * 4));
+  KMB_CUDA(c->lrow1.ensure(nn * 4));
+  KMB_CUDA(c->lw0.ensure(nn * 8));
+  KMB_CUDA(c->lw1.ensure(nn * 8));
+  KMB_CUDA(c->found.ensure(nn * 4));
+  KMB_CUDA(c->partial.ensure(static_cast<size_t>(G) * 8));
+  KMB_CUDA(c->ctrl.ensure(sizeof(kmb::Ctrl)));
+  KMB_CUDA(c->obj.ensure(8));
+  kmb::SolverArgs& a = *out;
+  a.C = dC;
+  a.pitch = pitch;
+  a.n = n;
+  a.W = W;
+  a.seed = seed;
+  a.continue_bfs = c->continue_bfs;
+  a.u = c->u.as<int64_t>();
+  a.v = c->v.as<int64_t>();
+  a.match_row = c->mrow.as<int32_t>();
+  a.match_col = c->mcol.as<int32_t>();
+  a.tree_par = c->tpar.as<int32_t>();
+  a.root_row = c->root.as<int32_t>();
+  a.claim = c->claim.as<uint64_t>();
+  a.list_row[0] = c->lrow0.as<int32_t>();
+  a.list_row[1] = c->lrow1.as<int32_t>();
+  a.list_w[0] = c->lw0.as<int64_t>();
+  a.list_w[1] = c->lw1.as<int64_t>();
+  a.found = c->found.as<int32_t>();
+  a.partial = c->partial.as<int64_t>();
+  a.ctrl = c->ctrl.as<kmb::Ctrl>();
+  *G_out = G;
+  return KMB_OK;
+}
+
 int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, int32_t seed,
                   double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
                   int64_t* total_cost, kmb_stats* stats) {
@@ -306,60 +366,12 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
     return solve_batch_impl(c, src, 1, n, seed, row_to_col, u, v, total_cost, stats, who, engine);
   }
 
-  // ---- grid engine: choose the slab width W (power of two) and CTA count G ----
-  int64_t maxg = c->max_ctas > 0 ? c->max_ctas : c->sm_count;
-  if (maxg > c->sm_count) maxg = c->sm_count;  // cooperative: one CTA per SM
-  int W = 4;
-  while ((n + W - 1) / W > maxg) W <<= 1;
-  const int G = (n + W - 1) / W;
-  const int64_t pitch = static_cast<int64_t>(G) * W;
-  const size_t nn = static_cast<size_t>(n);
-
-  const int32_t* dC = cost;
-  const bool dev_in = is_device_ptr(cost);
-  const bool aligned = (reinterpret_cast<uintptr_t>(cost) & 15) == 0;
-  if (!(dev_in && aligned && ld == pitch)) {
-    KMB_CUDA(c->cost.ensure(nn * pitch * 4));
-    KMB_CUDA(cudaMemcpy2DAsync(c->cost.p, pitch * 4, cost, ld * 4, nn * 4, nn, cudaMemcpyDefault, st));
-    dC = c->cost.as<int32_t>();
-  }
-  KMB_CUDA(c->u.ensure(nn * 8));
-  KMB_CUDA(c->v.ensure(nn * 8));
-  KMB_CUDA(c->mrow.ensure(nn * 4));
-  KMB_CUDA(c->mcol.ensure(nn * 4));
-  KMB_CUDA(c->tpar.ensure(nn * 4));
-  KMB_CUDA(c->root.ensure(nn * 4));
-  KMB_CUDA(c->claim.ensure(nn * 8));
-  KMB_CUDA(c->lrow0.ensure(nn * 4));
-  KMB_CUDA(c->lrow1.ensure(nn * 4));
-  KMB_CUDA(c->lw0.ensure(nn * 8));
-  KMB_CUDA(c->lw1.ensure(nn * 8));
-  KMB_CUDA(c->found.ensure(nn * 4));
-  KMB_CUDA(c->partial.ensure(static_cast<size_t>(G) * 8));
-  KMB_CUDA(c->ctrl.ensure(sizeof(kmb::Ctrl)));
-  KMB_CUDA(c->obj.ensure(8));
-
   kmb::SolverArgs a{};
-  a.C = dC;
-  a.pitch = pitch;
-  a.n = n;
-  a.W = W;
-  a.seed = seed;
-  a.continue_bfs = c->continue_bfs;
-  a.u = c->u.as<int64_t>();
-  a.v = c->v.as<int64_t>();
-  a.match_row = c->mrow.as<int32_t>();
-  a.match_col = c->mcol.as<int32_t>();
-  a.tree_par = c->tpar.as<int32_t>();
-  a.root_row = c->root.as<int32_t>();
-  a.claim = c->claim.as<uint64_t>();
-  a.list_row[0] = c->lrow0.as<int32_t>();
-  a.list_row[1] = c->lrow1.as<int32_t>();
-  a.list_w[0] = c->lw0.as<int64_t>();
-  a.list_w[1] = c->lw1.as<int64_t>();
-  a.found = c->found.as<int32_t>();
-  a.partial = c->partial.as<int64_t>();
-  a.ctrl = c->ctrl.as<kmb::Ctrl>();
+  int G = 0;
+  if (int r = prepare_grid(c, cost, n, ld, seed, &a, &G)) return r;
+  const size_t nn = static_cast<size_t>(n);
+  const int32_t* dC = a.C;
+  const int64_t pitch = a.pitch;
   a.deadline_ns = 0;
   if (time_budget_s > 0.0) {
     // relative budget (top bit set): the kernel adds it to its own %globaltimer
@@ -392,6 +404,32 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
     stats->rounds = h.rounds;
     for (int k = 0; k < 6; ++k) stats->stage_ns[k] = h.stage_ns[k];
   }
+  return KMB_OK;
+}
+
+int kmb_bench_scan(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, int32_t iters,
+                   double* seconds_per_pass, double* gbytes_per_s) {
+  if (!c) return fail(KMB_EINVAL, "kmb_bench_scan: NULL context");
+  if (n <= 0 || !cost || ld < n || iters <= 0) return fail(KMB_EINVAL, "kmb_bench_scan: bad arguments");
+  KMB_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  kmb::SolverArgs a{};
+  int G = 0;
+  if (int r = prepare_grid(c, cost, n, ld, KMB_SEED_BATCHED, &a, &G)) return r;
+  KMB_CUDA(c->tpar.ensure(static_cast<size_t>(n) * 8));  // reused as the key output
+  KMB_CUDA(cudaMemsetAsync(c->ctrl.p, 0, sizeof(kmb::Ctrl), st));
+  KMB_CUDA(kmb::launch_solver_init(a, st));  // row list 0..n-1 with the row minima as w
+  KMB_CUDA(kmb::launch_scan_all(a, G, c->tpar.as<uint64_t>(), st));  // warm-up
+  KMB_CUDA(cudaEventRecord(c->ev0, st));
+  for (int32_t k = 0; k < iters; ++k)
+    KMB_CUDA(kmb::launch_scan_all(a, G, c->tpar.as<uint64_t>(), st));
+  KMB_CUDA(cudaEventRecord(c->ev1, st));
+  KMB_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  const double t = ms * 1e-3 / iters;
+  if (seconds_per_pass) *seconds_per_pass = t;
+  if (gbytes_per_s) *gbytes_per_s = 4.0 * n * static_cast<double>(n) / t / 1e9;
   return KMB_OK;
 }
 

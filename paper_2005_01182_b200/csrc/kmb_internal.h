@@ -20,7 +20,7 @@ struct Ctrl {
   int32_t status;                  // 0 ok, <0 internal error
   int32_t stop;                    // time budget expired
   int32_t free_rows;               // unmatched rows when the engine stopped
-  int32_t pad_;
+  int32_t matched;                 // rows matched so far
   int64_t phases;
   int64_t dual_steps;
   int64_t rows_scanned;
@@ -51,9 +51,11 @@ struct SolverArgs {
 };
 
 cudaError_t launch_solver(const SolverArgs& a, int G, cudaStream_t st);
+cudaError_t launch_solver_init(const SolverArgs& a, cudaStream_t st);
 cudaError_t launch_objective(const int32_t* C, int64_t pitch, int n, const int32_t* match_row,
                              unsigned long long* out, cudaStream_t st);
 size_t solver_smem_bytes(int W);
+cudaError_t launch_scan_all(const SolverArgs& a, int G, uint64_t* keys_out, cudaStream_t st);
 int solver_threads();
 
 // ---- batched small instances (one CTA per instance, cost matrix in SMEM) ----

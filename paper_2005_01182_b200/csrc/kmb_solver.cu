@@ -43,6 +43,7 @@
 namespace kmb {
 
 constexpr int kThreads = 512;
+constexpr int kRelaxBatch = 8;  // rows in flight per thread in the scan
 
 struct SlabSmem {
   int64_t part[kThreads / 32];
@@ -113,21 +114,22 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
     if (g < R) {
       const int32_t* base = a.C + c0 + 4 * s;
       int r = head + g;
-      // 4 rows in flight per thread
-      for (; r + 3 * R < tail; r += 4 * R) {
-        int i[4];
-        uint32_t b[4];
-        int4 c[4];
+      // kRelaxBatch rows in flight per thread: all list/tag loads, then all
+      // 128-bit cost loads, then the folds
+      for (; r + (kRelaxBatch - 1) * R < tail; r += kRelaxBatch * R) {
+        int i[kRelaxBatch];
+        uint32_t b[kRelaxBatch];
+        int4 c[kRelaxBatch];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kRelaxBatch; ++k) {
           i[k] = ldcg(list + r + k * R);
           b[k] = row_bias(ldcg(listw + r + k * R));
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kRelaxBatch; ++k)
           c[k] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[k]) * a.pitch));
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kRelaxBatch; ++k) {
           best0 = umin64(best0, pack_key(static_cast<uint32_t>(c[k].x) + b[k], i[k]));
           best1 = umin64(best1, pack_key(static_cast<uint32_t>(c[k].y) + b[k], i[k]));
           best2 = umin64(best2, pack_key(static_cast<uint32_t>(c[k].z) + b[k], i[k]));
@@ -165,6 +167,11 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
 }
 
 // ---- the persistent engine ---------------------------------------------------
+// Incremental epochs (CPU mirror kmm_solve_incr): the search is
+// never restarted.  When a round absorbs free columns, the trees owning one are
+// augmented and dissolved (their rows/columns finalised and un-reached), columns
+// whose argmin row left are reset, the surviving rows are relaxed once more, and
+// the search goes on at the same D.
 __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const int W = a.W;
@@ -180,11 +187,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   const bool leader = (blockIdx.x == 0 && tid == 0);
   GridBarrier bar{&a.ctrl->bar_counter, 0ull, static_cast<unsigned>(G)};
   Ctrl* ctrl = a.ctrl;
+  const int gtid = blockIdx.x * kThreads + tid;
+  const int gthreads = G * kThreads;
 
   if (ldcg(&ctrl->status) != 0) return;  // invalid input (k_init_rows), all CTAs agree
-  for (int c = tid; c < W; c += kThreads) vloc[c] = 0;  // seed 0: v = 0
+  for (int c = tid; c < W; c += kThreads) {
+    vloc[c] = 0;  // seed 0: v = 0
+    skey[c] = KMB_KEY_INF;
+    rch[c] = (c0 + c < a.n) ? 0 : 1;  // padding columns never count
+  }
+  __syncthreads();
   int64_t dual_steps = 0, rows_scanned = 0;
-  // stage clock (leader only): 0 relax+local min, 1 B1, 2 absorb, 3 B2, 4 phase end, 5 B3
+  // stage clock (leader only): 0 relax+local min, 1 B1, 2 absorb, 3 B2, 4 epoch end, 5 B3
   long long prof[6] = {0, 0, 0, 0, 0, 0};
   long long rounds_total = 0;
   unsigned long long tprev = leader ? globaltimer_ns() : 0ull;
@@ -199,154 +213,150 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   unsigned long long deadline = a.deadline_ns;
   if (deadline >> 63) deadline = globaltimer_ns() + (deadline & ~(1ull << 63));  // relative budget
 
-  for (int phase = 0;; ++phase) {
-    const int p = phase & 1;
-    const int nroots = ldcg(&ctrl->tail[p]);
-    if (nroots == 0 || ldcg(&ctrl->stop) != 0) {
-      if (leader) ctrl->free_rows = nroots;
-      break;
-    }
+  int64_t D = 0;
+  int p = 0, epoch = 0, head = 0, tail = a.n;  // rows list[p][0, tail) are reached
+  bool first_round_of_epoch = true, fatal = false, stopped = false;
+  for (;;) {
     const int32_t* list = a.list_row[p];
     const int64_t* listw = a.list_w[p];
-    for (int c = tid; c < W; c += kThreads) {
-      skey[c] = KMB_KEY_INF;
-      rch[c] = (c0 + c < a.n) ? 0 : 1;  // padding columns never count
+    relax_slab(a, list, listw, head, tail, c0, W, skey);
+    rows_scanned += tail - head;
+    __syncthreads();
+    if (rounds_total == 0 && a.seed == 1)  // column reduction, hungarian.cpp:328-333
+      for (int c = tid; c < W; c += kThreads)
+        if (c0 + c < a.n) vloc[c] = key_val(skey[c]);
+    ++rounds_total;
+    // local min of unreached slack'
+    int64_t lm = KMB_I64_INF;
+    for (int c = tid; c < W; c += kThreads)
+      if (!rch[c]) {
+        const int64_t s = key_val(skey[c]) - vloc[c];
+        lm = s < lm ? s : lm;
+      }
+    lm = warp_min_i64(lm);
+    if (lane == 0) sm.part[wid] = lm;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t x = lane < kThreads / 32 ? sm.part[lane] : KMB_I64_INF;
+      x = warp_min_i64(x);
+      if (lane == 0) a.partial[blockIdx.x] = x;
+    }
+    KMB_STAGE(0);
+    bar.sync();  // ---------------------------------------------- B1
+    KMB_STAGE(1);
+    if (first_round_of_epoch && leader) {  // recycle the previous epoch's counters
+      ctrl->tail[p ^ 1] = 0;
+      ctrl->nfound[p ^ 1] = 0;
+    }
+    first_round_of_epoch = false;
+    if (wid == 0) {
+      int64_t x = KMB_I64_INF;
+      for (int b = lane; b < G; b += 32) {
+        const int64_t y = ldcg(a.partial + b);
+        x = y < x ? y : x;
+      }
+      x = warp_min_i64(x);
+      if (lane == 0) sm.m = x;
     }
     __syncthreads();
-
-    int64_t D = 0;
-    int head = 0, tail = nroots, nfound = 0;
-    bool fatal = false;  // identical in every CTA (all see the same m)
-    for (int round = 0;; ++round) {
-      relax_slab(a, list, listw, head, tail, c0, W, skey);
-      rows_scanned += tail - head;
-      ++rounds_total;
-      __syncthreads();
-      if (phase == 0 && round == 0 && a.seed == 1)  // column reduction, hungarian.cpp:328-333
-        for (int c = tid; c < W; c += kThreads)
-          if (c0 + c < a.n) vloc[c] = key_val(skey[c]);
-      // local min of unreached slack'
-      int64_t lm = KMB_I64_INF;
-      for (int c = tid; c < W; c += kThreads)
-        if (!rch[c]) {
-          const int64_t s = key_val(skey[c]) - vloc[c];
-          lm = s < lm ? s : lm;
-        }
-      lm = warp_min_i64(lm);
-      if (lane == 0) sm.part[wid] = lm;
-      __syncthreads();
-      if (wid == 0) {
-        int64_t x = lane < kThreads / 32 ? sm.part[lane] : KMB_I64_INF;
-        x = warp_min_i64(x);
-        if (lane == 0) a.partial[blockIdx.x] = x;
+    const int64_t m = sm.m;
+    if (m > D) {
+      if (m == KMB_I64_INF) {  // no unreached column: cannot happen on valid input
+        if (leader) ctrl->status = -2;
+        fatal = true;
+        break;
       }
-      KMB_STAGE(0);
-      bar.sync();  // ---------------------------------------------- B1
-      KMB_STAGE(1);
-      if (round == 0 && leader) {  // recycle the previous phase's counters
-        ctrl->tail[p ^ 1] = 0;
-        ctrl->nfound[p ^ 1] = 0;
-      }
-      if (wid == 0) {
-        int64_t x = KMB_I64_INF;
-        for (int b = lane; b < G; b += 32) {
-          const int64_t y = ldcg(a.partial + b);
-          x = y < x ? y : x;
-        }
-        x = warp_min_i64(x);
-        if (lane == 0) sm.m = x;
-      }
-      __syncthreads();
-      const int64_t m = sm.m;
-      if (m > D) {
-        if (nfound > 0) break;  // closure exhausted at this D (continue_bfs)
-        if (m == KMB_I64_INF) {  // no unreached column: cannot happen on valid input
-          if (leader) ctrl->status = -2;
-          fatal = true;
-          break;
-        }
-        D = m;  // dual step: no tight unreached column, no pending row
-        ++dual_steps;
-      }
-      // absorb zero-slack columns of the slab
-      for (int cb = 0; cb < W; cb += kThreads) {
-        const int c = cb + tid;
-        bool newrow = false, newfree = false;
-        int32_t i2 = -1, col = c0 + c;
-        int64_t w2 = 0;
-        int32_t root = 0;
-        if (c < W && !rch[c] && key_val(skey[c]) - vloc[c] == D) {
-          rch[c] = 1;
-          dcol[c] = D;
-          const int32_t par = key_row(skey[c]);
-          a.tree_par[col] = par;
-          root = ldcg(a.root_row + par);
-          i2 = ldcg(a.match_col + col);
-          if (i2 < 0) {
-            newfree = true;
-            atomicMin(reinterpret_cast<unsigned long long*>(a.claim + root), claim_key(phase, col));
-          } else {
-            newrow = true;
-            w2 = ldcg(a.u + i2) - D;
-            a.root_row[i2] = root;
-          }
-        }
-        // warp-aggregated appends
-        const unsigned rowmask = __ballot_sync(0xffffffffu, newrow);
-        if (rowmask) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&ctrl->tail[p], __popc(rowmask));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (newrow) {
-            const int pos = base + __popc(rowmask & ((1u << lane) - 1));
-            a.list_row[p][pos] = i2;
-            a.list_w[p][pos] = w2;
-          }
-        }
-        const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
-        if (fmask) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&ctrl->nfound[p], __popc(fmask));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (newfree) a.found[base + __popc(fmask & ((1u << lane) - 1))] = col;
-        }
-      }
-      KMB_STAGE(2);
-      bar.sync();  // ---------------------------------------------- B2
-      KMB_STAGE(3);
-      head = tail;
-      tail = ldcg(&ctrl->tail[p]);
-      nfound = ldcg(&ctrl->nfound[p]);
-      if (nfound > 0 && (!a.continue_bfs || head == tail)) break;
+      D = m;  // dual step: no tight unreached column, no pending row (:201-215)
+      ++dual_steps;
     }
-    if (fatal) break;
+    // absorb zero-slack columns of the slab (hungarian.cpp:186-199)
+    for (int cb = 0; cb < W; cb += kThreads) {
+      const int c = cb + tid;
+      bool newrow = false, newfree = false;
+      int32_t i2 = -1, col = c0 + c;
+      int64_t w2 = 0;
+      if (c < W && !rch[c] && key_val(skey[c]) - vloc[c] == D) {
+        rch[c] = 1;
+        dcol[c] = D;
+        const int32_t par = key_row(skey[c]);
+        a.tree_par[col] = par;
+        const int32_t root = ldcg(a.root_row + par);
+        i2 = ldcg(a.match_col + col);
+        if (i2 < 0) {
+          newfree = true;
+          atomicMin(reinterpret_cast<unsigned long long*>(a.claim + root), claim_key(epoch, col));
+        } else {
+          newrow = true;
+          w2 = ldcg(a.u + i2) - D;
+          a.root_row[i2] = root;
+        }
+      }
+      // warp-aggregated appends
+      const unsigned rowmask = __ballot_sync(0xffffffffu, newrow);
+      if (rowmask) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&ctrl->tail[p], __popc(rowmask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (newrow) {
+          const int pos = base + __popc(rowmask & ((1u << lane) - 1));
+          a.list_row[p][pos] = i2;
+          a.list_w[p][pos] = w2;
+        }
+      }
+      const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
+      if (fmask) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&ctrl->nfound[p], __popc(fmask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (newfree) a.found[base + __popc(fmask & ((1u << lane) - 1))] = col;
+      }
+    }
+    KMB_STAGE(2);
+    bar.sync();  // ---------------------------------------------- B2
+    KMB_STAGE(3);
+    head = tail;
+    tail = ldcg(&ctrl->tail[p]);
+    const int nfound = ldcg(&ctrl->nfound[p]);
+    if (nfound == 0) continue;
 
-    // ---- end of phase: finalise duals, flip paths, list next free rows -------
-    const int gtid = blockIdx.x * kThreads + tid;
-    const int gthreads = G * kThreads;
+    // ---- epoch end: augment and dissolve the trees that reached a free column ----
+    // columns of the slab: finalise dissolved ones, reset keys whose argmin row leaves
+    for (int c = tid; c < W; c += kThreads) {
+      const int col = c0 + c;
+      if (col >= a.n) continue;
+      if (rch[c]) {
+        const int32_t root = ldcg(a.root_row + ldcg(a.tree_par + col));
+        if (claimed_in(ldcg(a.claim + root), epoch)) {
+          vloc[c] -= D - dcol[c];
+          rch[c] = 0;
+          skey[c] = KMB_KEY_INF;
+        }
+      } else if (skey[c] != KMB_KEY_INF) {
+        const int32_t root = ldcg(a.root_row + key_row(skey[c]));
+        if (claimed_in(ldcg(a.claim + root), epoch)) skey[c] = KMB_KEY_INF;
+      }
+    }
+    // rows: finalise dissolved ones (u = w + D), carry the survivors over
     for (int r = gtid; r < tail; r += gthreads) {
       const int32_t i = ldcg(list + r);
-      const int64_t un = ldcg(listw + r) + D;
-      a.u[i] = un;
-      if (r < nroots && !claimed_in(ldcg(a.claim + i), phase)) {  // still free
+      const int64_t w = ldcg(listw + r);
+      if (claimed_in(ldcg(a.claim + ldcg(a.root_row + i)), epoch)) {
+        a.u[i] = w + D;
+      } else {
         const int pos = atomicAdd(&ctrl->tail[p ^ 1], 1);
         a.list_row[p ^ 1][pos] = i;
-        a.list_w[p ^ 1][pos] = un;
-        a.root_row[i] = i;
+        a.list_w[p ^ 1][pos] = w;
       }
     }
-    for (int c = tid; c < W; c += kThreads)
-      if (rch[c] && c0 + c < a.n) vloc[c] -= D - dcol[c];
+    // flip one parent-pointer path per claimed tree (its smallest free column)
+    int won = 0;
     for (int f = gtid; f < nfound; f += gthreads) {
       int32_t j = ldcg(a.found + f);
-      // winner: the smallest free column that reached this tree's root
-      int32_t i = ldcg(a.tree_par + j);
-      // walk to the root (the path is only read here; flips happen below by
-      // the winner alone, and trees are disjoint)
-      int32_t root = ldcg(a.root_row + i);
-      if (ldcg(a.claim + root) != claim_key(phase, j)) continue;
+      const int32_t root = ldcg(a.root_row + ldcg(a.tree_par + j));
+      if (ldcg(a.claim + root) != claim_key(epoch, j)) continue;
+      ++won;
       for (;;) {
-        i = ldcg(a.tree_par + j);
+        const int32_t i = ldcg(a.tree_par + j);
         const int32_t nxt = ldcg(a.match_row + i);
         a.match_row[i] = j;
         a.match_col[j] = i;
@@ -354,22 +364,72 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
         j = nxt;
       }
     }
+    won = __reduce_add_sync(0xffffffffu, won);
+    if (lane == 0 && won) atomicAdd(&ctrl->matched, won);
     if (leader) {
-      ctrl->phases = phase + 1;
+      ctrl->phases = epoch + 1;
       if (deadline && globaltimer_ns() > deadline) ctrl->stop = 1;
     }
     KMB_STAGE(4);
     bar.sync();  // ------------------------------------------------ B3
     KMB_STAGE(5);
+    p ^= 1;
+    ++epoch;
+    head = 0;
+    tail = ldcg(&ctrl->tail[p]);
+    first_round_of_epoch = true;
+    if (ldcg(&ctrl->matched) == a.n) break;
+    if (ldcg(&ctrl->stop) != 0) {
+      stopped = true;
+      break;
+    }
   }
+  if (stopped) {  // time budget: write back the surviving trees' lazy duals
+    for (int r = gtid; r < tail; r += gthreads) {
+      const int32_t i = ldcg(a.list_row[p] + r);
+      a.u[i] = ldcg(a.list_w[p] + r) + D;
+    }
+    for (int c = tid; c < W; c += kThreads)
+      if (rch[c] && c0 + c < a.n) vloc[c] -= D - dcol[c];
+  }
+  (void)fatal;
   for (int c = tid; c < W; c += kThreads)
     if (c0 + c < a.n) a.v[c0 + c] = vloc[c];
   if (leader) {
+    ctrl->free_rows = a.n - ldcg(&ctrl->matched);
     ctrl->dual_steps = dual_steps;
     ctrl->rows_scanned = rows_scanned;
     ctrl->rounds = rounds_total;
     for (int k = 0; k < 6; ++k) ctrl->stage_ns[k] = prof[k];
   }
+}
+
+// ---- full-frontier scan microbenchmark ------------------------------------------
+// The engine's reduced-cost scan (relax_slab) with every row in the frontier:
+// one pass over the whole n x n matrix per launch, keys written out so the pass
+// cannot be elided.  Measures what K3 sustains from HBM when it is not waiting
+// on barriers ("full-matrix pass").
+__global__ void __launch_bounds__(kThreads, 1) k_scan_all(SolverArgs a, uint64_t* keys_out) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  uint64_t* skey = reinterpret_cast<uint64_t*>(dyn);
+  const int W = a.W, c0 = blockIdx.x * W;
+  for (int c = threadIdx.x; c < W; c += kThreads) skey[c] = KMB_KEY_INF;
+  __syncthreads();
+  relax_slab(a, a.list_row[0], a.list_w[0], 0, a.n, c0, W, skey);
+  __syncthreads();
+  for (int c = threadIdx.x; c < W; c += kThreads)
+    if (c0 + c < a.n) keys_out[c0 + c] = skey[c];
+}
+
+cudaError_t launch_scan_all(const SolverArgs& a, int G, uint64_t* keys_out, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(a.W) * 8;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan_all, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k_scan_all<<<G, kThreads, smem, st>>>(a, keys_out);
+  return cudaGetLastError();
 }
 
 // ---- K10: objective  sum_i C[i][match_row[i]] (core.cpp:76-90, int64) -------
@@ -387,9 +447,13 @@ __global__ void k_objective(const int32_t* C, int64_t pitch, int n, const int32_
 
 size_t solver_smem_bytes(int W) { return static_cast<size_t>(W) * (8 + 8 + 8 + 1) + 16; }
 
-cudaError_t launch_solver(const SolverArgs& a, int G, cudaStream_t st) {
+cudaError_t launch_solver_init(const SolverArgs& a, cudaStream_t st) {
   k_init_rows<<<256, 256, 0, st>>>(a);
-  cudaError_t e = cudaGetLastError();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solver(const SolverArgs& a, int G, cudaStream_t st) {
+  cudaError_t e = launch_solver_init(a, st);
   if (e != cudaSuccess) return e;
   const size_t smem = solver_smem_bytes(a.W);
   if (smem > 48 * 1024) {
