@@ -63,8 +63,10 @@ enum kmb_status {
 enum kmb_option {
   KMB_OPT_MAX_CTAS = 1,     /* grid engine: upper bound on CTAs (0 = #SMs)      */
   KMB_OPT_CONTINUE_BFS = 2, /* 1: exhaust the tight closure before augmenting   */
-  KMB_OPT_ENGINE = 3        /* 0 auto, 1 grid (persistent), 2 CTA/SMEM (n<=224),
-                               3 warp/SMEM, 4 warp/L2 (n <= 256)                */
+  KMB_OPT_ENGINE = 3        /* 0 auto (warp n<=256, cluster n<=8192, grid),
+                               1 grid (persistent), 2 CTA/SMEM (n<=224),
+                               3 warp/SMEM, 4 warp/L2 (n <= 256),
+                               5 cluster (grid engine on one <=16-CTA cluster)  */
 };
 
 typedef struct kmb_stats {

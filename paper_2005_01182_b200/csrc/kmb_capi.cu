@@ -134,7 +134,7 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
     case KMB_OPT_MAX_CTAS: c->max_ctas = value; return KMB_OK;
     case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_ENGINE:
-      if (value < 0 || value > 4) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..4");
+      if (value < 0 || value > 5) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..5");
       c->engine = static_cast<int>(value);
       return KMB_OK;
     default: return fail(KMB_EINVAL, "kmb_set_option: unknown option");
@@ -281,10 +281,11 @@ int kmb_solve_batch_i32(kmb_context* c, const int32_t* costs, int32_t batch, int
 // Grid engine staging: slab width W (power of two) and CTA count G, pitched
 // cost copy when the caller's buffer is not already in that layout, workspace.
 static int prepare_grid(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, int32_t seed,
-                        kmb::SolverArgs* out, int* G_out) {
+                        kmb::SolverArgs* out, int* G_out, bool cluster = false) {
   cudaStream_t st = c->stream;
   int64_t maxg = c->max_ctas > 0 ? c->max_ctas : c->sm_count;
   if (maxg > c->sm_count) maxg = c->sm_count;  // cooperative: one CTA per SM
+  if (cluster && maxg > 16) maxg = 16;          // one thread-block cluster
   int W = 4;
   while ((n + W - 1) / W > maxg) W <<= 1;
   const int G = (n + W - 1) / W;
@@ -351,10 +352,13 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   cudaStream_t st = c->stream;
 
   int engine = c->engine;
-  if (engine == 0) engine = (n <= 128 && time_budget_s <= 0.0) ? 4 : 1;
+  // auto: one warp per instance up to n = 256 (no time budget there), one
+  // thread-block cluster up to n = 8192, the whole-GPU grid beyond (measured
+  // crossovers)
+  if (engine == 0) engine = (n <= 256 && time_budget_s <= 0.0) ? 4 : (n <= 8192 ? 5 : 1);
   if (engine == 2 && n > kmb::batch_max_n()) engine = 1;
-  if (engine >= 3 && n > kmb::warp_max_n()) engine = 1;
-  if (engine >= 2) {
+  if ((engine == 3 || engine == 4) && n > kmb::warp_max_n()) engine = 1;
+  if (engine >= 2 && engine <= 4) {
     if (time_budget_s > 0.0)
       return fail(KMB_EINVAL, "kmb_solve_i32: the per-instance engines have no time budget; use engine 1");
     const int32_t* src = cost;
@@ -366,9 +370,10 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
     return solve_batch_impl(c, src, 1, n, seed, row_to_col, u, v, total_cost, stats, who, engine);
   }
 
+  const bool cluster = engine == 5;
   kmb::SolverArgs a{};
   int G = 0;
-  if (int r = prepare_grid(c, cost, n, ld, seed, &a, &G)) return r;
+  if (int r = prepare_grid(c, cost, n, ld, seed, &a, &G, cluster)) return r;
   const size_t nn = static_cast<size_t>(n);
   const int32_t* dC = a.C;
   const int64_t pitch = a.pitch;
@@ -379,7 +384,7 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   }
   KMB_CUDA(cudaMemsetAsync(c->ctrl.p, 0, sizeof(kmb::Ctrl), st));
   KMB_CUDA(cudaEventRecord(c->ev0, st));
-  KMB_CUDA(kmb::launch_solver(a, G, st));
+  KMB_CUDA(kmb::launch_solver(a, G, cluster, st));
   KMB_CUDA(kmb::launch_objective(dC, pitch, n, a.match_row, c->obj.as<unsigned long long>(), st));
   KMB_CUDA(cudaEventRecord(c->ev1, st));
   int r;
@@ -400,7 +405,7 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     stats->seconds = ms * 1e-3;
     stats->converged = h.free_rows == 0 ? 1 : 0;
-    stats->engine = 1;
+    stats->engine = cluster ? 5 : 1;
     stats->rounds = h.rounds;
     for (int k = 0; k < 6; ++k) stats->stage_ns[k] = h.stage_ns[k];
   }

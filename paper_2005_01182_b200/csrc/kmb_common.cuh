@@ -93,6 +93,10 @@ struct GridBarrier {
   unsigned long long target;
   unsigned int G;
 
+  __device__ static GridBarrier make(unsigned long long* counter, unsigned int G) {
+    return GridBarrier{counter, 0ull, G};
+  }
+
   __device__ __forceinline__ void sync() {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -104,6 +108,17 @@ struct GridBarrier {
       __threadfence();
     }
     __syncthreads();
+  }
+};
+
+// All CTAs of the launch form ONE thread-block cluster (G <= 16): the hardware
+// cluster barrier (release/acquire at cluster scope, covers global memory).
+struct ClusterBarrier {
+  __device__ static ClusterBarrier make(unsigned long long*, unsigned int) { return ClusterBarrier{}; }
+  __device__ __forceinline__ void sync() {
+    asm volatile(
+        "barrier.cluster.arrive.release.aligned;\n"
+        "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
 };
 

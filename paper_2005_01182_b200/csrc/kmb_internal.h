@@ -50,7 +50,7 @@ struct SolverArgs {
   Ctrl* ctrl;
 };
 
-cudaError_t launch_solver(const SolverArgs& a, int G, cudaStream_t st);
+cudaError_t launch_solver(const SolverArgs& a, int G, bool cluster, cudaStream_t st);
 cudaError_t launch_solver_init(const SolverArgs& a, cudaStream_t st);
 cudaError_t launch_objective(const int32_t* C, int64_t pitch, int n, const int32_t* match_row,
                              unsigned long long* out, cudaStream_t st);

@@ -172,6 +172,7 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
 // augmented and dissolved (their rows/columns finalised and un-reached), columns
 // whose argmin row left are reset, the surviving rows are relaxed once more, and
 // the search goes on at the same D.
+template <class Barrier>
 __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const int W = a.W;
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   const int G = gridDim.x;
   const int c0 = blockIdx.x * W;
   const bool leader = (blockIdx.x == 0 && tid == 0);
-  GridBarrier bar{&a.ctrl->bar_counter, 0ull, static_cast<unsigned>(G)};
+  Barrier bar = Barrier::make(&a.ctrl->bar_counter, static_cast<unsigned>(G));
   Ctrl* ctrl = a.ctrl;
   const int gtid = blockIdx.x * kThreads + tid;
   const int gthreads = G * kThreads;
@@ -452,18 +453,41 @@ cudaError_t launch_solver_init(const SolverArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_solver(const SolverArgs& a, int G, cudaStream_t st) {
+cudaError_t launch_solver(const SolverArgs& a, int G, bool cluster, cudaStream_t st) {
   cudaError_t e = launch_solver_init(a, st);
   if (e != cudaSuccess) return e;
   const size_t smem = solver_smem_bytes(a.W);
+  if (!cluster) {
+    auto kern = k_solve<GridBarrier>;
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    void* params[] = {const_cast<SolverArgs*>(&a)};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(G), dim3(kThreads), params,
+                                       smem, st);
+  }
+  // one thread-block cluster of G <= 16 CTAs: hardware cluster barriers
+  auto kern = k_solve<ClusterBarrier>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
   if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  void* params[] = {const_cast<SolverArgs*>(&a)};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_solve), dim3(G), dim3(kThreads),
-                                     params, smem, st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 cudaError_t launch_objective(const int32_t* C, int64_t pitch, int n, const int32_t* match_row,

@@ -87,7 +87,7 @@ def check_against(res, ref, c, dual_steps=None):
 def test_known_2x2(solver):  # test_hungarian.cpp:72-85
     c = np.array([[1, 3], [2, 1]], np.int32)
     for seed in (KMB_SEED_KM, KMB_SEED_BATCHED):
-        for engine in (1, 2, 3, 4):
+        for engine in (1, 2, 3, 4, 5):
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, seed)
             assert r.total_cost == 2
@@ -108,7 +108,7 @@ def test_known_constant(solver):  # :133-142: constant 6x6 cost 4 -> 24, one pha
     assert r.stats["dual_steps"] == 0
 
 
-@pytest.mark.parametrize("engine", [1, 2, 3, 4])
+@pytest.mark.parametrize("engine", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("seed", [KMB_SEED_KM, KMB_SEED_BATCHED])
 def test_random_small_vs_reference(solver, engine, seed):
     rng = np.random.default_rng(100 + 10 * engine + seed)
@@ -126,12 +126,13 @@ def test_random_small_vs_reference(solver, engine, seed):
         solver.set_option(OPT_ENGINE, 0)
 
 
+@pytest.mark.parametrize("engine", [1, 5])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 13, 31, 33, 127, 129, 200, 255, 257, 300, 513, 1000, 1001])
-def test_ragged_sizes_grid(solver, n):
+def test_ragged_sizes_grid(solver, n, engine):
     rng = np.random.default_rng(n)
     c = rng.integers(0, 5000, size=(n, n)).astype(np.int32)
     ref = O.ref_solve_batched_km(c)
-    solver.set_option(OPT_ENGINE, 1)
+    solver.set_option(OPT_ENGINE, engine)
     try:
         r = solver.solve(c, KMB_SEED_BATCHED)
     finally:
@@ -176,7 +177,7 @@ def test_matching_equals_mirror(solver):
         c = rng.integers(0, 20, size=(n, n)).astype(np.int32)
         m = O.mirror_solve(c, 1)
         mi = O.mirror_solve_incr(c, 1)
-        engines = [1] + ([2] if n <= 224 else []) + ([3, 4] if n <= 256 else [])
+        engines = [1, 5] + ([2] if n <= 224 else []) + ([3, 4] if n <= 256 else [])
         for engine in engines:
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, KMB_SEED_BATCHED)
@@ -193,7 +194,7 @@ def test_matching_equals_mirror(solver):
 def test_negative_cost_rejected(solver):
     c = np.ones((5, 5), np.int32)
     c[2, 3] = -1
-    for engine in (1, 2, 3, 4):
+    for engine in (1, 2, 3, 4, 5):
         solver.set_option(OPT_ENGINE, engine)
         with pytest.raises(KmbError, match="costs must be nonnegative"):
             solver.solve(c, KMB_SEED_BATCHED)
@@ -203,7 +204,7 @@ def test_negative_cost_rejected(solver):
 def test_out_of_device_range_rejected(solver):
     c = np.ones((5, 5), np.int32)
     c[0, 0] = 2**29
-    for engine in (1, 2, 3, 4):
+    for engine in (1, 2, 3, 4, 5):
         solver.set_option(OPT_ENGINE, engine)
         with pytest.raises(KmbError, match="device range"):
             solver.solve(c, KMB_SEED_BATCHED)
@@ -213,13 +214,20 @@ def test_out_of_device_range_rejected(solver):
     check_against(solver.solve(c, KMB_SEED_BATCHED), ref, c)
 
 
-def test_time_budget(solver):
+@pytest.mark.parametrize("engine", [1, 5])
+def test_time_budget(solver, engine):
     c = W.CONFIGS["c2"].make()
-    solver.set_option(OPT_ENGINE, 1)
+    solver.set_option(OPT_ENGINE, engine)
     r = solver.solve(c, KMB_SEED_BATCHED, time_budget_s=1e-6)
     solver.set_option(OPT_ENGINE, 0)
     assert not r.converged
     assert (r.row_to_col >= 0).sum() < c.shape[0]
+    # the duals written back on expiry stay feasible (lazy duals finalised)
+    cc = c.astype(np.int64)
+    assert (cc - r.u[:, None] - r.v[None, :]).min() >= 0
+    ok = r.row_to_col >= 0
+    rows = np.nonzero(ok)[0]
+    assert (cc[rows, r.row_to_col[ok]] == r.u[rows] + r.v[r.row_to_col[ok]]).all()
 
 
 # ---- BASELINE configs -----------------------------------------------------------
