@@ -63,10 +63,12 @@ enum kmb_status {
 enum kmb_option {
   KMB_OPT_MAX_CTAS = 1,     /* grid engine: upper bound on CTAs (0 = #SMs)      */
   KMB_OPT_CONTINUE_BFS = 2, /* 1: exhaust the tight closure before augmenting   */
-  KMB_OPT_ENGINE = 3        /* 0 auto (warp n<=256, cluster n<=8192, grid),
+  KMB_OPT_ENGINE = 3,       /* 0 auto (warp n<=256, cluster n<=8192, grid),
                                1 grid (persistent), 2 CTA/SMEM (n<=224),
                                3 warp/SMEM, 4 warp/L2 (n <= 256),
                                5 cluster (grid engine on one <=16-CTA cluster)  */
+  KMB_OPT_WARPS_PER_SM = 4  /* warp engine: resident instances per SM (0 = max);
+                               bounds the L2 working set of streamed matrices   */
 };
 
 typedef struct kmb_stats {
@@ -78,8 +80,10 @@ typedef struct kmb_stats {
   int32_t converged;       /* 0 when the time budget expired                 */
   int32_t engine;          /* 1 grid, 2 SMEM                                 */
   int64_t rounds;          /* search rounds (relax | min | absorb)           */
-  int64_t stage_ns[6];     /* grid engine, CTA 0's clock: relax, barrier 1,
-                              absorb, barrier 2, phase end, barrier 3        */
+  int64_t stage_ns[6];     /* grid engine, CTA 0's clock (ns): relax, barrier 1,
+                              absorb, barrier 2, epoch end, barrier 3;
+                              warp engine: SM cycles summed over instances in
+                              relax, min, absorb, epoch end                  */
   int64_t max_instance_cycles; /* batch engines: slowest instance (SM clocks) */
   int64_t sum_instance_cycles; /* batch engines: sum over instances          */
 } kmb_stats;

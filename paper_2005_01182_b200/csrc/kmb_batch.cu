@@ -303,8 +303,7 @@ __global__ void __launch_bounds__(256) k_batch_solve(BatchArgs a) {
         o[0] = phases;
         o[1] = dual_steps;
         o[2] = rows_scanned;
-        o[3] = 0;
-        o[4] = 0;
+        for (int k = 3; k < KMB_ISTATS; ++k) o[k] = 0;
       }
     }
     __syncthreads();

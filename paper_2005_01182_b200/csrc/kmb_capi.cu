@@ -71,6 +71,7 @@ struct kmb_context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t max_ctas = 0;
+  int64_t warps_per_sm = 0;  // warp engine residency bound (0 = occupancy limit)
   int continue_bfs = 0;
   int engine = 0;
   // grid-engine workspace
@@ -133,6 +134,7 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
   switch (option) {
     case KMB_OPT_MAX_CTAS: c->max_ctas = value; return KMB_OK;
     case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
+    case KMB_OPT_WARPS_PER_SM: c->warps_per_sm = value; return KMB_OK;
     case KMB_OPT_ENGINE:
       if (value < 0 || value > 5) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..5");
       c->engine = static_cast<int>(value);
@@ -194,9 +196,9 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     KMB_CUDA(cudaEventRecord(c->ev0, st));
     KMB_CUDA(kmb::launch_batch(a, c->sm_count, st, &grid));
   } else {
-    const int np = (n + 3) & ~3;
+    const int np = kmb::warp_pitch(n);
     const int32_t* src = dcost;
-    if (np != n) {  // 16 B row alignment for 128-bit loads / TMA: pad once
+    if (np != n) {  // rows padded to the warp width (in-bounds 128-bit loads): pad once
       KMB_CUDA(c->bpad.ensure(static_cast<size_t>(batch) * n * np * 4));
       KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4,
                                  static_cast<size_t>(batch) * n, cudaMemcpyDeviceToDevice, st));
@@ -216,7 +218,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.stats = c->bstat.as<int64_t>();
     a.status = c->bstatus.as<int32_t>();
     KMB_CUDA(cudaEventRecord(c->ev0, st));
-    KMB_CUDA(kmb::launch_warp_batch(a, c->sm_count, engine == 3, st, &grid));
+    KMB_CUDA(kmb::launch_warp_batch(a, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), st, &grid));
   }
   KMB_CUDA(cudaEventRecord(c->ev1, st));
   if (dr2c != row_to_col) { int r = copy_out(row_to_col, dr2c, nb * 4, st); if (r) return r; }
@@ -249,6 +251,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       stats->rounds += o[3];
       stats->sum_instance_cycles += o[4];
       if (o[4] > stats->max_instance_cycles) stats->max_instance_cycles = o[4];
+      for (int k = 0; k < 4; ++k) stats->stage_ns[k] += o[5 + k];  // batch: SM cycles, summed
     }
     stats->cost_bytes_read = static_cast<int64_t>(batch) * n * n * 4;  // HBM: each matrix once
     float ms = 0.f;

@@ -8,8 +8,8 @@
 namespace kmb {
 
 // per-instance stats of the batch engines: phases/epochs, dual steps, rows
-// scanned, rounds, SM cycles
-constexpr int KMB_ISTATS = 5;
+// scanned, rounds, SM cycles, then cycles in relax / min / absorb / epoch end
+constexpr int KMB_ISTATS = 9;
 
 // Device control block of one single-instance solve.  Counters that are
 // recycled between phases are double-buffered by phase parity (see k_solve).
@@ -81,7 +81,7 @@ cudaError_t launch_batch(const BatchArgs& a, int sm_count, cudaStream_t st, int*
 namespace kmb {
 // ---- warp engine (one warp per instance, n <= 256) -----------------------------
 struct WarpArgs {
-  const int32_t* C;      // batch x n x pitch (pitch % 4 == 0), instances back to back
+  const int32_t* C;      // batch x n x pitch (pitch == warp_pitch(n)), instances back to back
   int32_t batch;
   int32_t n;
   int32_t pitch;
@@ -95,6 +95,7 @@ struct WarpArgs {
   int32_t* status;       // batch
 };
 int warp_max_n();
-cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, cudaStream_t st,
-                              int* grid_out);
+int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)
+cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int warps_per_sm,
+                              cudaStream_t st, int* grid_out);
 }  // namespace kmb

@@ -77,30 +77,25 @@ struct RowVec {
   int32_t x[CPL];
 };
 
-// Loads the lane's CPL columns of one row; `avail` = pitch - c0 (elements left
-// in the padded row), chunks past it read as 0 (padding columns are masked).
+// Loads the lane's CPL columns of one row.  The pitch is padded to the warp
+// width (32 * CPL), so every lane's vector load is in bounds; padding columns
+// read whatever the pad holds and are masked as "reached".
 template <int CPL, bool SMEM_C>
-__device__ __forceinline__ RowVec<CPL> load_row(const int32_t* base, int avail) {
+__device__ __forceinline__ RowVec<CPL> load_row(const int32_t* p) {
   RowVec<CPL> r;
-#pragma unroll
-  for (int q = 0; q < CPL; ++q) r.x[q] = 0;
   if constexpr (CPL >= 4) {
 #pragma unroll
     for (int h = 0; h < CPL / 4; ++h) {
-      if (4 * h < avail) {
-        const int4* p = reinterpret_cast<const int4*>(base) + h;
-        const int4 t = SMEM_C ? *p : __ldg(p);
-        r.x[4 * h + 0] = t.x; r.x[4 * h + 1] = t.y; r.x[4 * h + 2] = t.z; r.x[4 * h + 3] = t.w;
-      }
+      const int4* q = reinterpret_cast<const int4*>(p) + h;
+      const int4 t = SMEM_C ? *q : __ldg(q);
+      r.x[4 * h + 0] = t.x; r.x[4 * h + 1] = t.y; r.x[4 * h + 2] = t.z; r.x[4 * h + 3] = t.w;
     }
   } else if constexpr (CPL == 2) {
-    if (avail > 0) {
-      const int2* p = reinterpret_cast<const int2*>(base);
-      const int2 t = SMEM_C ? *p : __ldg(p);
-      r.x[0] = t.x; r.x[1] = t.y;
-    }
+    const int2* q = reinterpret_cast<const int2*>(p);
+    const int2 t = SMEM_C ? *q : __ldg(q);
+    r.x[0] = t.x; r.x[1] = t.y;
   } else {
-    if (avail > 0) r.x[0] = SMEM_C ? *base : __ldg(base);
+    r.x[0] = SMEM_C ? *p : __ldg(p);
   }
   return r;
 }
@@ -164,9 +159,10 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   using KO = Keys<NARROW>;
   using K = typename KO::K;
   constexpr uint32_t FULL = 0xffffffffu;
-  const int n = a.n, np = a.pitch;
+  const int n = a.n;
+  const uint32_t np = static_cast<uint32_t>(a.pitch);
   const int c0 = CPL * lane;
-  const int avail = np - c0;
+  const int32_t* const lb = Cm + c0;  // this lane's columns of row 0
   int32_t* const u = S.u;
   int32_t* const w = S.w;
   int32_t* const root_row = S.root_row;
@@ -199,35 +195,46 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
   int status = 0;
   const long long t_start = clock64();
+  long long cyc[4] = {0, 0, 0, 0};  // relax, min, absorb, epoch end
+  long long tl = t_start;
+#define KMB_WSTAGE(k)                 \
+  do {                                \
+    const long long t_ = clock64();   \
+    cyc[k] += t_ - tl;                \
+    tl = t_;                          \
+  } while (0)
   __syncwarp();
 
   while (nfree > 0) {
     ++rounds;
     // ---- relax rows[head, nrows)  (hungarian.cpp:164-172) ----
     int r = head;
-    for (; r + 3 < nrows; r += 4) {
-      int2 e[4];
-      RowVec<CPL> cv[4];
+    // RB rows in flight: entries, then all row loads, then the folds
+    constexpr int RB = CPL <= 4 ? 8 : 4;
+    for (; r + RB - 1 < nrows; r += RB) {
+      int2 e[RB];
+      RowVec<CPL> cv[RB];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) e[k] = rows[r + k];
+      for (int k = 0; k < RB; ++k) e[k] = rows[r + k];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        cv[k] = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(e[k].x) * np + c0, avail);
+      for (int k = 0; k < RB; ++k)
+        cv[k] = load_row<CPL, SMEM_C>(lb + static_cast<uint32_t>(e[k].x) * np);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < RB; ++k)
 #pragma unroll
         for (int q = 0; q < CPL; ++q)
           key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), e[k].x));
     }
     for (; r < nrows; ++r) {
       const int2 e = rows[r];
-      const RowVec<CPL> cv = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(e.x) * np + c0, avail);
+      const RowVec<CPL> cv = load_row<CPL, SMEM_C>(lb + static_cast<uint32_t>(e.x) * np);
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
         key[q] = KO::kmin(key[q], KO::make(cv.x[q], static_cast<uint32_t>(e.y), e.x));
     }
     rows_scanned += nrows - head;
     head = nrows;
+    KMB_WSTAGE(0);
     if (epochs == 0 && rounds == 1 && a.seed == 1) {  // column reduction, :328-333
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
@@ -250,6 +257,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       D = m;  // dual step (hungarian.cpp:207-215), applied lazily
       ++dual_steps;
     }
+    KMB_WSTAGE(1);
     // ---- absorb zero-slack columns (hungarian.cpp:186-199) ----
     // Usually one column per round turns tight: only its lane branches in, and
     // appends go through warp-private shared counters (no per-column ballots).
@@ -282,6 +290,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     __syncwarp();
     nrows = S.ctr[0];
     const int nfound = S.ctr[1];
+    KMB_WSTAGE(2);
     if (nfound == 0) continue;
 
     // ---- epoch end: augment and dissolve the trees that reached a free column.
@@ -350,7 +359,9 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     nrows = ns;
     head = 0;  // survivors relax once more for the reset columns
     ++epochs;
+    KMB_WSTAGE(3);
   }
+#undef KMB_WSTAGE
   const long long cycles = clock64() - t_start;
   // ---- outputs ----
   int64_t tot = 0;
@@ -358,7 +369,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     const int32_t mr = match_row[k];
     a.row_to_col[static_cast<int64_t>(inst) * n + k] = mr;
     a.u[static_cast<int64_t>(inst) * n + k] = u[k];
-    if (mr >= 0) tot += SMEM_C ? Cm[static_cast<int64_t>(k) * np + mr] : __ldg(Cm + static_cast<int64_t>(k) * np + mr);
+    if (mr >= 0) tot += SMEM_C ? Cm[k * np + mr] : __ldg(Cm + k * np + mr);
   }
 #pragma unroll
   for (int q = 0; q < CPL; ++q)
@@ -374,6 +385,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       o[2] = rows_scanned;
       o[3] = rounds;
       o[4] = cycles;
+      for (int k = 0; k < 4; ++k) o[5 + k] = cyc[k];
     }
   }
   return status;
@@ -413,7 +425,6 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
   __syncwarp();
   uint32_t parity = 0;
   const int c0 = CPL * lane;
-  const int avail = np - c0;
 
   for (int inst = blockIdx.x * wpb + wib; inst < a.batch; inst += gridDim.x * wpb) {
     const int32_t* Cg = a.C + static_cast<int64_t>(inst) * n * np;
@@ -445,22 +456,31 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
     // validation (core.cpp:144-145 + device range) and row reductions
     // (hungarian.cpp:323-327): the warp walks the rows, lanes across columns
     int32_t lo_all = 0x7fffffff, hi_all = 0;
-    for (int i = 0; i < n; ++i) {
-      const RowVec<CPL> cv = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(i) * np + c0, avail);
-      int32_t lo = 0x7fffffff, hi = 0;
+    // 8 rows in flight: loads first, then the per-row reductions
+    for (int i0 = 0; i0 < n; i0 += 8) {
+      RowVec<CPL> cv[8];
 #pragma unroll
-      for (int q = 0; q < CPL; ++q)
-        if (c0 + q < n) {
-          lo = min(lo, cv.x[q]);
-          hi = max(hi, cv.x[q]);
+      for (int k = 0; k < 8; ++k)
+        cv[k] = load_row<CPL, SMEM_C>(Cm + static_cast<int64_t>(min(i0 + k, n - 1)) * np + c0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k;
+        if (i >= n) break;  // warp-uniform
+        int32_t lo = 0x7fffffff, hi = 0;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          if (c0 + q < n) {
+            lo = min(lo, cv[k].x[q]);
+            hi = max(hi, cv[k].x[q]);
+          }
+        lo = __reduce_min_sync(FULL, lo);
+        lo_all = min(lo_all, lo);
+        hi_all = max(hi_all, hi);
+        if (lane == (i & 31)) {
+          const int32_t u0 = a.seed == 1 ? lo : 0;
+          S.u[i] = u0;
+          S.w[i] = u0;
         }
-      lo = __reduce_min_sync(FULL, lo);
-      lo_all = min(lo_all, lo);
-      hi_all = max(hi_all, hi);
-      if (lane == (i & 31)) {
-        const int32_t u0 = a.seed == 1 ? lo : 0;
-        S.u[i] = u0;
-        S.w[i] = u0;
       }
     }
     hi_all = __reduce_max_sync(FULL, hi_all);
@@ -486,8 +506,8 @@ size_t warp_smem_per_warp(int n, int pitch, bool smem_c) {
 }
 
 template <int CPL, bool SMEM_C>
-static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, cudaStream_t st,
-                            int* grid_out) {
+static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, int warps_per_sm,
+                            cudaStream_t st, int* grid_out) {
   auto kern = k_warp_batch<CPL, SMEM_C>;
   const size_t smem = warp_smem_per_warp(a.n, a.pitch, SMEM_C) * wpb;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -498,6 +518,7 @@ static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, cudaStream
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int warps_needed = a.batch;
+  if (warps_per_sm > 0 && warps_per_sm / wpb < occ) occ = warps_per_sm / wpb > 0 ? warps_per_sm / wpb : 1;
   int grid = sm_count * occ;
   const int grid_needed = (warps_needed + wpb - 1) / wpb;
   if (grid > grid_needed) grid = grid_needed;
@@ -506,15 +527,20 @@ static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, cudaStream
   return cudaGetLastError();
 }
 
-cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, cudaStream_t st,
-                              int* grid_out) {
-  if (a.n < 1 || a.n > 256 || a.pitch % 4 != 0) return cudaErrorInvalidValue;
-  const int cpl = a.n <= 32 ? 1 : a.n <= 64 ? 2 : a.n <= 128 ? 4 : 8;
+int warp_pitch(int n) {
+  const int cpl = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
+  return 32 * cpl;
+}
+
+cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int warps_per_sm,
+                              cudaStream_t st, int* grid_out) {
+  if (a.n < 1 || a.n > 256 || a.pitch != warp_pitch(a.n)) return cudaErrorInvalidValue;
+  const int cpl = a.pitch / 32;
   if (smem_c && warp_smem_per_warp(a.n, a.pitch, true) > 227 * 1024) smem_c = false;
   const int wpb = smem_c ? 1 : 4;
-#define KMB_L(C)                                                                   \
-  return smem_c ? launch_t<C, true>(a, sm_count, wpb, st, grid_out)                \
-                : launch_t<C, false>(a, sm_count, wpb, st, grid_out)
+#define KMB_L(C)                                                                          \
+  return smem_c ? launch_t<C, true>(a, sm_count, wpb, warps_per_sm, st, grid_out)         \
+                : launch_t<C, false>(a, sm_count, wpb, warps_per_sm, st, grid_out)
   switch (cpl) {
     case 1: KMB_L(1);
     case 2: KMB_L(2);
