@@ -108,6 +108,25 @@ int kmb_solve_batch_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, i
                         int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
                         int64_t* total_cost, kmb_stats* stats);
 
+/* ---- column-sharded single instance across ranks/GPUs (config 5) ----------
+ * Rank r owns columns [col_begin, col_begin + ncols) of the n x n matrix
+ * (`slab`: n rows x ncols, leading dimension ld).  Every rank calls
+ * kmb_solve_sharded_i32 collectively; each returns the full assignment and u
+ * (replicated) and the v of its own columns.  The per-round min-slack combine
+ * and the entry exchanges go through NCCL (kmb_shard_init_nccl; rank 0 makes
+ * the id with kmb_nccl_unique_id and the caller broadcasts it) or through
+ * caller callbacks (kmb_shard_init_callbacks; e.g. torch.distributed gloo). */
+typedef int (*kmb_allreduce_min_i64_fn)(int64_t* inout, int32_t count, void* user);
+typedef int (*kmb_allgather_fn)(const void* send, int64_t bytes, void* recv, void* user);
+int kmb_nccl_unique_id(uint8_t* out128);
+int kmb_shard_init_nccl(kmb_context* ctx, int32_t nranks, int32_t rank, const uint8_t* id128);
+int kmb_shard_init_callbacks(kmb_context* ctx, int32_t nranks, int32_t rank,
+                             kmb_allreduce_min_i64_fn allreduce_min, kmb_allgather_fn allgather,
+                             void* user);
+int kmb_solve_sharded_i32(kmb_context* ctx, const int32_t* slab, int32_t n, int64_t ld,
+                          int32_t col_begin, int32_t ncols, int32_t seed, int32_t* row_to_col,
+                          int64_t* u, int64_t* v_slab, int64_t* total_cost, kmb_stats* stats);
+
 /* Diagnostics: the grid engine's reduced-cost scan with every row in the
  * frontier (one full pass over the matrix per iteration), averaged over
  * `iters` passes; bytes counted = 4*n*n per pass. */

@@ -20,7 +20,7 @@ GEN_SO = os.path.join(PKG, "libkmb_gen.so")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["kmb_solver.cu", "kmb_batch.cu", "kmb_warp.cu", "kmb_capi.cu"]
+CU_SOURCES = ["kmb_solver.cu", "kmb_batch.cu", "kmb_warp.cu", "kmb_shard.cu", "kmb_capi.cu"]
 CU_HEADERS = ["kmb_common.cuh", "kmb_internal.h"]
 
 
@@ -51,7 +51,7 @@ def build_lib(force: bool = False, extra: list[str] | None = None) -> str:
     if force or _stale(LIB_SO, deps):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, *srcs, "-o", LIB_SO + ".tmp",
-               "-lcudart"]
+               "-lcudart", "-ldl"]
         cmd += extra or []
         _run(cmd)
         os.replace(LIB_SO + ".tmp", LIB_SO)

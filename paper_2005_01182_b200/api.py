@@ -27,7 +27,9 @@ OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM = 1, 2, 3, 4
 
 # every symbol include/kmb.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
-               "kmb_solve_batch_i32", "kmb_bench_scan", "kmb_last_error", "kmb_abi_version")
+               "kmb_solve_batch_i32", "kmb_nccl_unique_id", "kmb_shard_init_nccl",
+               "kmb_shard_init_callbacks", "kmb_solve_sharded_i32", "kmb_bench_scan",
+               "kmb_last_error", "kmb_abi_version")
 
 
 class KmbUnavailable(RuntimeError):

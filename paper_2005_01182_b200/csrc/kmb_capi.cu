@@ -79,7 +79,16 @@ struct kmb_context {
       ctrl, obj;
   // batch workspace
   DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus;
+  // column-sharded solve: the collective (NCCL or caller callbacks)
+  std::unique_ptr<kmb::Exchange> exchange;
 };
+
+namespace kmb {
+std::unique_ptr<Exchange>& context_exchange(kmb_context* c) { return c->exchange; }
+cudaStream_t context_stream(kmb_context* c) { return c->stream; }
+int context_device(kmb_context* c) { return c->device; }
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace kmb
 
 extern "C" {
 

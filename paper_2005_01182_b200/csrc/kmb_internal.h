@@ -4,6 +4,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
+#include <string>
+
+#include "kmb.h"
+#include "kmb_shard_proto.h"
 
 namespace kmb {
 
@@ -98,4 +103,21 @@ int warp_max_n();
 int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)
 cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int warps_per_sm,
                               cudaStream_t st, int* grid_out);
+}  // namespace kmb
+
+namespace kmb {
+// ---- column-sharded solve (kmb_shard.cu): the collective interface ------------
+using Exchange = ShardExchange;  // kmb_shard_proto.h
+struct CallbackExchange : Exchange {
+  kmb_allreduce_min_i64_fn ar = nullptr;
+  kmb_allgather_fn ag = nullptr;
+  void* user = nullptr;
+  int allreduce_min(int64_t* p, int32_t count) override { return ar(p, count, user); }
+  int allgather(const void* s, int64_t bytes, void* r) override { return ag(s, bytes, r, user); }
+};
+// context accessors (the context struct lives in kmb_capi.cu)
+std::unique_ptr<Exchange>& context_exchange(kmb_context* c);
+cudaStream_t context_stream(kmb_context* c);
+int context_device(kmb_context* c);
+void set_last_error(const std::string& msg);
 }  // namespace kmb

@@ -6,6 +6,10 @@ set -e
 HERE=$(cd "$(dirname "$0")" && pwd)
 ROOT=$(cd "$HERE/../.." && pwd)
 REF=${OT_REF_DIR:-/root/reference/proj}
+mkdir -p "$HERE/build"
+# simulated-shard protocol library (no reference needed)
+g++ -O2 -std=c++17 -fPIC -shared -I"$ROOT/paper_2005_01182_b200/csrc" "$HERE/shard_sim.cpp" \
+  -o "$HERE/build/libshardsim.so"
 if [ ! -f "$REF/include/ot/hungarian.hpp" ]; then
   echo "reference headers absent; keeping prebuilt binary" ; exit 0
 fi
