@@ -344,8 +344,10 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "k_warp_batch", "peak_source": peak_src,
-                         "note": "SMEM-resident: algorithmic bytes are SURVEY 8(d) 4n^2 per phase, "
-                                 "re-read from shared memory; HBM reads each matrix once"},
+                         "note": "L1/L2-resident re-reads: algorithmic bytes are SURVEY 8(d)'s "
+                                 "4n^2 per phase (+2 reductions) per instance, mostly served from "
+                                 "L2, so achieved can exceed the HBM peak; traffic = ncu DRAM "
+                                 "bytes of one launch (profiles/ncu_batch_summary.json)"},
             "cpu_baseline": cpu,
             "e2e": {"value": BATCH / (e2e_ms * 1e-3), "unit": "solves/s",
                     "h2d_bytes_per_step": int(host.nbytes),

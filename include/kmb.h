@@ -64,9 +64,10 @@ enum kmb_option {
   KMB_OPT_MAX_CTAS = 1,     /* grid engine: upper bound on CTAs (0 = #SMs)      */
   KMB_OPT_CONTINUE_BFS = 2, /* 1: exhaust the tight closure before augmenting   */
   KMB_OPT_ENGINE = 3,       /* 0 auto (warp n<=256, cluster n<=8192, grid),
-                               1 grid (persistent), 2 CTA/SMEM (n<=224),
-                               3 warp/SMEM, 4 warp/L2 (n <= 256),
-                               5 cluster (grid engine on one <=16-CTA cluster)  */
+                               1 grid (persistent), 2 CTA/SMEM, 6 CTA/L2,
+                               3 warp/SMEM, 4 warp/L2 (2,3,4,6: n <= 256),
+                               5 cluster (grid engine on one <=16-CTA cluster);
+                               stats->engine 7 = column-sharded              */
   KMB_OPT_WARPS_PER_SM = 4  /* warp engine: resident instances per SM (0 = max);
                                bounds the L2 working set of streamed matrices   */
 };
@@ -78,7 +79,7 @@ typedef struct kmb_stats {
   int64_t cost_bytes_read; /* 4*n*(rows_scanned + n) (+ reductions)          */
   double seconds;          /* device time of the solve (CUDA events)         */
   int32_t converged;       /* 0 when the time budget expired                 */
-  int32_t engine;          /* 1 grid, 2 SMEM                                 */
+  int32_t engine;          /* the engine that ran (KMB_OPT_ENGINE numbering) */
   int64_t rounds;          /* search rounds (relax | min | absorb)           */
   int64_t stage_ns[6];     /* grid engine, CTA 0's clock (ns): relax, barrier 1,
                               absorb, barrier 2, epoch end, barrier 3;

@@ -1,15 +1,19 @@
-// Batched small instances (BASELINE config 3: 4096 independent n=128 solves):
-// one CTA per instance, the whole n x n cost matrix staged into shared memory
-// by a TMA bulk copy (cp.async.bulk + mbarrier), every per-phase structure in
-// SMEM, __syncthreads as the only barrier.  Persistent CTAs stride over the
-// instances; several CTAs per SM overlap one instance's TMA load with the
-// others' solves.
+// CTA engine for batched small instances (BASELINE config 3: 4096 independent
+// n = 128 solves): ONE CTA PER INSTANCE, one column per thread (T = 32*ceil(n/32)),
+// persistent CTAs striding over the instances.  Same search as the grid and
+// warp engines — incremental epochs with lazy duals (hungarian.cpp:175-217
+// restated), argmin-parent forest augmentation in place of TightPhase
+// (:223-309), the reductions of :323-333 as seed 1 — laid out so a round's
+// dependency chain is short: each thread folds only its own column, the
+// min-slack reduction is one REDUX per warp plus one shared-memory exchange,
+// and a round costs two CTA barriers.
 //
-// The algorithm is exactly the engine of kmb_solver.cu with G = 1 (thread j
-// owns column j, so the per-column min needs no cross-thread merge):
-// multi-source search with lazy duals (hungarian.cpp:175-217 restated),
-// argmin-parent forest augmentation in place of TightPhase
-// (hungarian.cpp:223-309), reductions of hungarian.cpp:323-333 as seed 1.
+// Cost source (template SMEM_C): the instance's matrix staged into shared
+// memory by one TMA bulk copy (cp.async.bulk + mbarrier), or streamed from
+// L2 with coalesced loads (more CTAs per SM, bounded by KMB_OPT_WARPS_PER_SM
+// so the resident matrices stay in L2).
+// Keys (NARROW): 32-bit ((c - w + 2^22) << 8) | row when n <= 256 and costs
+// < 2^21, else 64-bit ((c - w + 2^30) << 32) | row (kmb_common.cuh).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -19,315 +23,391 @@
 
 namespace kmb {
 
-constexpr int kBatchMaxN = 224;  // n*n*4 + per-row state must fit 227 KB
+namespace {
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+__device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes,
-                                              uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-struct BatchSmem {
-  uint64_t bar;
-  int32_t tail;
-  int32_t ntail;
-  int32_t nfound;
-  int32_t status;
-  int64_t part[8];
-  int64_t m;
+template <bool NARROW>
+struct CKeys;
+template <>
+struct CKeys<false> {
+  using K = uint64_t;
+  static constexpr K INF = ~0ull;
+  __device__ static uint32_t tag(int32_t w, int32_t) {
+    return static_cast<uint32_t>(static_cast<int32_t>(KMB_BIAS) - w);
+  }
+  __device__ static K make(int32_t c, uint32_t tag, int32_t row) {
+    return (static_cast<uint64_t>(static_cast<uint32_t>(c) + tag) << 32) | static_cast<uint32_t>(row);
+  }
+  __device__ static int32_t val(K k) { return static_cast<int32_t>(static_cast<int64_t>(k >> 32) - KMB_BIAS); }
+  __device__ static int32_t row(K k) { return static_cast<int32_t>(static_cast<uint32_t>(k)); }
+  __device__ static K kmin(K a, K b) { return a < b ? a : b; }
+};
+template <>
+struct CKeys<true> {
+  using K = uint32_t;
+  static constexpr K INF = 0xffffffffu;
+  static constexpr int32_t NB = 1 << 22;
+  __device__ static uint32_t tag(int32_t w, int32_t row) {
+    return (static_cast<uint32_t>(NB - w) << 8) | static_cast<uint32_t>(row);
+  }
+  __device__ static K make(int32_t c, uint32_t tag, int32_t) { return (static_cast<uint32_t>(c) << 8) + tag; }
+  __device__ static int32_t val(K k) { return static_cast<int32_t>(k >> 8) - NB; }
+  __device__ static int32_t row(K k) { return static_cast<int32_t>(k & 0xffu); }
+  __device__ static K kmin(K a, K b) { return min(a, b); }
 };
 
-// dynamic smem: Cs[n*n] | u[n] w[n] (i64) | claim[n] (u64) | list[2][n]
-//               match_row[n] match_col[n] root_row[n] tree_par[n] found[n] (i32)
-__host__ __device__ inline size_t batch_smem_bytes(int n) {
-  const size_t cs = ((static_cast<size_t>(n) * n * 4) + 15) & ~static_cast<size_t>(15);
-  return cs + static_cast<size_t>(n) * (8 + 8 + 8 + 4 * 7);
+__device__ __forceinline__ uint32_t cclaim(int epoch, int col) {
+  return (static_cast<uint32_t>(0xFFFFFE - epoch) << 8) | static_cast<uint32_t>(col);
+}
+__device__ __forceinline__ bool cclaimed(uint32_t c, int epoch) {
+  return (c >> 8) == static_cast<uint32_t>(0xFFFFFE - epoch);
 }
 
-__global__ void __launch_bounds__(256) k_batch_solve(BatchArgs a) {
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ BatchSmem sm;
-  const int n = a.n;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int T = blockDim.x, nw = T >> 5;
-  int32_t* Cs = reinterpret_cast<int32_t*>(dyn);
-  const size_t cs_bytes = ((static_cast<size_t>(n) * n * 4) + 15) & ~static_cast<size_t>(15);
-  int64_t* u = reinterpret_cast<int64_t*>(dyn + cs_bytes);
-  int64_t* w = u + n;
-  uint64_t* claim = reinterpret_cast<uint64_t*>(w + n);
-  int32_t* lists = reinterpret_cast<int32_t*>(claim + n);
-  int32_t* match_row = lists + 2 * n;
-  int32_t* match_col = match_row + n;
-  int32_t* root_row = match_col + n;
-  int32_t* tree_par = root_row + n;
-  int32_t* found = tree_par + n;
+struct CtaShared {
+  uint64_t bar;  // mbarrier of the TMA bulk copy
+  int32_t nrows, nfound, ns, won;
+  int32_t lo_all, hi_all;
+  int32_t red[8];  // per-warp min slack' / partial sums
+};
 
-  const bool bulk = ((n * n) & 3) == 0;  // 16 B granularity of cp.async.bulk
-  if (tid == 0) mbar_init(&sm.bar, 1);
-  __syncthreads();
-  uint32_t mbar_parity = 0;
-  const int j = tid;  // owned column (and row, for per-row init)
+template <bool SMEM_C>
+__device__ __forceinline__ int32_t ldc(const int32_t* p) {
+  if constexpr (SMEM_C) return *p;
+  else return __ldg(p);
+}
+
+}  // namespace
+
+// dynamic smem: [Cs n*n (SMEM_C)] | rows[2][n] (int2) | u w root_row match_row
+// match_col tree_par found (int32 x n) | claim (u32 x n)
+__host__ __device__ inline size_t cta_smem_bytes(int n, bool smem_c) {
+  const size_t cs = smem_c ? ((static_cast<size_t>(n) * n * 4 + 15) & ~static_cast<size_t>(15)) : 0;
+  return cs + static_cast<size_t>(n) * (2 * 8 + 8 * 4);
+}
+
+template <bool SMEM_C, bool NARROW>
+__device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, int inst,
+                                         CtaShared& sm, int2* rows, int2* spare, int32_t* u,
+                                         int32_t* w, int32_t* root_row, int32_t* match_row,
+                                         int32_t* match_col, int32_t* tree_par, int32_t* found,
+                                         uint32_t* claim) {
+  using KO = CKeys<NARROW>;
+  using K = typename KO::K;
+  constexpr uint32_t FULL = 0xffffffffu;
+  const int n = a.n, T = blockDim.x, nw = T >> 5;
+  const int j = threadIdx.x, lane = j & 31, wid = j >> 5;
   const bool own = j < n;
+  const int32_t* colp = Cm + (own ? j : 0);  // this thread's column
+
+  for (int k = j; k < n; k += T) rows[k] = make_int2(k, static_cast<int32_t>(KO::tag(w[k], k)));
+  if (j == 0) {
+    sm.nrows = n;
+    sm.nfound = 0;
+  }
+  K key = KO::INF;
+  int32_t v = 0, dc = 0;
+  bool rch = !own;
+  int nrows = n, head = 0, nfree = n;
+  int32_t D = 0;
+  int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
+  int status = 0;
+  long long cyc[4] = {0, 0, 0, 0};  // relax, min (incl. B1), absorb (incl. B2), epoch end
+  long long tl = clock64();
+#define KMB_CSTAGE(k)               \
+  do {                              \
+    const long long t_ = clock64(); \
+    cyc[k] += t_ - tl;              \
+    tl = t_;                        \
+  } while (0)
+  __syncthreads();
+
+  while (nfree > 0) {
+    ++rounds;
+    // ---- relax rows[head, nrows) for column j (hungarian.cpp:164-172) ----
+    int r = head;
+    for (; r + 7 < nrows; r += 8) {
+      int2 e[8];
+      int32_t c[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e[k] = rows[r + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
+    }
+    for (; r < nrows; ++r) {
+      const int2 e = rows[r];
+      key = KO::kmin(key, KO::make(ldc<SMEM_C>(colp + e.x * n), static_cast<uint32_t>(e.y), e.x));
+    }
+    if (rounds == 1 && a.seed == 1 && own) v = KO::val(key);  // column reduction, :328-333
+    rows_scanned += nrows - head;
+    head = nrows;
+    KMB_CSTAGE(0);
+    // ---- min unreached slack' (hungarian.cpp:203-206): REDUX + one exchange ----
+    const int32_t s = rch ? 0x7fffffff : KO::val(key) - v;
+    const int32_t wm = __reduce_min_sync(FULL, s);
+    if (lane == 0) sm.red[wid] = wm;
+    __syncthreads();  // ------------------------------------------------ B1
+    int32_t m = sm.red[0];
+    for (int q = 1; q < nw; ++q) m = min(m, sm.red[q]);
+    if (m > D) {
+      if (m == 0x7fffffff) {
+        status = -2;
+        break;
+      }
+      D = m;  // dual step (hungarian.cpp:207-215), applied lazily
+      ++dual_steps;
+    }
+    KMB_CSTAGE(1);
+    // ---- absorb (hungarian.cpp:186-199) ----
+    if (!rch && s == D) {
+      rch = true;
+      dc = D;
+      const int32_t par = KO::row(key);
+      tree_par[j] = par;
+      const int32_t root = root_row[par];
+      const int32_t i2 = match_col[j];
+      if (i2 < 0) {
+        atomicMin(claim + root, cclaim(epochs, j));
+        found[atomicAdd(&sm.nfound, 1)] = j;
+      } else {
+        const int32_t w2 = u[i2] - D;
+        w[i2] = w2;
+        root_row[i2] = root;
+        rows[atomicAdd(&sm.nrows, 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
+      }
+    }
+    __syncthreads();  // ------------------------------------------------ B2
+    nrows = sm.nrows;
+    const int nfound = sm.nfound;
+    KMB_CSTAGE(2);
+    if (nfound == 0) continue;
+
+    // ---- epoch end: augment and dissolve the trees that reached a free column
+    if (own) {
+      if (rch) {
+        if (cclaimed(claim[root_row[tree_par[j]]], epochs)) {
+          v -= D - dc;
+          rch = false;
+          key = KO::INF;
+        }
+      } else if (key != KO::INF && cclaimed(claim[root_row[KO::row(key)]], epochs)) {
+        key = KO::INF;
+      }
+    }
+    if (j == 0) {
+      sm.ns = 0;
+      sm.won = 0;
+    }
+    __syncthreads();
+    for (int q = j; q < nrows; q += T) {
+      const int2 e = rows[q];
+      if (cclaimed(claim[root_row[e.x]], epochs)) u[e.x] = w[e.x] + D;
+      else spare[atomicAdd(&sm.ns, 1)] = e;
+    }
+    for (int f = j; f < nfound; f += T) {
+      int32_t jj = found[f];
+      if (claim[root_row[tree_par[jj]]] != cclaim(epochs, jj)) continue;
+      atomicAdd(&sm.won, 1);
+      for (;;) {
+        const int32_t i = tree_par[jj];
+        const int32_t nx = match_row[i];
+        match_row[i] = jj;
+        match_col[jj] = i;
+        if (nx < 0) break;
+        jj = nx;
+      }
+    }
+    __syncthreads();
+    nfree -= sm.won;
+    nrows = sm.ns;
+    int2* t = rows;
+    rows = spare;
+    spare = t;
+    head = 0;  // survivors relax once more for the reset columns
+    ++epochs;
+    __syncthreads();
+    if (j == 0) {
+      sm.nrows = nrows;
+      sm.nfound = 0;
+    }
+    __syncthreads();
+    KMB_CSTAGE(3);
+  }
+#undef KMB_CSTAGE
+  // ---- outputs ----
+  int32_t tot = 0;  // per-thread entry < 2^29; per-warp sum < 2^34 -> reduce in 64 bits
+  int64_t tot64 = 0;
+  if (own) {
+    const int32_t mr = match_row[j];
+    a.row_to_col[static_cast<int64_t>(inst) * n + j] = mr;
+    a.u[static_cast<int64_t>(inst) * n + j] = u[j];
+    a.v[static_cast<int64_t>(inst) * n + j] = v;
+    if (mr >= 0) tot = ldc<SMEM_C>(Cm + j * n + mr);
+  }
+  tot64 = tot;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot64 += __shfl_xor_sync(FULL, tot64, o);
+  __syncthreads();
+  if (lane == 0) reinterpret_cast<int64_t*>(spare)[wid] = tot64;  // spare rows are dead now
+  __syncthreads();
+  if (j == 0) {
+    int64_t t = 0;
+    for (int q = 0; q < nw; ++q) t += reinterpret_cast<int64_t*>(spare)[q];
+    a.total_cost[inst] = t;
+    if (a.stats) {
+      int64_t* o = a.stats + KMB_ISTATS * static_cast<int64_t>(inst);
+      o[0] = epochs;
+      o[1] = dual_steps;
+      o[2] = rows_scanned;
+      o[3] = rounds;
+      o[4] = cyc[0] + cyc[1] + cyc[2] + cyc[3];
+      for (int k = 0; k < 4; ++k) o[5 + k] = cyc[k];
+    }
+  }
+  return status;
+}
+
+template <bool SMEM_C>
+__global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ CtaShared sm;
+  const int n = a.n, T = blockDim.x;
+  const int j = threadIdx.x;
+  const size_t cs = SMEM_C ? ((static_cast<size_t>(n) * n * 4 + 15) & ~static_cast<size_t>(15)) : 0;
+  int32_t* Cs = reinterpret_cast<int32_t*>(dyn);
+  int2* rows = reinterpret_cast<int2*>(dyn + cs);
+  int2* spare = rows + n;
+  int32_t* u = reinterpret_cast<int32_t*>(spare + n);
+  int32_t* w = u + n;
+  int32_t* root_row = w + n;
+  int32_t* match_row = root_row + n;
+  int32_t* match_col = match_row + n;
+  int32_t* tree_par = match_col + n;
+  int32_t* found = tree_par + n;
+  uint32_t* claim = reinterpret_cast<uint32_t*>(found + n);
+  const bool bulk = SMEM_C && ((static_cast<int64_t>(n) * n) & 3) == 0;
+  if (bulk && j == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&sm.bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t parity = 0;
 
   for (int inst = blockIdx.x; inst < a.batch; inst += gridDim.x) {
     const int32_t* Cg = a.C + static_cast<int64_t>(inst) * n * n;
-    // ---- stage the cost matrix: TMA bulk copy into SMEM ----
-    if (bulk) {
-      if (tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t total = static_cast<uint32_t>(n) * n * 4;
-        mbar_arrive_expect_tx(&sm.bar, total);
-        const uint32_t chunk = 32768;
-        for (uint32_t off = 0; off < total; off += chunk) {
-          const uint32_t b = total - off < chunk ? total - off : chunk;
-          bulk_copy_g2s(reinterpret_cast<unsigned char*>(Cs) + off,
-                        reinterpret_cast<const unsigned char*>(Cg) + off, b, &sm.bar);
+    const int32_t* Cm = SMEM_C ? Cs : Cg;
+    if constexpr (SMEM_C) {  // stage the matrix: TMA bulk copy into shared memory
+      if (bulk) {
+        if (j == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const uint32_t total = static_cast<uint32_t>(n) * n * 4;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&sm.bar)),
+                       "r"(total)
+                       : "memory");
+          for (uint32_t off = 0; off < total; off += 32768u) {
+            const uint32_t b = total - off < 32768u ? total - off : 32768u;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                    "r"(saddr(reinterpret_cast<unsigned char*>(Cs) + off)),
+                "l"(reinterpret_cast<const unsigned char*>(Cg) + off), "r"(b), "r"(saddr(&sm.bar))
+                : "memory");
+          }
         }
+      } else {
+        for (int k = j; k < n * n; k += T) Cs[k] = Cg[k];
       }
-    } else {
-      for (int k = tid; k < n * n; k += T) Cs[k] = Cg[k];
     }
-    // per-row / per-column init overlaps the copy
-    if (own) {
-      match_row[j] = -1;
-      match_col[j] = -1;
-      claim[j] = KMB_KEY_INF;
-      root_row[j] = j;
-      lists[j] = j;
+    for (int k = j; k < n; k += T) {
+      match_row[k] = -1;
+      match_col[k] = -1;
+      claim[k] = 0xFFFFFFFFu;
+      root_row[k] = k;
     }
-    if (tid == 0) {
-      sm.tail = n;
-      sm.ntail = 0;
-      sm.nfound = 0;
-      sm.status = 0;
+    if (j == 0) {
+      sm.lo_all = 0x7fffffff;
+      sm.hi_all = 0;
     }
     if (bulk) {
-      mbar_wait(&sm.bar, mbar_parity);
-      mbar_parity ^= 1;
+      asm volatile(
+          "{\n.reg .pred p;\nW_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          "@!p bra W_%=;\n}\n" ::"r"(saddr(&sm.bar)),
+          "r"(parity)
+          : "memory");
+      parity ^= 1;
     }
     __syncthreads();
     // validation (core.cpp:144-145 + device range) and row reductions
-    // (hungarian.cpp:323-327): one warp per row, conflict-free
-    for (int i = wid; i < n; i += nw) {
-      int32_t lo = 0x7fffffff, hi = 0;
-      for (int k = lane; k < n; k += 32) {
-        const int32_t x = Cs[i * n + k];
-        lo = min(lo, x);
-        hi = max(hi, x);
+    // (hungarian.cpp:323-327): one warp per row, lanes across columns
+    {
+      const int lane = j & 31, wid = j >> 5, nw = T >> 5;
+      int32_t lo_all = 0x7fffffff, hi_all = 0;
+      for (int i = wid; i < n; i += nw) {
+        int32_t lo = 0x7fffffff, hi = 0;
+        for (int k = lane; k < n; k += 32) {
+          const int32_t x = ldc<SMEM_C>(Cm + i * n + k);
+          lo = min(lo, x);
+          hi = max(hi, x);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        lo_all = min(lo_all, lo);
+        hi_all = max(hi_all, hi);
+        if (lane == 0) {
+          const int32_t u0 = a.seed == 1 ? lo : 0;
+          u[i] = u0;
+          w[i] = u0;
+        }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
-      const int64_t u0 = a.seed == 1 ? lo : 0;
       if (lane == 0) {
-        if (lo < 0) atomicMax(&sm.status, 2);
-        else if (hi >= (1 << 29)) atomicMax(&sm.status, 3);
-        u[i] = u0;
-        w[i] = u0;
+        atomicMin(&sm.lo_all, lo_all);
+        atomicMax(&sm.hi_all, hi_all);
       }
     }
     __syncthreads();
-    if (sm.status != 0) {  // invalid instance: report, produce no assignment
-      if (own) a.row_to_col[static_cast<int64_t>(inst) * n + j] = -1;
-      if (tid == 0) {
-        a.status[inst] = sm.status;
-        a.total_cost[inst] = 0;
-      }
-      __syncthreads();
-      continue;
+    const int32_t lo_all = sm.lo_all, hi_all = sm.hi_all;
+    int status = lo_all < 0 ? 2 : (hi_all >= (1 << 29) ? 3 : 0);
+    if (status) {
+      for (int k = j; k < n; k += T) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
+      if (j == 0) a.total_cost[inst] = 0;
+    } else if (hi_all < (1 << 21)) {
+      status = cta_solve<SMEM_C, true>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
+                                       match_col, tree_par, found, claim);
+    } else {
+      status = cta_solve<SMEM_C, false>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
+                                        match_col, tree_par, found, claim);
     }
-
-    int64_t v = 0, dc = 0;
-    int64_t dual_steps = 0, rows_scanned = 0, phases = 0;
-    int32_t* list = lists;
-    int32_t* next = lists + n;
-    bool fatal = false;
-    for (int phase = 0;; ++phase) {
-      const int nroots = sm.tail;
-      if (nroots == 0) break;
-      uint64_t key = KMB_KEY_INF;
-      bool rch = !own;
-      int64_t D = 0;
-      int head = 0, tail = nroots, nfound = 0;
-      for (int round = 0;; ++round) {
-        // relax rows list[head, tail) for column j (hungarian.cpp:164-172)
-        if (own) {
-          int r = head;
-          for (; r + 3 < tail; r += 4) {
-            int32_t i[4];
-            uint32_t c[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) i[k] = list[r + k];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              c[k] = static_cast<uint32_t>(Cs[i[k] * n + j]) + row_bias(w[i[k]]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) key = umin64(key, pack_key(c[k], i[k]));
-          }
-          for (; r < tail; ++r) {
-            const int32_t i = list[r];
-            key = umin64(key, pack_key(static_cast<uint32_t>(Cs[i * n + j]) + row_bias(w[i]), i));
-          }
-          if (phase == 0 && round == 0 && a.seed == 1) v = key_val(key);  // :328-333
-        }
-        rows_scanned += tail - head;
-        int64_t s = (!rch) ? key_val(key) - v : KMB_I64_INF;
-        s = warp_min_i64(s);
-        if (lane == 0) sm.part[wid] = s;
-        __syncthreads();
-        int64_t m = KMB_I64_INF;
-        for (int q = 0; q < nw; ++q) m = sm.part[q] < m ? sm.part[q] : m;
-        if (m > D) {
-          if (nfound > 0) break;  // closure exhausted (continue_bfs)
-          if (m == KMB_I64_INF) {
-            fatal = true;
-            break;
-          }
-          D = m;
-          ++dual_steps;
-        }
-        if (!rch && key_val(key) - v == D) {  // absorb (hungarian.cpp:186-199)
-          rch = true;
-          dc = D;
-          const int32_t par = key_row(key);
-          tree_par[j] = par;
-          const int32_t root = root_row[par];
-          const int32_t i2 = match_col[j];
-          if (i2 < 0) {
-            atomicMin(reinterpret_cast<unsigned long long*>(claim + root), claim_key(phase, j));
-            found[atomicAdd(&sm.nfound, 1)] = j;
-          } else {
-            w[i2] = u[i2] - D;
-            root_row[i2] = root;
-            list[atomicAdd(&sm.tail, 1)] = i2;
-          }
-        }
-        __syncthreads();
-        head = tail;
-        tail = sm.tail;
-        nfound = sm.nfound;
-        if (nfound > 0 && (!a.continue_bfs || head == tail)) break;
-      }
-      if (fatal) break;
-      // ---- end of phase ----
-      for (int r = tid; r < tail; r += T) {
-        const int32_t i = list[r];
-        const int64_t un = w[i] + D;
-        u[i] = un;
-        if (r < nroots && !claimed_in(claim[i], phase)) {
-          const int pos = atomicAdd(&sm.ntail, 1);
-          next[pos] = i;
-          w[i] = un;
-          root_row[i] = i;
-        }
-      }
-      if (rch && own) v -= D - dc;
-      for (int f = tid; f < nfound; f += T) {
-        int32_t jj = found[f];
-        const int32_t root = root_row[tree_par[jj]];
-        if (claim[root] != claim_key(phase, jj)) continue;
-        for (;;) {
-          const int32_t i = tree_par[jj];
-          const int32_t nxt = match_row[i];
-          match_row[i] = jj;
-          match_col[jj] = i;
-          if (nxt < 0) break;
-          jj = nxt;
-        }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        sm.tail = sm.ntail;
-        sm.ntail = 0;
-        sm.nfound = 0;
-      }
-      int32_t* t = list;
-      list = next;
-      next = t;
-      ++phases;
-      __syncthreads();
-    }
-    // ---- outputs ----
-    int64_t tot = 0;
-    if (own) {
-      const int32_t mr = match_row[j];
-      a.row_to_col[static_cast<int64_t>(inst) * n + j] = mr;
-      a.u[static_cast<int64_t>(inst) * n + j] = u[j];
-      a.v[static_cast<int64_t>(inst) * n + j] = v;
-      tot = mr >= 0 ? Cs[j * n + mr] : 0;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    __syncthreads();  // everyone done reading sm.part / Cs before reuse
-    if (lane == 0) sm.part[wid] = tot;
-    __syncthreads();
-    if (tid == 0) {
-      int64_t t = 0;
-      for (int q = 0; q < nw; ++q) t += sm.part[q];
-      a.total_cost[inst] = t;
-      a.status[inst] = fatal ? -2 : 0;  // KMB_EINTERNAL
-      if (a.stats) {
-        int64_t* o = a.stats + KMB_ISTATS * static_cast<int64_t>(inst);
-        o[0] = phases;
-        o[1] = dual_steps;
-        o[2] = rows_scanned;
-        for (int k = 3; k < KMB_ISTATS; ++k) o[k] = 0;
-      }
-    }
+    if (j == 0) a.status[inst] = status;
     __syncthreads();
   }
 }
 
-int batch_max_n() { return kBatchMaxN; }
+int batch_max_n() { return 256; }
 
-cudaError_t launch_batch(const BatchArgs& a, int sm_count, cudaStream_t st, int* grid_out) {
-  if (a.n < 1 || a.n > kBatchMaxN) return cudaErrorInvalidValue;
+cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warps_per_sm,
+                         cudaStream_t st, int* grid_out) {
+  if (a.n < 1 || a.n > 256) return cudaErrorInvalidValue;
   const int threads = ((a.n + 31) / 32) * 32;
-  const size_t smem = batch_smem_bytes(a.n);
-  cudaError_t e = cudaFuncSetAttribute(k_batch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (smem_c && cta_smem_bytes(a.n, true) > 200 * 1024) smem_c = false;
+  const size_t smem = cta_smem_bytes(a.n, smem_c);
+  auto kern = smem_c ? k_cta_batch<true> : k_cta_batch<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch_solve, threads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   if (e != cudaSuccess) return e;
-  if (occ < 1) occ = 1;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  const int wpc = threads / 32;
+  if (warps_per_sm > 0 && warps_per_sm / wpc < occ) occ = warps_per_sm / wpc > 0 ? warps_per_sm / wpc : 1;
   int grid = sm_count * occ;
   if (grid > a.batch) grid = a.batch;
-  if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
-  k_batch_solve<<<grid, threads, smem, st>>>(a);
+  kern<<<grid, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -81,6 +82,10 @@ struct kmb_context {
   DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus;
   // column-sharded solve: the collective (NCCL or caller callbacks)
   std::unique_ptr<kmb::Exchange> exchange;
+  // chunked host-input pipeline of the batch engines
+  static constexpr int kAux = 4;
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t aux_ev[kAux] = {};
 };
 
 namespace kmb {
@@ -129,6 +134,10 @@ void kmb_destroy(kmb_context* c) {
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (int k = 0; k < kmb_context::kAux; ++k) {
+    if (c->aux_ev[k]) cudaEventDestroy(c->aux_ev[k]);
+    if (c->aux[k]) cudaStreamDestroy(c->aux[k]);
+  }
   delete c;
 }
 
@@ -145,7 +154,7 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
     case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_WARPS_PER_SM: c->warps_per_sm = value; return KMB_OK;
     case KMB_OPT_ENGINE:
-      if (value < 0 || value > 5) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..5");
+      if (value < 0 || value > 6) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..6");
       c->engine = static_cast<int>(value);
       return KMB_OK;
     default: return fail(KMB_EINVAL, "kmb_set_option: unknown option");
@@ -172,9 +181,18 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   cudaStream_t st = c->stream;
   const size_t cbytes = static_cast<size_t>(batch) * n * n * sizeof(int32_t);
   const int32_t* dcost = costs;
-  if (!is_device_ptr(costs)) {
+  if (engine == 0 || engine == 1 || engine == 5) engine = 4;  // auto: warp engine, costs from L2
+  // Host input to the warp engine in its natural pitch: stream the batch in
+  // chunks, each chunk's kernel starting as soon as its H2D copy lands, so the
+  // PCIe transfer overlaps the solves (the transfer, not the GPU, bounds the
+  // end-to-end rate).
+  const bool host_in = !is_device_ptr(costs);
+  const bool pipelined = host_in && (engine == 3 || engine == 4) && kmb::warp_pitch(n) == n &&
+                         batch >= 1024;
+  if (host_in) {
     KMB_CUDA(c->bcost.ensure(cbytes));
-    KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
+    if (!pipelined)
+      KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
     dcost = c->bcost.as<int32_t>();
   }
   const size_t nb = static_cast<size_t>(batch) * n;
@@ -186,10 +204,8 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   if (!is_device_ptr(total_cost)) { KMB_CUDA(c->btot.ensure(batch * 8)); dtot = c->btot.as<int64_t>(); }
   KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8));
   KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
-  if (engine == 0 || engine == 1) engine = 4;  // auto: warp engine, costs from L2
-  if (engine == 2 && n > kmb::batch_max_n()) engine = 4;
   int grid = 0;
-  if (engine == 2) {
+  if (engine == 2 || engine == 6) {
     kmb::BatchArgs a{};
     a.C = dcost;
     a.batch = batch;
@@ -203,7 +219,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.stats = c->bstat.as<int64_t>();
     a.status = c->bstatus.as<int32_t>();
     KMB_CUDA(cudaEventRecord(c->ev0, st));
-    KMB_CUDA(kmb::launch_batch(a, c->sm_count, st, &grid));
+    KMB_CUDA(kmb::launch_batch(a, c->sm_count, engine == 2, static_cast<int>(c->warps_per_sm), st, &grid));
   } else {
     const int np = kmb::warp_pitch(n);
     const int32_t* src = dcost;
@@ -227,7 +243,39 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.stats = c->bstat.as<int64_t>();
     a.status = c->bstatus.as<int32_t>();
     KMB_CUDA(cudaEventRecord(c->ev0, st));
-    KMB_CUDA(kmb::launch_warp_batch(a, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), st, &grid));
+    if (!pipelined) {
+      KMB_CUDA(kmb::launch_warp_batch(a, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), st, &grid));
+    } else {
+      if (!c->aux[0]) {
+        for (int k = 0; k < kmb_context::kAux; ++k) {
+          KMB_CUDA(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
+          KMB_CUDA(cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming));
+        }
+      }
+      const int K = 8;
+      const int chunk = (batch + K - 1) / K;
+      for (int k = 0; k < K; ++k) {
+        const int lo = k * chunk, cnt = std::min(chunk, batch - lo);
+        if (cnt <= 0) break;
+        cudaStream_t s = c->aux[k % kmb_context::kAux];
+        KMB_CUDA(cudaStreamWaitEvent(s, c->ev0, 0));
+        const size_t off = static_cast<size_t>(lo) * n * n;
+        KMB_CUDA(cudaMemcpyAsync(c->bcost.as<int32_t>() + off, costs + off,
+                                 static_cast<size_t>(cnt) * n * n * 4, cudaMemcpyHostToDevice, s));
+        kmb::WarpArgs ak = a;
+        ak.C = a.C + off;
+        ak.batch = cnt;
+        ak.row_to_col = a.row_to_col + static_cast<size_t>(lo) * n;
+        ak.u = a.u + static_cast<size_t>(lo) * n;
+        ak.v = a.v + static_cast<size_t>(lo) * n;
+        ak.total_cost = a.total_cost + lo;
+        ak.stats = a.stats + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
+        ak.status = a.status + lo;
+        KMB_CUDA(kmb::launch_warp_batch(ak, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), s, &grid));
+        KMB_CUDA(cudaEventRecord(c->aux_ev[k % kmb_context::kAux], s));
+        KMB_CUDA(cudaStreamWaitEvent(st, c->aux_ev[k % kmb_context::kAux], 0));
+      }
+    }
   }
   KMB_CUDA(cudaEventRecord(c->ev1, st));
   if (dr2c != row_to_col) { int r = copy_out(row_to_col, dr2c, nb * 4, st); if (r) return r; }
@@ -368,9 +416,9 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   // thread-block cluster up to n = 8192, the whole-GPU grid beyond (measured
   // crossovers)
   if (engine == 0) engine = (n <= 256 && time_budget_s <= 0.0) ? 4 : (n <= 8192 ? 5 : 1);
-  if (engine == 2 && n > kmb::batch_max_n()) engine = 1;
+  if ((engine == 2 || engine == 6) && n > kmb::batch_max_n()) engine = 1;
   if ((engine == 3 || engine == 4) && n > kmb::warp_max_n()) engine = 1;
-  if (engine >= 2 && engine <= 4) {
+  if ((engine >= 2 && engine <= 4) || engine == 6) {
     if (time_budget_s > 0.0)
       return fail(KMB_EINVAL, "kmb_solve_i32: the per-instance engines have no time budget; use engine 1");
     const int32_t* src = cost;

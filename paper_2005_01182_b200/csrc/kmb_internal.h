@@ -79,7 +79,8 @@ struct BatchArgs {
 };
 
 int batch_max_n();
-cudaError_t launch_batch(const BatchArgs& a, int sm_count, cudaStream_t st, int* grid_out);
+cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warps_per_sm,
+                         cudaStream_t st, int* grid_out);
 
 }  // namespace kmb
 

@@ -462,7 +462,7 @@ int kmb_solve_sharded_i32(kmb_context* c, const int32_t* slab, int32_t n, int64_
     stats->cost_bytes_read = 4ll * ncols * (res.rows_scanned + n);
     stats->seconds = ms * 1e-3;  // wall of the whole collective solve on this rank's stream
     stats->converged = 1;
-    stats->engine = 6;
+    stats->engine = 7;
   }
   return KMB_OK;
 }

@@ -87,7 +87,7 @@ def check_against(res, ref, c, dual_steps=None):
 def test_known_2x2(solver):  # test_hungarian.cpp:72-85
     c = np.array([[1, 3], [2, 1]], np.int32)
     for seed in (KMB_SEED_KM, KMB_SEED_BATCHED):
-        for engine in (1, 2, 3, 4, 5):
+        for engine in (1, 2, 3, 4, 5, 6):
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, seed)
             assert r.total_cost == 2
@@ -108,7 +108,7 @@ def test_known_constant(solver):  # :133-142: constant 6x6 cost 4 -> 24, one pha
     assert r.stats["dual_steps"] == 0
 
 
-@pytest.mark.parametrize("engine", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("engine", [1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("seed", [KMB_SEED_KM, KMB_SEED_BATCHED])
 def test_random_small_vs_reference(solver, engine, seed):
     rng = np.random.default_rng(100 + 10 * engine + seed)
@@ -169,23 +169,20 @@ def test_continue_bfs_same_duals(solver, cont):
 
 def test_matching_equals_mirror(solver):
     """The engines are deterministic: same forest, same claims -> the same
-    matching as the step-by-step CPU mirror of their schedule (restart: the CTA
-    engine; incremental epochs: the grid and warp engines)."""
+    matching as the step-by-step CPU mirror of their (incremental-epoch)
+    schedule, whatever the engine."""
     rng = np.random.default_rng(3)
     for t in range(20):
         n = int(rng.integers(2, 300))
         c = rng.integers(0, 20, size=(n, n)).astype(np.int32)
-        m = O.mirror_solve(c, 1)
         mi = O.mirror_solve_incr(c, 1)
-        engines = [1, 5] + ([2] if n <= 224 else []) + ([3, 4] if n <= 256 else [])
+        engines = [1, 5] + ([2, 3, 4, 6] if n <= 256 else [])
         for engine in engines:
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, KMB_SEED_BATCHED)
-            ref = m if engine == 2 else mi
-            np.testing.assert_array_equal(r.row_to_col, ref.row_to_col)
-            assert r.stats["phases"] == ref.phases
-            if engine != 2:
-                assert r.stats["rounds"] == ref.rounds
+            np.testing.assert_array_equal(r.row_to_col, mi.row_to_col)
+            assert r.stats["phases"] == mi.phases
+            assert r.stats["rounds"] == mi.rounds
     solver.set_option(OPT_ENGINE, 0)
 
 
@@ -194,7 +191,7 @@ def test_matching_equals_mirror(solver):
 def test_negative_cost_rejected(solver):
     c = np.ones((5, 5), np.int32)
     c[2, 3] = -1
-    for engine in (1, 2, 3, 4, 5):
+    for engine in (1, 2, 3, 4, 5, 6):
         solver.set_option(OPT_ENGINE, engine)
         with pytest.raises(KmbError, match="costs must be nonnegative"):
             solver.solve(c, KMB_SEED_BATCHED)
@@ -204,7 +201,7 @@ def test_negative_cost_rejected(solver):
 def test_out_of_device_range_rejected(solver):
     c = np.ones((5, 5), np.int32)
     c[0, 0] = 2**29
-    for engine in (1, 2, 3, 4, 5):
+    for engine in (1, 2, 3, 4, 5, 6):
         solver.set_option(OPT_ENGINE, engine)
         with pytest.raises(KmbError, match="device range"):
             solver.solve(c, KMB_SEED_BATCHED)
@@ -249,7 +246,7 @@ def test_config2(solver):
     check_against(r, ref, c)
 
 
-@pytest.mark.parametrize("engine", [2, 3, 4])
+@pytest.mark.parametrize("engine", [2, 3, 4, 6])
 def test_config3_subset(solver, engine):
     c = W.CONFIGS["c3"].make(batch=64)
     solver.set_option(OPT_ENGINE, engine)

@@ -8,7 +8,7 @@ from paper_2005_01182_b200.api import OPT_ENGINE
 
 s = Solver(0)
 rng = np.random.default_rng(0)
-for engine in (2, 3, 4):
+for engine in (2, 3, 4, 6):
     s.set_option(OPT_ENGINE, engine)
     bad = 0
     for t in range(60):
@@ -29,7 +29,7 @@ dc = torch.from_numpy(c).cuda()
 r2c = torch.empty((b, n), dtype=torch.int32, device="cuda"); u = torch.empty((b, n), dtype=torch.int64, device="cuda")
 v = torch.empty_like(u); tot = torch.empty(b, dtype=torch.int64, device="cuda")
 ref_tot = None
-for engine in (2, 3, 4):
+for engine in (2, 3, 4, 6):
     s.set_option(OPT_ENGINE, engine)
     ts = []
     for it in range(5):
