@@ -26,6 +26,9 @@ struct Ctrl {
   int32_t stop;                    // time budget expired
   int32_t free_rows;               // unmatched rows when the engine stopped
   int32_t matched;                 // rows matched so far
+  int32_t rcnt[3];                 // row appends per barrier interval (k % 3)
+  int32_t fcnt[3];                 // free-column appends per barrier interval
+  int32_t pad2_[2];
   int64_t phases;
   int64_t dual_steps;
   int64_t rows_scanned;

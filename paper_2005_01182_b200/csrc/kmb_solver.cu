@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   }
   __syncthreads();
   int64_t dual_steps = 0, rows_scanned = 0;
-  // stage clock (leader only): 0 relax+local min, 1 B1, 2 absorb, 3 B2, 4 epoch end, 5 B3
+  // stage clock (leader only): 0 relax + absorb + local min, 1 B1, 2 dual-step absorb,
+  // 3 B2 (dual steps only), 4 epoch end, 5 B3
   long long prof[6] = {0, 0, 0, 0, 0, 0};
   long long rounds_total = 0;
   unsigned long long tprev = leader ? globaltimer_ns() : 0ull;
@@ -214,9 +215,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   unsigned long long deadline = a.deadline_ns;
   if (deadline >> 63) deadline = globaltimer_ns() + (deadline & ~(1ull << 63));  // relative budget
 
+  // Shared append counters are triple-buffered by barrier index: appends made
+  // between barriers k-1 and k go to cnt[k % 3], every CTA reads it right after
+  // barrier k, and the leader clears cnt[(k+2) % 3] after barrier k (last read
+  // after barrier k-1, next used after barrier k+1), so a fast CTA's appends
+  // never race a slow CTA's read.
+  int kb = 0;
+  auto gsync = [&]() {
+    bar.sync();
+    ++kb;
+    if (leader) {
+      ctrl->rcnt[(kb + 2) % 3] = 0;
+      ctrl->fcnt[(kb + 2) % 3] = 0;
+    }
+  };
   int64_t D = 0;
   int p = 0, epoch = 0, head = 0, tail = a.n;  // rows list[p][0, tail) are reached
-  bool first_round_of_epoch = true, fatal = false, stopped = false;
+  int nfound = 0;                              // free columns absorbed this epoch
+  bool fatal = false, stopped = false;
   for (;;) {
     const int32_t* list = a.list_row[p];
     const int64_t* listw = a.list_w[p];
@@ -227,7 +243,56 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       for (int c = tid; c < W; c += kThreads)
         if (c0 + c < a.n) vloc[c] = key_val(skey[c]);
     ++rounds_total;
-    // local min of unreached slack'
+    // absorb the slab's tight columns at the current D (hungarian.cpp:186-199):
+    // tightness is a per-column test, no global information needed
+    auto absorb_at = [&](int64_t Dn) {
+      int* rc = &ctrl->rcnt[(kb + 1) % 3];
+      int* fc = &ctrl->fcnt[(kb + 1) % 3];
+      for (int cb = 0; cb < W; cb += kThreads) {
+        const int c = cb + tid;
+        bool newrow = false, newfree = false;
+        int32_t i2 = -1, col = c0 + c;
+        int64_t w2 = 0;
+        if (c < W && !rch[c] && key_val(skey[c]) - vloc[c] == Dn) {
+          rch[c] = 1;
+          dcol[c] = Dn;
+          const int32_t par = key_row(skey[c]);
+          a.tree_par[col] = par;
+          const int32_t root = ldcg(a.root_row + par);
+          i2 = ldcg(a.match_col + col);
+          if (i2 < 0) {
+            newfree = true;
+            atomicMin(reinterpret_cast<unsigned long long*>(a.claim + root), claim_key(epoch, col));
+          } else {
+            newrow = true;
+            w2 = ldcg(a.u + i2) - Dn;
+            a.root_row[i2] = root;
+          }
+        }
+        // warp-aggregated appends
+        const unsigned rowmask = __ballot_sync(0xffffffffu, newrow);
+        if (rowmask) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(rc, __popc(rowmask));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (newrow) {
+            const int pos = tail + base + __popc(rowmask & ((1u << lane) - 1));
+            a.list_row[p][pos] = i2;
+            a.list_w[p][pos] = w2;
+          }
+        }
+        const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
+        if (fmask) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(fc, __popc(fmask));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (newfree) a.found[nfound + base + __popc(fmask & ((1u << lane) - 1))] = col;
+        }
+      }
+    };
+    absorb_at(D);
+    __syncthreads();
+    // min slack' of the columns still unreached: only used if no CTA progressed
     int64_t lm = KMB_I64_INF;
     for (int c = tid; c < W; c += kThreads)
       if (!rch[c]) {
@@ -243,81 +308,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       if (lane == 0) a.partial[blockIdx.x] = x;
     }
     KMB_STAGE(0);
-    bar.sync();  // ---------------------------------------------- B1
+    gsync();  // ---------------------------------------------------- B1
     KMB_STAGE(1);
-    if (first_round_of_epoch && leader) {  // recycle the previous epoch's counters
-      ctrl->tail[p ^ 1] = 0;
-      ctrl->nfound[p ^ 1] = 0;
-    }
-    first_round_of_epoch = false;
-    if (wid == 0) {
-      int64_t x = KMB_I64_INF;
-      for (int b = lane; b < G; b += 32) {
-        const int64_t y = ldcg(a.partial + b);
-        x = y < x ? y : x;
+    int added = ldcg(&ctrl->rcnt[kb % 3]);
+    int fadded = ldcg(&ctrl->fcnt[kb % 3]);
+    if (added == 0 && fadded == 0) {
+      // no tight column anywhere and no pending row: dual step (:201-215)
+      if (wid == 0) {
+        int64_t x = KMB_I64_INF;
+        for (int b = lane; b < G; b += 32) {
+          const int64_t y = ldcg(a.partial + b);
+          x = y < x ? y : x;
+        }
+        x = warp_min_i64(x);
+        if (lane == 0) sm.m = x;
       }
-      x = warp_min_i64(x);
-      if (lane == 0) sm.m = x;
-    }
-    __syncthreads();
-    const int64_t m = sm.m;
-    if (m > D) {
+      __syncthreads();
+      const int64_t m = sm.m;
       if (m == KMB_I64_INF) {  // no unreached column: cannot happen on valid input
         if (leader) ctrl->status = -2;
         fatal = true;
         break;
       }
-      D = m;  // dual step: no tight unreached column, no pending row (:201-215)
+      D = m;
       ++dual_steps;
+      absorb_at(D);
+      KMB_STAGE(2);
+      gsync();  // ------------------------------------------------ B2 (dual steps only)
+      KMB_STAGE(3);
+      added = ldcg(&ctrl->rcnt[kb % 3]);
+      fadded = ldcg(&ctrl->fcnt[kb % 3]);
     }
-    // absorb zero-slack columns of the slab (hungarian.cpp:186-199)
-    for (int cb = 0; cb < W; cb += kThreads) {
-      const int c = cb + tid;
-      bool newrow = false, newfree = false;
-      int32_t i2 = -1, col = c0 + c;
-      int64_t w2 = 0;
-      if (c < W && !rch[c] && key_val(skey[c]) - vloc[c] == D) {
-        rch[c] = 1;
-        dcol[c] = D;
-        const int32_t par = key_row(skey[c]);
-        a.tree_par[col] = par;
-        const int32_t root = ldcg(a.root_row + par);
-        i2 = ldcg(a.match_col + col);
-        if (i2 < 0) {
-          newfree = true;
-          atomicMin(reinterpret_cast<unsigned long long*>(a.claim + root), claim_key(epoch, col));
-        } else {
-          newrow = true;
-          w2 = ldcg(a.u + i2) - D;
-          a.root_row[i2] = root;
-        }
-      }
-      // warp-aggregated appends
-      const unsigned rowmask = __ballot_sync(0xffffffffu, newrow);
-      if (rowmask) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&ctrl->tail[p], __popc(rowmask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (newrow) {
-          const int pos = base + __popc(rowmask & ((1u << lane) - 1));
-          a.list_row[p][pos] = i2;
-          a.list_w[p][pos] = w2;
-        }
-      }
-      const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
-      if (fmask) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&ctrl->nfound[p], __popc(fmask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (newfree) a.found[base + __popc(fmask & ((1u << lane) - 1))] = col;
-      }
-    }
-    KMB_STAGE(2);
-    bar.sync();  // ---------------------------------------------- B2
-    KMB_STAGE(3);
     head = tail;
-    tail = ldcg(&ctrl->tail[p]);
-    const int nfound = ldcg(&ctrl->nfound[p]);
+    tail += added;
+    nfound += fadded;
     if (nfound == 0) continue;
 
     // ---- epoch end: augment and dissolve the trees that reached a free column ----
@@ -338,13 +362,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       }
     }
     // rows: finalise dissolved ones (u = w + D), carry the survivors over
+    int* sc = &ctrl->rcnt[(kb + 1) % 3];
     for (int r = gtid; r < tail; r += gthreads) {
       const int32_t i = ldcg(list + r);
       const int64_t w = ldcg(listw + r);
       if (claimed_in(ldcg(a.claim + ldcg(a.root_row + i)), epoch)) {
         a.u[i] = w + D;
       } else {
-        const int pos = atomicAdd(&ctrl->tail[p ^ 1], 1);
+        const int pos = atomicAdd(sc, 1);
         a.list_row[p ^ 1][pos] = i;
         a.list_w[p ^ 1][pos] = w;
       }
@@ -372,13 +397,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       if (deadline && globaltimer_ns() > deadline) ctrl->stop = 1;
     }
     KMB_STAGE(4);
-    bar.sync();  // ------------------------------------------------ B3
+    gsync();  // ---------------------------------------------------- B3
     KMB_STAGE(5);
     p ^= 1;
     ++epoch;
     head = 0;
-    tail = ldcg(&ctrl->tail[p]);
-    first_round_of_epoch = true;
+    tail = ldcg(&ctrl->rcnt[kb % 3]);  // survivors
+    nfound = 0;
     if (ldcg(&ctrl->matched) == a.n) break;
     if (ldcg(&ctrl->stop) != 0) {
       stopped = true;
