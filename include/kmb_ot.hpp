@@ -115,7 +115,16 @@ inline SolveResult solve_batched_km_b200(const OTInstance& inst, const BatchedKM
   const auto t0 = std::chrono::steady_clock::now();
   const int32_t n = inst.n;
   QuantizedCosts q = quantize_costs(inst.cost, config.B);  // the reference's own, :33-53
-  const std::vector<int32_t> c = kmb_detail::narrow(q.chat, "solve_batched_km");
+  // B a multiple of N (e.g. the lossless B = N*n): chat = k*C exactly and the
+  // search is scale-equivariant, so solve C and scale the duals by k when chat
+  // itself would leave the device range.
+  int64_t k = 1;
+  if (q.N > 0 && config.B % q.N == 0) {
+    int64_t mx = 0;
+    for (int64_t x : q.chat) mx = x > mx ? x : mx;
+    if (mx >= (int64_t{1} << 29)) k = config.B / q.N;
+  }
+  const std::vector<int32_t> c = kmb_detail::narrow(k > 1 ? inst.cost : q.chat, "solve_batched_km");
   std::vector<int32_t> r2c(n, -1);
   std::vector<int64_t> u(n), v(n);
   int64_t total = 0;
@@ -128,6 +137,10 @@ inline SolveResult solve_batched_km_b200(const OTInstance& inst, const BatchedKM
   if (duals) {
     duals->u = u;
     duals->v = v;
+    if (k > 1) {
+      for (int64_t& x : duals->u) x *= k;
+      for (int64_t& x : duals->v) x *= k;
+    }
   }
   if (quantized) *quantized = q;
   // iterations = phases + dual adjustments (hungarian.cpp:375); the dual-step

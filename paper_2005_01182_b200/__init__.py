@@ -10,7 +10,9 @@ Layers:
   workloads.py                seeded inputs for the BASELINE configs
 """
 from .api import (KMB_SEED_BATCHED, KMB_SEED_KM, KmbError, KmbUnavailable, Result, Solver,
-                  default_solver, load_library, quantize_costs, solve_batched_km, solve_km)
+                  calibrate_batch_level, default_solver, load_library, quantize_costs,
+                  solve_batched_km, solve_km)
 
 __all__ = ["KMB_SEED_BATCHED", "KMB_SEED_KM", "KmbError", "KmbUnavailable", "Result", "Solver",
-           "default_solver", "load_library", "quantize_costs", "solve_batched_km", "solve_km"]
+           "calibrate_batch_level", "default_solver", "load_library", "quantize_costs",
+           "solve_batched_km", "solve_km"]

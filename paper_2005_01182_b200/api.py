@@ -290,10 +290,19 @@ def solve_batched_km(cost, B: int | None = None, supplies=None, demands=None,
     if B is None:
         B = max(int(c64.max()), 1)
     chat, N, lossless = quantize_costs(c64, int(B))
-    if chat.size and chat.max() >= 2**29:
-        _range_error("solve_batched_km")
     s = solver or default_solver()
-    r = s.solve(chat.astype(np.int32), KMB_SEED_BATCHED, time_budget_s)
+    scale = int(B) // N if int(B) % N == 0 and N > 0 else 0
+    if scale > 1 and chat.size and chat.max() >= 2**29 and c64.max() < 2**29:
+        # B a multiple of N (e.g. the lossless B = N*n): chat = k*C exactly.  The
+        # search is scale-equivariant (every slack, delta and comparison scales by
+        # k > 0), so the reference's duals on chat are k times the duals on C.
+        r = s.solve(c64.astype(np.int32), KMB_SEED_BATCHED, time_budget_s)
+        r.u = r.u * scale
+        r.v = r.v * scale
+    else:
+        if chat.size and chat.max() >= 2**29:
+            _range_error("solve_batched_km")
+        r = s.solve(chat.astype(np.int32), KMB_SEED_BATCHED, time_budget_s)
     r.exact = bool(lossless and r.converged)
     rows = np.arange(c64.shape[0])
     ok = r.row_to_col >= 0
@@ -301,6 +310,24 @@ def solve_batched_km(cost, B: int | None = None, supplies=None, demands=None,
     if return_quantized:
         return r, (chat, int(B), N, lossless)
     return r
+
+
+def calibrate_batch_level(cost, exact: float, target_ratio: float = 1.1,
+                          solver: Solver | None = None) -> int:
+    """Smallest power-of-two quantization level B whose batched-KM objective is
+    within ``target_ratio`` of ``exact``; capped at the lossless B = N*n
+    (the reference's calibrate_batch_level, bench.cpp:296-308).  This is the
+    paper's lossy 1.1-approximate mode (Table 3)."""
+    c = np.asarray(cost, dtype=np.int64)
+    cap = max(int(c.max()) if c.size else 0, 1) * c.shape[0]
+    B = 1
+    while True:
+        if B >= cap:
+            return cap
+        r = solve_batched_km(c, B, solver=solver)
+        if r.objective <= target_ratio * exact * (1 + 1e-12):
+            return B
+        B *= 2
 
 
 def _range_error(who: str):

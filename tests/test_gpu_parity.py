@@ -303,3 +303,59 @@ def test_large_config_golden(solver, key):
         blk = cc[lo:lo + 2048] - r.u[lo:lo + 2048, None] - r.v[None, :]
         assert blk.min() >= 0
     assert (cc[np.arange(c.shape[0]), r.row_to_col] == r.u + r.v[r.row_to_col]).all()
+
+
+# ---- reference-shaped API: quantization (hungarian.cpp:33-53), lossy mode ------
+
+def test_api_batched_km_quantization_matches_reference():
+    """solve_batched_km(cost, B) vs ot::solve_batched_km(inst, {B}) for lossy B,
+    B = N (identity) and B = N*n (lossless scaling, test_hungarian.cpp:144-156):
+    duals on chat and the chat-optimum bit-exact, exact = lossless
+    (hungarian.cpp:374-376).  With lossy B, chat has many tied optima whose TRUE
+    cost differs, so the true objective is held to the reference's bound instead
+    (test_hungarian.cpp:158-172: OPT <= obj <= OPT + n*N/B)."""
+    from paper_2005_01182_b200 import solve_batched_km
+    rng = np.random.default_rng(19)
+    for t in range(40):
+        n = int(rng.integers(2, 50))
+        c = rng.integers(0, int(rng.choice([50, 5000, 100000])), size=(n, n))
+        N = max(int(c.max()), 1)
+        opt = O.ref_solve_km(c).objective
+        for B in (1, 2, 5, 37, 64, N, N * n):
+            ref = O.ref_solve_batched_km(c, B=B, want_chat=True)
+            r, (chat, _, _, lossless) = solve_batched_km(c, B, return_quantized=True)
+            np.testing.assert_array_equal(chat, ref.chat)
+            assert r.exact == ref.exact == lossless
+            np.testing.assert_array_equal(r.u, ref.u)
+            np.testing.assert_array_equal(r.v, ref.v)
+            rows = np.arange(n)
+            assert chat[rows, r.row_to_col].sum() == ref.chat[rows, ref.row_to_col].sum()
+            assert opt <= r.objective <= opt + n * N / B
+            if lossless:
+                assert r.objective == ref.objective
+
+
+def test_api_solve_km_and_errors():
+    from paper_2005_01182_b200 import solve_batched_km, solve_km
+    c = np.array([[1, 3], [2, 1]])
+    r = solve_km(c)
+    assert r.objective == 2.0 and r.row_to_col.tolist() == [0, 1] and r.iterations == 2
+    with pytest.raises(ValueError, match="requires a unit-capacity square instance"):
+        solve_km(c, supplies=[2, 1], demands=[1, 2])
+    with pytest.raises(ValueError, match="costs must be nonnegative"):
+        solve_batched_km(np.array([[1, -1], [0, 0]]))
+    with pytest.raises(ValueError, match="B must be positive"):
+        solve_batched_km(c, 0)
+
+
+def test_calibrate_batch_level_matches_reference_rule():
+    """The paper's lossy 1.1-approximate mode: the same B as the reference's
+    calibrate_batch_level (bench.cpp:296-308) computed with the reference solver."""
+    from paper_2005_01182_b200 import calibrate_batch_level
+    c = W.CONFIGS["c1"].make().astype(np.int64)
+    exact = O.ref_solve_km(c).objective
+    cap = max(int(c.max()), 1) * c.shape[0]
+    B = 1
+    while B < cap and O.ref_solve_batched_km(c, B=B).objective > 1.1 * exact * (1 + 1e-12):
+        B *= 2
+    assert calibrate_batch_level(c, exact, 1.1) == min(B, cap)
