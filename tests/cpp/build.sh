@@ -18,3 +18,12 @@ g++ -O2 -std=c++20 -I"$REF/include" -I"$ROOT/include" "$HERE/test_drop_in.cpp" \
   -L"$ROOT/oracle/_ref" -lotref -L"$ROOT/paper_2005_01182_b200" -lkmb \
   -Wl,-rpath,'$ORIGIN/../../../oracle/_ref' -Wl,-rpath,'$ORIGIN/../../../paper_2005_01182_b200' \
   -o "$HERE/build/test_drop_in"
+# the reference harness (run_suite, make_solver, calibration rule) with the B200
+# solvers registered as SolverSpecs: the reference library is compiled from its
+# own sources for this test
+g++ -O2 -std=c++20 -I"$REF/include" -I"$ROOT/include" "$HERE/test_harness.cpp" \
+  "$REF/src/bench.cpp" "$REF/src/core.cpp" "$REF/src/hungarian.cpp" "$REF/src/netsimplex.cpp" \
+  "$REF/src/auction.cpp" "$REF/src/scaling.cpp" "$REF/src/datasets.cpp" "$REF/src/io.cpp" \
+  -L"$ROOT/paper_2005_01182_b200" -lkmb \
+  -Wl,-rpath,'$ORIGIN/../../../paper_2005_01182_b200' -o "$HERE/build/test_harness"
+

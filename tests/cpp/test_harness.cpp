@@ -1,0 +1,117 @@
+// C++ harness integration: the B200 solvers
+// registered as SolverSpec plugins (bench.hpp:24-29) and driven by the
+// UNMODIFIED reference harness — run_suite (bench.cpp:67-125: exact objective
+// by network simplex, median-of-repeats timing) and calibrate_all's batch-level
+// rule — next to the reference's own "km" / "batched_km" specs
+// (make_solver, bench.cpp:404-422).  Built by tests/cpp/build.sh against the
+// reference sources, run on the GPU by tests/test_cpp_drop_in.py.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "ot/bench.hpp"
+#include "ot/core.hpp"
+#include "ot/datasets.hpp"
+#include "ot/hungarian.hpp"
+#include "kmb_ot.hpp"
+
+using namespace ot;
+
+static int g_fail = 0;
+#define CHECK(cond)                                                                        \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      ++g_fail;                                                                            \
+      std::fprintf(stderr, "%s:%d: CHECK(%s) failed\n", __FILE__, __LINE__, #cond);        \
+    }                                                                                      \
+  } while (0)
+
+// The plugin registrations a maintainer adds next to make_solver's
+static SolverSpec km_b200_spec() {
+  SolverSpec s;
+  s.name = "km_b200";
+  s.unit_only = true;
+  s.run = [](const OTInstance& inst, double budget) {
+    return solve_km_b200(inst, nullptr, nullptr, budget);
+  };
+  return s;
+}
+
+static SolverSpec batched_km_b200_spec(int64_t B) {
+  SolverSpec s;
+  s.name = "batched_km_b200";
+  s.params = "B=" + std::to_string(B);
+  s.unit_only = true;
+  s.run = [B](const OTInstance& inst, double budget) {
+    BatchedKMConfig cfg;
+    cfg.B = B;
+    cfg.time_budget_s = budget;
+    return solve_batched_km_b200(inst, cfg);
+  };
+  return s;
+}
+
+int main() {
+  std::vector<OTInstance> insts;
+  insts.push_back(gen_circle_square(100));  // cs100, acceptance criterion 1: 732033
+  std::mt19937 rng(7);
+  for (int t = 0; t < 3; ++t) {
+    OTInstance inst;
+    inst.n = inst.m = 40 + 20 * t;
+    inst.name = "rand" + std::to_string(t);
+    std::uniform_int_distribution<int64_t> d(0, 100000);
+    inst.cost.resize(static_cast<size_t>(inst.n) * inst.n);
+    for (auto& c : inst.cost) c = d(rng);
+    inst.supplies.assign(inst.n, 1);
+    inst.demands.assign(inst.n, 1);
+    insts.push_back(inst);
+  }
+  CalibrationEntry lossless;
+  lossless.B = 1;  // overwritten per instance below; run_suite takes one roster
+  BenchConfig cfg;
+  cfg.repeats = 2;
+  cfg.timeout_s = 60.0;
+  for (const OTInstance& inst : insts) {
+    const int64_t B = std::max<int64_t>(inst.max_cost(), 1);  // lossless (identity)
+    CalibrationEntry ce;
+    ce.B = B;
+    const std::vector<SolverSpec> roster = {make_solver("km"), km_b200_spec(),
+                                            make_solver("batched_km", &ce),
+                                            batched_km_b200_spec(B)};
+    const std::vector<BenchRecord> recs = run_suite({inst}, roster, cfg);
+    CHECK(recs.size() == 4);
+    for (const BenchRecord& r : recs) {
+      std::printf("%-8s %-16s %-10s obj=%.0f exact=%.0f ratio=%.6f t=%.4fs conv=%d\n",
+                  r.instance.c_str(), r.solver.c_str(), r.params.c_str(), r.objective,
+                  r.exact_objective, r.ratio, r.wall_seconds, r.converged ? 1 : 0);
+      CHECK(r.applicable && r.converged);
+      CHECK(r.objective == r.exact_objective);
+    }
+    if (inst.name == "cs100") CHECK(recs[1].objective == 732033.0);
+  }
+  // the paper's lossy mode through the harness: calibrated B (bench.cpp:296-308)
+  // gives the same quantization level for the reference and the B200 solver
+  {
+    const OTInstance& inst = insts[1];
+    const double exact = solve_km(inst).objective;
+    int64_t Bref = 1, Bgpu = 1;
+    const int64_t cap = std::max<int64_t>(1, inst.max_cost()) * inst.n;
+    for (int64_t B = 1;; B *= 2) {
+      if (B >= cap) { Bref = cap; break; }
+      BatchedKMConfig c; c.B = B;
+      if (solve_batched_km(inst, c).objective <= 1.1 * exact * (1 + 1e-12)) { Bref = B; break; }
+    }
+    for (int64_t B = 1;; B *= 2) {
+      if (B >= cap) { Bgpu = cap; break; }
+      BatchedKMConfig c; c.B = B;
+      if (solve_batched_km_b200(inst, c).objective <= 1.1 * exact * (1 + 1e-12)) { Bgpu = B; break; }
+    }
+    std::printf("calibrated B: reference %lld, b200 %lld\n", static_cast<long long>(Bref),
+                static_cast<long long>(Bgpu));
+    CHECK(Bref == Bgpu);
+  }
+  std::printf("harness: %d failed\n", g_fail);
+  return g_fail ? 1 : 0;
+}

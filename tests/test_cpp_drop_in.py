@@ -16,3 +16,14 @@ def test_cpp_drop_in():
     out = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failed" in out.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_reference_harness():
+    """The B200 solvers as SolverSpec plugins inside the reference's run_suite."""
+    b = os.path.join(HERE, "cpp", "build", "test_harness")
+    if not os.path.exists(b):
+        pytest.fail(f"{b} missing: run tests/cpp/build.sh where /root/reference exists")
+    out = subprocess.run([b], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "harness: 0 failed" in out.stdout
