@@ -97,15 +97,16 @@ struct GridBarrier {
     return GridBarrier{counter, 0ull, G};
   }
 
+  // bar.sync makes the CTA's writes visible to thread 0, whose release
+  // reduction (cumulative) publishes them at gpu scope; the acquire poll orders
+  // every later read after the other CTAs' releases.  No full fences.
   __device__ __forceinline__ void sync() {
     __syncthreads();
     if (threadIdx.x == 0) {
       target += G;
-      __threadfence();
-      atomicAdd(counter, 1ull);
+      asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(counter) : "memory");
       while (ld_acquire_u64(counter) < target) {
       }
-      __threadfence();
     }
     __syncthreads();
   }
