@@ -8,11 +8,11 @@
 // holds no free column; the step over the full closure with delta = min slack.
 // How it gets there differs from the reference:
 //
-//  * Lazy duals.  Within a phase D is the accumulated dual shift; row i reached
+//  * Lazy duals.  D is the dual shift accumulated by the search; row i reached
 //    at shift Dr stores w_i = u_i - Dr, so a column's slack' = min_i (C_ij - w_i)
 //    - v_j never changes under a dual step and column j is tight iff slack' == D.
 //    A dual step is therefore D = min unreached slack' — no O(n) update — and
-//    the duals are finalised once per phase (u_i = w_i + D, v_j -= D - Dc_j).
+//    the duals are written back when a tree dissolves (u_i = w_i + D, v_j -= D - Dc_j).
 //  * Relax = reduced-cost scan (hungarian.cpp:164-172).  CTA b owns columns
 //    [b*W, b*W+W) of every row; each round it streams the W-wide slab of every
 //    newly reached row with 128-bit no-allocate loads and folds them into
@@ -29,10 +29,12 @@
 //    free rows; every tree that reached a free column flips the path of its
 //    smallest such column.  Paths of distinct trees are vertex-disjoint.
 //
-// One round = relax | barrier | min + absorb | barrier.  A phase ends after
-// the round that absorbs a free column (or, with continue_bfs, when the tight
-// closure at the current D is exhausted), then finalises duals, flips paths and
-// lists the next phase's free rows behind one more barrier.
+// One round = relax + local absorb at D | barrier (+ dual step, absorb, barrier
+// when nothing anywhere became tight).  An epoch ends after the round that
+// absorbs a free column: claimed trees are dissolved and augmented, survivors
+// stay reached (incremental epochs).  The barrier is a template:
+// GridBarrier (software, any G <= #SMs, cooperative launch) or ClusterBarrier
+// (one thread-block cluster of G <= 16 CTAs, hardware barrier.cluster).
 #include <cuda_runtime.h>
 
 #include <cstdint>
