@@ -68,8 +68,11 @@ enum kmb_option {
                                3 warp/SMEM, 4 warp/L2 (2,3,4,6: n <= 256),
                                5 cluster (grid engine on one <=16-CTA cluster);
                                stats->engine 7 = column-sharded              */
-  KMB_OPT_WARPS_PER_SM = 4  /* warp engine: resident instances per SM (0 = max);
+  KMB_OPT_WARPS_PER_SM = 4, /* warp engine: resident instances per SM (0 = max);
                                bounds the L2 working set of streamed matrices   */
+  KMB_OPT_U16 = 5           /* warp/L2 engine (n in 65..256): stream 16-bit
+                               offsets from the row minima, exact (rows with an
+                               offset >= 65535 fall back to int32); 0 = default */
 };
 
 typedef struct kmb_stats {
@@ -133,6 +136,11 @@ int kmb_solve_sharded_i32(kmb_context* ctx, const int32_t* slab, int32_t n, int6
  * `iters` passes; bytes counted = 4*n*n per pass. */
 int kmb_bench_scan(kmb_context* ctx, const int32_t* cost, int32_t n, int64_t ld, int32_t iters,
                    double* seconds_per_pass, double* gbytes_per_s);
+
+/* Diagnostics: per-instance counters of the last batch solve, KMB_ISTATS = 11
+ * int64 per instance (epochs, dual steps, rows scanned, rounds, SM cycles,
+ * cycles in relax / min / absorb / epoch end, %globaltimer start / end). */
+int kmb_last_instance_stats(kmb_context* ctx, int64_t* out, int64_t capacity, int64_t* count);
 
 /* Thread-local message of the last failing call on this thread. */
 const char* kmb_last_error(void);

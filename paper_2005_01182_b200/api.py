@@ -23,13 +23,13 @@ from . import _build
 
 KMB_SEED_KM = 0
 KMB_SEED_BATCHED = 1
-OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM = 1, 2, 3, 4
+OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_U16 = 1, 2, 3, 4, 5
 
 # every symbol include/kmb.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
                "kmb_solve_batch_i32", "kmb_nccl_unique_id", "kmb_shard_init_nccl",
                "kmb_shard_init_callbacks", "kmb_solve_sharded_i32", "kmb_bench_scan",
-               "kmb_last_error", "kmb_abi_version")
+               "kmb_last_instance_stats", "kmb_last_error", "kmb_abi_version")
 
 
 class KmbUnavailable(RuntimeError):
@@ -163,6 +163,14 @@ class Solver:
                                            C.byref(st) if st is not None else None)
         self._check(rc)
         return st
+
+    def last_instance_stats(self, batch: int):
+        """Per-instance counters of the last batch solve: (batch, 11) int64."""
+        out = np.zeros(batch * 11, np.int64)
+        cnt = C.c_int64()
+        self._check(self._lib.kmb_last_instance_stats(self._h, C.c_void_p(out.ctypes.data), out.size,
+                                                      C.byref(cnt)))
+        return out.reshape(batch, 11)
 
     def bench_scan(self, cost, n: int, ld: int, iters: int = 5) -> tuple[float, float]:
         """Full-frontier scan microbenchmark: (seconds per pass, GB/s)."""

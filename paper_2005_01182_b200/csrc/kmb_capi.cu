@@ -73,13 +73,14 @@ struct kmb_context {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t max_ctas = 0;
   int64_t warps_per_sm = 0;  // warp engine residency bound (0 = occupancy limit)
+  int64_t u16 = 0;           // warp/L2 engine: 16-bit row-offset packing (opt-in)
   int continue_bfs = 0;
   int engine = 0;
   // grid-engine workspace
   DevBuf cost, u, v, mrow, mcol, tpar, root, claim, lrow0, lrow1, lw0, lw1, found, partial,
       ctrl, obj;
   // batch workspace
-  DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus;
+  DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus, b16, brmin, bimin, bimax;
   // column-sharded solve: the collective (NCCL or caller callbacks)
   std::unique_ptr<kmb::Exchange> exchange;
   // chunked host-input pipeline of the batch engines
@@ -129,7 +130,7 @@ void kmb_destroy(kmb_context* c) {
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
-                    &c->obj, &c->bcost, &c->bpad, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
+                    &c->obj, &c->bcost, &c->bpad, &c->b16, &c->brmin, &c->bimin, &c->bimax, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
                     &c->bstatus})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -153,6 +154,7 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
     case KMB_OPT_MAX_CTAS: c->max_ctas = value; return KMB_OK;
     case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_WARPS_PER_SM: c->warps_per_sm = value; return KMB_OK;
+    case KMB_OPT_U16: c->u16 = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_ENGINE:
       if (value < 0 || value > 6) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..6");
       c->engine = static_cast<int>(value);
@@ -242,8 +244,29 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.total_cost = dtot;
     a.stats = c->bstat.as<int64_t>();
     a.status = c->bstatus.as<int32_t>();
+    // U16 mode (warp/L2 engine, 4 or 8 columns per lane): a packing pass writes
+    // 16-bit offsets from the row minima, halving the bytes every relax streams
+    const bool u16 = engine == 4 && c->u16 && (np == 128 || np == 256);
+    if (u16) {
+      const size_t rows_all = static_cast<size_t>(batch) * n;
+      KMB_CUDA(c->b16.ensure(rows_all * np * 2));
+      KMB_CUDA(c->brmin.ensure(rows_all * 4));
+      KMB_CUDA(c->bimin.ensure(static_cast<size_t>(batch) * 4));
+      KMB_CUDA(c->bimax.ensure(static_cast<size_t>(batch) * 4));
+      a.C16 = c->b16.as<uint16_t>();
+      a.rmin = c->brmin.as<int32_t>();
+      a.imin = c->bimin.as<int32_t>();
+      a.imax = c->bimax.as<int32_t>();
+    }
+    auto pack = [&](const kmb::WarpArgs& ak, cudaStream_t s) -> cudaError_t {
+      if (!u16) return cudaSuccess;
+      return kmb::launch_pack16(ak, c->sm_count, const_cast<uint16_t*>(ak.C16),
+                                const_cast<int32_t*>(ak.rmin), const_cast<int32_t*>(ak.imin),
+                                const_cast<int32_t*>(ak.imax), s);
+    };
     KMB_CUDA(cudaEventRecord(c->ev0, st));
     if (!pipelined) {
+      KMB_CUDA(pack(a, st));
       KMB_CUDA(kmb::launch_warp_batch(a, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), st, &grid));
     } else {
       if (!c->aux[0]) {
@@ -271,6 +294,13 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
         ak.total_cost = a.total_cost + lo;
         ak.stats = a.stats + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
         ak.status = a.status + lo;
+        if (u16) {
+          ak.C16 = a.C16 + static_cast<size_t>(lo) * n * np;
+          ak.rmin = a.rmin + static_cast<size_t>(lo) * n;
+          ak.imin = a.imin + lo;
+          ak.imax = a.imax + lo;
+        }
+        KMB_CUDA(pack(ak, s));
         KMB_CUDA(kmb::launch_warp_batch(ak, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), s, &grid));
         KMB_CUDA(cudaEventRecord(c->aux_ev[k % kmb_context::kAux], s));
         KMB_CUDA(cudaStreamWaitEvent(st, c->aux_ev[k % kmb_context::kAux], 0));
@@ -469,6 +499,16 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
     stats->rounds = h.rounds;
     for (int k = 0; k < 6; ++k) stats->stage_ns[k] = h.stage_ns[k];
   }
+  return KMB_OK;
+}
+
+int kmb_last_instance_stats(kmb_context* c, int64_t* out, int64_t capacity, int64_t* count) {
+  if (!c || !out || !count) return fail(KMB_EINVAL, "kmb_last_instance_stats: bad arguments");
+  KMB_CUDA(cudaSetDevice(c->device));
+  const int64_t have = static_cast<int64_t>(c->bstat.bytes / 8);
+  const int64_t k = capacity < have ? capacity : have;
+  *count = have / kmb::KMB_ISTATS;
+  if (k > 0) KMB_CUDA(cudaMemcpy(out, c->bstat.p, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost));
   return KMB_OK;
 }
 

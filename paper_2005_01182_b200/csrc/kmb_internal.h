@@ -13,8 +13,9 @@
 namespace kmb {
 
 // per-instance stats of the batch engines: phases/epochs, dual steps, rows
-// scanned, rounds, SM cycles, then cycles in relax / min / absorb / epoch end
-constexpr int KMB_ISTATS = 9;
+// scanned, rounds, SM cycles, cycles in relax / min / absorb / epoch end, then
+// %globaltimer at the instance's start and end (ns)
+constexpr int KMB_ISTATS = 11;
 
 // Device control block of one single-instance solve.  Counters that are
 // recycled between phases are double-buffered by phase parity (see k_solve).
@@ -102,8 +103,16 @@ struct WarpArgs {
   int64_t* total_cost;   // batch
   int64_t* stats;        // batch x KMB_ISTATS (may be null)
   int32_t* status;       // batch
+  // U16 mode (optional, from launch_pack16): 16-bit offsets from the row
+  // minimum, row minima with the "wide" flag in bit 31, per-instance min/max
+  const uint16_t* C16;
+  const int32_t* rmin;
+  const int32_t* imin;
+  const int32_t* imax;
 };
 int warp_max_n();
+cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_t* rmin,
+                          int32_t* imin, int32_t* imax, cudaStream_t st);
 int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)
 cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int warps_per_sm,
                               cudaStream_t st, int* grid_out);

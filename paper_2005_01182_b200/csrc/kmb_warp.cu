@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kmb_common.cuh"
 #include "kmb_internal.h"
@@ -105,7 +107,7 @@ __device__ __forceinline__ RowVec<CPL> load_row(const int32_t* p) {
 // Per-warp shared state (n <= 256), in 32-bit words: u, w, root_row,
 // match_row, match_col, tree_par, claim, found (8n) + two row lists of
 // (row, tag) pairs (4n).
-__host__ __device__ constexpr int warp_state_words(int n) { return 12 * n; }
+__host__ __device__ constexpr int warp_state_words(int n) { return 13 * n; }
 
 // Column keys.  Wide: ((c - w + 2^30) << 32) | row (any n, costs < 2^29).
 // Narrow (n <= 256, costs < 2^21): ((c - w + 2^22) << 8) | row in 32 bits, so a
@@ -147,13 +149,52 @@ struct Keys<true> {
 
 struct WarpSmem {
   int32_t *u, *w, *root_row, *match_row, *match_col, *tree_par, *found;
+  int32_t* rmin;  // U16 mode: row minimum | (wide row << 31)
   int32_t* ctr;  // [0] rows tail, [1] free columns found this epoch
   uint32_t* claim;
   int2 *rows, *spare;  // (row, tag)
 };
 
 // One instance, whole warp.  Returns the status (0 ok, -2 internal).
-template <int CPL, bool SMEM_C, bool NARROW>
+// U16 rows: 4 or 8 offsets from the row minimum (warp-width pitch, 8/16 B per
+// lane), returned already shifted into key position (d << 8) — one PRMT each.
+template <int CPL>
+__device__ __forceinline__ RowVec<CPL> load_row16(const uint16_t* p) {
+  RowVec<CPL> r;
+  if constexpr (CPL == 8) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t wv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      r.x[2 * h] = static_cast<int32_t>(__byte_perm(wv[h], 0u, 0x4104));
+      r.x[2 * h + 1] = static_cast<int32_t>(__byte_perm(wv[h], 0u, 0x4324));
+    }
+  } else {
+    static_assert(CPL == 4, "U16 rows need 4 or 8 columns per lane");
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+    r.x[0] = static_cast<int32_t>(__byte_perm(t.x, 0u, 0x4104));
+    r.x[1] = static_cast<int32_t>(__byte_perm(t.x, 0u, 0x4324));
+    r.x[2] = static_cast<int32_t>(__byte_perm(t.y, 0u, 0x4104));
+    r.x[3] = static_cast<int32_t>(__byte_perm(t.y, 0u, 0x4324));
+  }
+  return r;
+}
+
+// U16 mode (narrow keys only): a row's tag folds its minimum in,
+// key = (d << 8) + (tag + (rowmin << 8)) with d = C - rowmin; rows holding an
+// offset >= 65535 ("wide") carry bit 31 and are relaxed from the int32 matrix.
+template <bool NARROW, bool U16>
+__device__ __forceinline__ uint32_t row_tag(int32_t w, int32_t row, const int32_t* rmin) {
+  const uint32_t t = Keys<NARROW>::tag(w, row);
+  if constexpr (U16) {
+    const int32_t rm = rmin[row];
+    return rm < 0 ? (t | 0x80000000u) : t + (static_cast<uint32_t>(rm) << 8);
+  } else {
+    return t;
+  }
+}
+
+template <int CPL, bool SMEM_C, bool NARROW, bool U16 = false>
 __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* Cm, int inst,
                                               const WarpSmem& S, int lane) {
   using KO = Keys<NARROW>;
@@ -174,7 +215,9 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   int2* rows = S.rows;
   int2* spare = S.spare;
 
-  for (int k = lane; k < n; k += 32) rows[k] = make_int2(k, KO::tag(w[k], k));
+  const uint16_t* const lb16 = U16 ? a.C16 + static_cast<int64_t>(inst) * n * np + c0 : nullptr;
+  for (int k = lane; k < n; k += 32)
+    rows[k] = make_int2(k, static_cast<int32_t>(row_tag<NARROW, U16>(w[k], k, S.rmin)));
   if (lane == 0) {
     S.ctr[0] = n;
     S.ctr[1] = 0;
@@ -211,6 +254,64 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     int r = head;
     // RB rows in flight: entries, then all row loads, then the folds
     constexpr int RB = CPL <= 4 ? 8 : 4;
+    if constexpr (U16) {
+      // offsets arrive pre-shifted: key = min(key, (d << 8) + tag'); the last
+      // short batch repeats its last row (idempotent) instead of a serial tail
+      auto fold16 = [&](int2 e, const RowVec<CPL>& cv) {
+        if (e.y < 0) {  // wide row (rare, warp-uniform): exact int32 values
+          const RowVec<CPL> c32 = load_row<CPL, false>(lb + static_cast<uint32_t>(e.x) * np);
+          const uint32_t t = static_cast<uint32_t>(e.y) & 0x7fffffffu;
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) key[q] = KO::kmin(key[q], KO::make(c32.x[q], t, e.x));
+        } else {
+#pragma unroll
+          for (int q = 0; q < CPL; ++q)
+            key[q] = KO::kmin(key[q], static_cast<uint32_t>(cv.x[q]) + static_cast<uint32_t>(e.y));
+        }
+      };
+      for (; r + RB - 1 < nrows; r += RB) {
+        int2 e[RB];
+        RowVec<CPL> cv[RB];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) e[k] = rows[r + k];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) cv[k] = load_row16<CPL>(lb16 + static_cast<uint32_t>(e[k].x) * np);
+        int any_wide = 0;
+#pragma unroll
+        for (int k = 0; k < RB; ++k) any_wide |= e[k].y;
+        if (any_wide >= 0) {  // common case: no wide row in the batch, branch-free folds
+#pragma unroll
+          for (int k = 0; k < RB; ++k)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+              key[q] = KO::kmin(key[q], static_cast<uint32_t>(cv[k].x[q]) + static_cast<uint32_t>(e[k].y));
+        } else {
+#pragma unroll
+          for (int k = 0; k < RB; ++k) fold16(e[k], cv[k]);
+        }
+      }
+      if (r < nrows) {
+        int2 e[4];
+        RowVec<CPL> cv[4];
+        for (; r < nrows; r += 4) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) e[k] = rows[min(r + k, nrows - 1)];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) cv[k] = load_row16<CPL>(lb16 + static_cast<uint32_t>(e[k].x) * np);
+          if ((e[0].y | e[1].y | e[2].y | e[3].y) >= 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int q = 0; q < CPL; ++q)
+                key[q] = KO::kmin(key[q], static_cast<uint32_t>(cv[k].x[q]) + static_cast<uint32_t>(e[k].y));
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) fold16(e[k], cv[k]);
+          }
+        }
+        r = nrows;
+      }
+    }
     for (; r + RB - 1 < nrows; r += RB) {
       int2 e[RB];
       RowVec<CPL> cv[RB];
@@ -283,7 +384,8 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
           const int32_t w2 = u[i2] - D;
           w[i2] = w2;
           root_row[i2] = root;
-          rows[atomicAdd(S.ctr, 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
+          rows[atomicAdd(S.ctr, 1)] =
+              make_int2(i2, static_cast<int32_t>(row_tag<NARROW, U16>(w2, i2, S.rmin)));
         }
       }
     }
@@ -392,7 +494,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
 }
 
 template <int CPL, bool SMEM_C>
-__global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
+__global__ void __launch_bounds__(128, 7) k_warp_batch(WarpArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;  // warp in block
@@ -419,7 +521,10 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
   S.tree_par = S.match_col + n;
   S.claim = reinterpret_cast<uint32_t*>(S.tree_par + n);
   S.found = reinterpret_cast<int32_t*>(S.claim + n);
+  S.rmin = S.found + n;
   S.ctr = ctr;
+  constexpr bool kU16able = !SMEM_C && (CPL == 4 || CPL == 8);
+  const bool use16 = kU16able && a.C16 != nullptr;
 
   if (SMEM_C && lane == 0) mbar_init1(bar);
   __syncwarp();
@@ -427,6 +532,7 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
   const int c0 = CPL * lane;
 
   for (int inst = blockIdx.x * wpb + wib; inst < a.batch; inst += gridDim.x * wpb) {
+    const unsigned long long t_inst0 = globaltimer_ns();
     const int32_t* Cg = a.C + static_cast<int64_t>(inst) * n * np;
     const int32_t* Cm = Cg;
     if constexpr (SMEM_C) {
@@ -454,8 +560,20 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
     }
     __syncwarp();
     // validation (core.cpp:144-145 + device range) and row reductions
-    // (hungarian.cpp:323-327): the warp walks the rows, lanes across columns
+    // (hungarian.cpp:323-327): the warp walks the rows, lanes across columns —
+    // or, in U16 mode, reads what the packing pass (k_pack16) computed
     int32_t lo_all = 0x7fffffff, hi_all = 0;
+    if (use16) {
+      for (int k = lane; k < n; k += 32) {
+        const int32_t rm = __ldg(a.rmin + static_cast<int64_t>(inst) * n + k);
+        S.rmin[k] = rm;
+        const int32_t u0 = a.seed == 1 ? (rm & 0x7fffffff) : 0;
+        S.u[k] = u0;
+        S.w[k] = u0;
+      }
+      lo_all = __ldg(a.imin + inst);
+      hi_all = __ldg(a.imax + inst);
+    } else {
     // 8 rows in flight: loads first, then the per-row reductions
     for (int i0 = 0; i0 < n; i0 += 8) {
       RowVec<CPL> cv[8];
@@ -484,18 +602,94 @@ __global__ void __launch_bounds__(128) k_warp_batch(WarpArgs a) {
       }
     }
     hi_all = __reduce_max_sync(FULL, hi_all);
+    }
     int status = lo_all < 0 ? 2 : (hi_all >= (1 << 29) ? 3 : 0);
     __syncwarp();
     if (status == 0) {
-      status = hi_all < (1 << 21) ? solve_instance<CPL, SMEM_C, true>(a, Cm, inst, S, lane)
-                                  : solve_instance<CPL, SMEM_C, false>(a, Cm, inst, S, lane);
+      if constexpr (kU16able) {
+        if (use16 && hi_all < (1 << 21))
+          status = solve_instance<CPL, false, true, true>(a, Cm, inst, S, lane);
+        else if (hi_all < (1 << 21))
+          status = solve_instance<CPL, SMEM_C, true>(a, Cm, inst, S, lane);
+        else
+          status = solve_instance<CPL, SMEM_C, false>(a, Cm, inst, S, lane);
+      } else {
+        status = hi_all < (1 << 21) ? solve_instance<CPL, SMEM_C, true>(a, Cm, inst, S, lane)
+                                    : solve_instance<CPL, SMEM_C, false>(a, Cm, inst, S, lane);
+      }
     } else {
       for (int k = lane; k < n; k += 32) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
       if (lane == 0) a.total_cost[inst] = 0;
     }
-    if (lane == 0) a.status[inst] = status;
+    if (lane == 0) {
+      a.status[inst] = status;
+      if (a.stats) {
+        a.stats[KMB_ISTATS * static_cast<int64_t>(inst) + 9] = static_cast<int64_t>(t_inst0);
+        a.stats[KMB_ISTATS * static_cast<int64_t>(inst) + 10] = static_cast<int64_t>(globaltimer_ns());
+      }
+    }
     __syncwarp();
   }
+}
+
+// U16 packing pass: per row, the minimum and the offsets d = C - min saturated
+// at 65535 (16 bits, same warp-width pitch); a row with a saturated offset is
+// flagged "wide" (bit 31 of its minimum) and relaxed from the int32 matrix.
+// Also the per-instance min/max used for validation.  One warp per row.
+template <int CPL>
+__global__ void __launch_bounds__(256) k_pack16(WarpArgs a, uint16_t* C16, int32_t* rmin,
+                                                int32_t* imin, int32_t* imax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows_all = static_cast<int64_t>(a.batch) * a.n;
+  const int c0 = CPL * lane;
+  for (int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < nrows_all;
+       g += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const RowVec<CPL> cv = load_row<CPL, false>(a.C + g * a.pitch + c0);
+    int32_t lo = 0x7fffffff, hi = 0;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+      if (c0 + q < a.n) {
+        lo = min(lo, cv.x[q]);
+        hi = max(hi, cv.x[q]);
+      }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    uint32_t d[CPL];
+    bool wide = false;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int64_t x = static_cast<int64_t>(cv.x[q]) - lo;
+      d[q] = x >= 65535 || x < 0 ? 65535u : static_cast<uint32_t>(x);
+      wide |= (c0 + q < a.n) && x >= 65535;
+    }
+    wide = __any_sync(0xffffffffu, wide);
+    uint16_t* out = C16 + g * a.pitch + c0;
+    if constexpr (CPL == 8) {
+      *reinterpret_cast<uint4*>(out) = make_uint4(d[0] | (d[1] << 16), d[2] | (d[3] << 16),
+                                                  d[4] | (d[5] << 16), d[6] | (d[7] << 16));
+    } else {
+      *reinterpret_cast<uint2*>(out) = make_uint2(d[0] | (d[1] << 16), d[2] | (d[3] << 16));
+    }
+    if (lane == 0) {
+      rmin[g] = wide ? (lo | static_cast<int32_t>(0x80000000u)) : lo;
+      const int inst = static_cast<int>(g / a.n);
+      atomicMin(imin + inst, lo);
+      atomicMax(imax + inst, hi);
+    }
+  }
+}
+
+cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_t* rmin,
+                          int32_t* imin, int32_t* imax, cudaStream_t st) {
+  const int cpl = a.pitch / 32;
+  if (cpl != 4 && cpl != 8) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(imin, 0x7f, static_cast<size_t>(a.batch) * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(imax, 0, static_cast<size_t>(a.batch) * 4, st);
+  if (e != cudaSuccess) return e;
+  const int blocks = sm_count * 8;
+  if (cpl == 4) k_pack16<4><<<blocks, 256, 0, st>>>(a, C16, rmin, imin, imax);
+  else k_pack16<8><<<blocks, 256, 0, st>>>(a, C16, rmin, imin, imax);
+  return cudaGetLastError();
 }
 
 int warp_max_n() { return 256; }
@@ -513,10 +707,21 @@ static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, int warps_
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
+  // the per-warp state lives in shared memory: ask for the largest carveout so
+  // residency is set by registers, not by an L1-favouring split
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * wpb, smem);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
+  if (getenv("KMB_DEBUG_OCC")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "k_warp_batch<%d,%d>: %d CTAs/SM x %d warps, dyn smem %zu B, regs %d, static smem %zu, local %zu, maxthr %d\n",
+            CPL, SMEM_C ? 1 : 0, occ, wpb, smem, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes, fa.maxThreadsPerBlock);
+  }
   const int warps_needed = a.batch;
   if (warps_per_sm > 0 && warps_per_sm / wpb < occ) occ = warps_per_sm / wpb > 0 ? warps_per_sm / wpb : 1;
   int grid = sm_count * occ;
