@@ -359,3 +359,34 @@ def test_calibrate_batch_level_matches_reference_rule():
     while B < cap and O.ref_solve_batched_km(c, B=B).objective > 1.1 * exact * (1 + 1e-12):
         B *= 2
     assert calibrate_batch_level(c, exact, 1.1) == min(B, cap)
+
+
+def test_warp_engine_u16_mode_exact(solver):
+    """KMB_OPT_U16: 16-bit row offsets with an exact int32 fallback for rows
+    whose range reaches 65535 ("wide" rows) — same duals as the reference,
+    including instances forced to have wide rows."""
+    from paper_2005_01182_b200.api import OPT_U16
+    rng = np.random.default_rng(61)
+    c = W.CONFIGS["c3"].make(batch=48).copy()
+    for t in range(0, 48, 3):  # make some rows wide
+        c[t, rng.integers(0, 128), rng.integers(0, 128)] += 200000
+    solver.set_option(OPT_ENGINE, 4)
+    solver.set_option(OPT_U16, 1)
+    try:
+        r = solver.solve_batch(c, KMB_SEED_BATCHED)
+        for n in (100, 128, 200, 256):  # 4 and 8 columns per lane, padded pitches
+            cc = rng.integers(0, 70000 + 2000 * (n % 7), size=(6, n, n)).astype(np.int32)
+            rr = solver.solve_batch(cc, KMB_SEED_BATCHED)
+            for t in range(6):
+                ref = O.ref_solve_batched_km(cc[t])
+                assert rr.total_cost[t] == ref.total_cost
+                np.testing.assert_array_equal(rr.u[t], ref.u)
+                np.testing.assert_array_equal(rr.v[t], ref.v)
+    finally:
+        solver.set_option(OPT_U16, 0)
+        solver.set_option(OPT_ENGINE, 0)
+    for t in range(48):
+        ref = O.ref_solve_batched_km(c[t])
+        assert r.total_cost[t] == ref.total_cost
+        np.testing.assert_array_equal(r.u[t], ref.u)
+        np.testing.assert_array_equal(r.v[t], ref.v)
