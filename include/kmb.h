@@ -131,6 +131,20 @@ int kmb_solve_sharded_i32(kmb_context* ctx, const int32_t* slab, int32_t n, int6
                           int32_t col_begin, int32_t ncols, int32_t seed, int32_t* row_to_col,
                           int64_t* u, int64_t* v_slab, int64_t* total_cost, kmb_stats* stats);
 
+/* ---- cost construction (the caller before the path) -----------------------
+ * The reference's build_instance (datasets.cpp:184-214) on the GPU:
+ * out[b][i][j] = llround(scale * d(a_b[i], b_b[j])) with d the Euclidean
+ * distance accumulated in double over the dimensions in order (squared = 1:
+ * the squared distance, BASELINE configs 2 and 4).  a: batch x n x dim,
+ * b: batch x m x dim, as double (dtype KMB_F64) or float promoted to double
+ * (KMB_F32); out: batch x n x m int32.  Pointers may be host or device memory;
+ * bit-identical to the reference on the same points.  KMB_ERANGE when a cost
+ * does not fit int32 (the output is then undefined). */
+enum { KMB_F64 = 0, KMB_F32 = 1 };
+int kmb_costs_from_points(kmb_context* ctx, const void* a, const void* b, int32_t dtype,
+                          int32_t batch, int32_t n, int32_t m, int32_t dim, double scale,
+                          int32_t squared, int32_t* out);
+
 /* Diagnostics: the grid engine's reduced-cost scan with every row in the
  * frontier (one full pass over the matrix per iteration), averaged over
  * `iters` passes; bytes counted = 4*n*n per pass. */

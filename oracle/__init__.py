@@ -64,6 +64,9 @@ def _load_ref():
             C.POINTER(C.c_int64), _i32p, C.POINTER(C.c_double)]
         lib.otref_quantize_costs.argtypes = [
             _i64p, C.c_int64, C.c_int64, _i64p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+        lib.otref_build_instance.argtypes = [_f64p, C.c_int32, _f64p, C.c_int32, C.c_int32,
+                                             C.c_double, _i64p]
         lib.otref_solve_many_i32.argtypes = [
             _i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i64p, C.POINTER(C.c_double)]
         _ref = lib
@@ -182,6 +185,21 @@ def ref_quantize_costs(cost, B: int):
     if rc:
         raise RefError(rc, lib.otref_last_error().decode())
     return chat[: c.size], N.value, bool(ll.value)
+
+
+def ref_build_instance(a, b, scale: float) -> np.ndarray:
+    """The reference's build_instance (datasets.cpp:184-214) on unit-weight
+    point clouds: llround(scale * Euclidean distance), int64 n x m."""
+    lib = _load_ref()
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    n, dim = a.shape
+    m = b.shape[0]
+    out = np.zeros(n * m, np.int64)
+    rc = lib.otref_build_instance(a, n, b, m, dim, float(scale), out)
+    if rc:
+        raise RefError(rc, lib.otref_last_error().decode())
+    return out.reshape(n, m)
 
 
 def ref_solve_many_i32(costs: np.ndarray, mode: int = 1, nthreads: int = 1):

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "ot/core.hpp"
+#include "ot/datasets.hpp"
 #include "ot/hungarian.hpp"
 
 namespace {
@@ -140,6 +141,24 @@ int otref_quantize_costs(const int64_t* cost, int64_t count, int64_t B,
     if (chat && !q.chat.empty()) std::memcpy(chat, q.chat.data(), sizeof(int64_t) * q.chat.size());
     if (N) *N = q.N;
     if (lossless) *lossless = q.lossless ? 1 : 0;
+  });
+}
+
+// ot::build_instance (datasets.cpp:184-214): C_ij = llround(scale * ||a_i - b_j||)
+// for unit-weight point clouds a (n x dim) and b (m x dim); the pin for the GPU
+// cost construction (csrc/kmb_costs.cu).
+int otref_build_instance(const double* a, int32_t n, const double* b, int32_t m, int32_t dim,
+                         double scale, int64_t* cost) {
+  return guarded([&] {
+    ot::PointCloudDistribution sa, sb;
+    sa.dim = sb.dim = dim;
+    sa.coords.assign(a, a + static_cast<size_t>(n) * dim);
+    sb.coords.assign(b, b + static_cast<size_t>(m) * dim);
+    sa.weights.assign(n, 1);
+    sb.weights.assign(m, 1);
+    if (n != m) throw std::invalid_argument("otref_build_instance: unit weights need n == m");
+    const ot::OTInstance inst = ot::build_instance(sa, sb, {scale}, "pts");
+    std::memcpy(cost, inst.cost.data(), sizeof(int64_t) * inst.cost.size());
   });
 }
 

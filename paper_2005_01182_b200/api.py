@@ -29,7 +29,8 @@ OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_U16 = 1, 2, 3,
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
                "kmb_solve_batch_i32", "kmb_nccl_unique_id", "kmb_shard_init_nccl",
                "kmb_shard_init_callbacks", "kmb_solve_sharded_i32", "kmb_bench_scan",
-               "kmb_last_instance_stats", "kmb_last_error", "kmb_abi_version")
+               "kmb_last_instance_stats", "kmb_costs_from_points", "kmb_last_error",
+               "kmb_abi_version")
 
 
 class KmbUnavailable(RuntimeError):
@@ -73,6 +74,8 @@ def load_library(path: str | None = None):
                                             vp, vp, vp, vp, C.POINTER(Stats)]
         lib.kmb_bench_scan.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.kmb_costs_from_points.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_int32, C.c_int32, C.c_double, C.c_int32, vp]
         lib.kmb_last_error.restype = C.c_char_p
         lib.kmb_abi_version.restype = C.c_int
         _lib = lib
@@ -179,6 +182,43 @@ class Solver:
         self._check(self._lib.kmb_bench_scan(self._h, C.c_void_p(_ptr(cost)), n, ld, iters,
                                              C.byref(t), C.byref(g)))
         return t.value, g.value
+
+    def costs_from_points(self, a, b, scale: float, squared: bool = False, out=None):
+        """The reference's build_instance (datasets.cpp:184-214) on the GPU:
+        ``llround(scale * ||a_i - b_j||)`` (``squared``: the squared distance).
+
+        ``a``: (n, dim) or (batch, n, dim), ``b`` likewise with m points; float64
+        or float32 (promoted to double), numpy (host) or torch (host or cuda).
+        Returns int32 costs (batch, n, m) or (n, m) in ``out`` (allocated like
+        ``a`` when None).  Raises KmbError(KMB_ERANGE) when a cost overflows int32.
+        """
+        single = len(a.shape) == 2
+        if single:
+            a, b = a[None], b[None]
+        if a.dtype not in (np.float64, np.float32) and str(a.dtype) not in (
+                "torch.float64", "torch.float32"):
+            raise ValueError("points must be float64 or float32")
+        if str(a.dtype) != str(b.dtype):
+            raise ValueError("a and b must share a dtype")
+        if hasattr(a, "contiguous"):
+            a, b = a.contiguous(), b.contiguous()
+        else:
+            a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+        batch, n, dim = a.shape
+        if b.shape[0] != batch or b.shape[2] != dim:
+            raise ValueError("point dimensions differ")
+        m = b.shape[1]
+        dtype = 0 if str(a.dtype).endswith("float64") else 1
+        if out is None:
+            if hasattr(a, "new_empty"):
+                import torch
+                out = torch.empty((batch, n, m), dtype=torch.int32, device=a.device)
+            else:
+                out = np.empty((batch, n, m), np.int32)
+        self._check(self._lib.kmb_costs_from_points(
+            self._h, C.c_void_p(_ptr(a)), C.c_void_p(_ptr(b)), dtype, batch, n, m, dim,
+            float(scale), int(bool(squared)), C.c_void_p(_ptr(out))))
+        return out[0] if single else out
 
     # -- numpy convenience -------------------------------------------------------
     def solve(self, cost: np.ndarray, seed: int = KMB_SEED_BATCHED,

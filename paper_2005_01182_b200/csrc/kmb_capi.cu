@@ -81,6 +81,8 @@ struct kmb_context {
       ctrl, obj;
   // batch workspace
   DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus, b16, brmin, bimin, bimax;
+  // cost construction workspace (host-resident points / output)
+  DevBuf pa, pb, pout, pbad;
   // column-sharded solve: the collective (NCCL or caller callbacks)
   std::unique_ptr<kmb::Exchange> exchange;
   // chunked host-input pipeline of the batch engines
@@ -131,7 +133,7 @@ void kmb_destroy(kmb_context* c) {
   for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
                     &c->obj, &c->bcost, &c->bpad, &c->b16, &c->brmin, &c->bimin, &c->bimax, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
-                    &c->bstatus})
+                    &c->bstatus, &c->pa, &c->pb, &c->pout, &c->pbad})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -509,6 +511,56 @@ int kmb_last_instance_stats(kmb_context* c, int64_t* out, int64_t capacity, int6
   const int64_t k = capacity < have ? capacity : have;
   *count = have / kmb::KMB_ISTATS;
   if (k > 0) KMB_CUDA(cudaMemcpy(out, c->bstat.p, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost));
+  return KMB_OK;
+}
+
+int kmb_costs_from_points(kmb_context* c, const void* a, const void* b, int32_t dtype,
+                          int32_t batch, int32_t n, int32_t m, int32_t dim, double scale,
+                          int32_t squared, int32_t* out) {
+  if (!c) return fail(KMB_EINVAL, "kmb_costs_from_points: NULL context");
+  if (!a || !b || !out || batch <= 0 || n <= 0 || m <= 0 || dim <= 0 ||
+      (dtype != KMB_F64 && dtype != KMB_F32))
+    return fail(KMB_EINVAL, "kmb_costs_from_points: bad arguments");
+  if (!(scale > 0.0)) return fail(KMB_EINVAL, "quantization scale must be positive");
+  KMB_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const size_t es = dtype == KMB_F64 ? 8 : 4;
+  const size_t abytes = es * batch * static_cast<size_t>(n) * dim;
+  const size_t bbytes = es * batch * static_cast<size_t>(m) * dim;
+  const size_t obytes = 4 * static_cast<size_t>(batch) * n * m;
+  const void* da = a;
+  const void* db = b;
+  if (!is_device_ptr(a)) {
+    KMB_CUDA(c->pa.ensure(abytes));
+    KMB_CUDA(cudaMemcpyAsync(c->pa.p, a, abytes, cudaMemcpyHostToDevice, st));
+    da = c->pa.p;
+  }
+  if (!is_device_ptr(b)) {
+    KMB_CUDA(c->pb.ensure(bbytes));
+    KMB_CUDA(cudaMemcpyAsync(c->pb.p, b, bbytes, cudaMemcpyHostToDevice, st));
+    db = c->pb.p;
+  }
+  const bool host_out = !is_device_ptr(out);
+  int32_t* dout = out;
+  if (host_out) {
+    KMB_CUDA(c->pout.ensure(obytes));
+    dout = c->pout.as<int32_t>();
+  }
+  KMB_CUDA(c->pbad.ensure(sizeof(int32_t)));
+  KMB_CUDA(cudaMemsetAsync(c->pbad.p, 0, sizeof(int32_t), st));
+  if (dtype == KMB_F64)
+    KMB_CUDA(kmb::launch_costs<double>(static_cast<const double*>(da), static_cast<const double*>(db),
+                                       batch, n, m, dim, scale, squared, dout,
+                                       c->pbad.as<int32_t>(), st));
+  else
+    KMB_CUDA(kmb::launch_costs<float>(static_cast<const float*>(da), static_cast<const float*>(db),
+                                      batch, n, m, dim, scale, squared, dout,
+                                      c->pbad.as<int32_t>(), st));
+  if (host_out) KMB_CUDA(cudaMemcpyAsync(out, dout, obytes, cudaMemcpyDeviceToHost, st));
+  int32_t bad = 0;
+  KMB_CUDA(cudaMemcpyAsync(&bad, c->pbad.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  KMB_CUDA(cudaStreamSynchronize(st));
+  if (bad) return fail(KMB_ERANGE, "kmb_costs_from_points: a cost does not fit int32");
   return KMB_OK;
 }
 

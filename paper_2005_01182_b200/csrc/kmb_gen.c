@@ -161,3 +161,46 @@ uint64_t kmb_fnv1a64(const void* data, int64_t nbytes) {
   }
   return h;
 }
+
+/* ---- the point sets behind configs 2-4 (same streams as the cost generators
+ * above), for GPU cost construction (csrc/kmb_costs.cu) ------------------ */
+
+/* config 2: a, b = n x 2 doubles */
+void kmb_gen_geometric_points(double* a, double* b, int32_t n, uint64_t seed) {
+  const uint64_t sa = stream_of(seed, 2), sb = stream_of(seed, 3);
+  for (int32_t p = 0; p < 2 * n; ++p) {
+    a[p] = unit(sa, (uint64_t)p, 0);
+    b[p] = unit(sb, (uint64_t)p, 0);
+  }
+}
+
+/* config 4: a, b = n x 3 doubles */
+void kmb_gen_gmm_points(double* a, double* b, int32_t n, int32_t comps, double box, double sigma,
+                        uint64_t seed) {
+  double* mu = malloc(sizeof(double) * 3 * (size_t)comps);
+  const uint64_t sm = stream_of(seed, 5);
+  for (int32_t k = 0; k < 3 * comps; ++k) mu[k] = box * unit(sm, (uint64_t)k, 0);
+  for (int s = 0; s < 2; ++s) {
+    double* P = s == 0 ? a : b;
+    const uint64_t sc = stream_of(seed, 6 + 2 * (uint64_t)s);
+    const uint64_t sz = stream_of(seed, 7 + 2 * (uint64_t)s);
+    for (int32_t p = 0; p < n; ++p) {
+      const int32_t comp = (int32_t)bounded(sc, (uint64_t)p, (uint64_t)comps);
+      for (int d = 0; d < 3; ++d)
+        P[3 * p + d] = mu[3 * comp + d] + sigma * normal(sz, (uint64_t)(3 * p + d));
+    }
+  }
+  free(mu);
+}
+
+/* config 3: instances first..first+batch-1; a, b = batch x n x dim floats */
+void kmb_gen_embedding_vectors(float* a, float* b, int32_t first, int32_t batch, int32_t n,
+                               int32_t dim, uint64_t seed) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int32_t t = 0; t < batch; ++t) {
+    const uint64_t st = stream_of(seed, (4ULL << 32) | (uint64_t)(first + t));
+    const int64_t nd = (int64_t)n * dim;
+    for (int64_t k = 0; k < nd; ++k) a[(size_t)t * nd + k] = (float)normal(st, (uint64_t)k);
+    for (int64_t k = 0; k < nd; ++k) b[(size_t)t * nd + k] = (float)normal(st, (uint64_t)(nd + k));
+  }
+}

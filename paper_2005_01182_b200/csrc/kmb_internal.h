@@ -116,6 +116,10 @@ cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_
 int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)
 cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int warps_per_sm,
                               cudaStream_t st, int* grid_out);
+// cost construction (kmb_costs.cu)
+template <typename P>
+cudaError_t launch_costs(const P* a, const P* b, int32_t batch, int32_t n, int32_t m, int32_t dim,
+                         double scale, int32_t squared, int32_t* out, int32_t* bad, cudaStream_t st);
 }  // namespace kmb
 
 namespace kmb {

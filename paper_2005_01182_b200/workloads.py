@@ -36,6 +36,13 @@ def _load():
                                                 C.c_int32, C.c_double, C.c_uint64]
         lib.kmb_gen_gmm.argtypes = [_i32p, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                     C.c_double, C.c_uint64]
+        _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+        _f32p = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
+        lib.kmb_gen_geometric_points.argtypes = [_f64p, _f64p, C.c_int32, C.c_uint64]
+        lib.kmb_gen_gmm_points.argtypes = [_f64p, _f64p, C.c_int32, C.c_int32, C.c_double,
+                                           C.c_double, C.c_uint64]
+        lib.kmb_gen_embedding_vectors.argtypes = [_f32p, _f32p, C.c_int32, C.c_int32, C.c_int32,
+                                                  C.c_int32, C.c_uint64]
         lib.kmb_fnv1a64.argtypes = [C.c_void_p, C.c_int64]
         lib.kmb_fnv1a64.restype = C.c_uint64
         _lib = lib
@@ -71,6 +78,27 @@ def gmm(n: int, comps: int = 16, box: float = 100.0, sigma: float = 1.0,
     out = np.empty((n, n), np.int32)
     _load().kmb_gen_gmm(out, n, comps, box, sigma, scale, seed)
     return out
+
+
+def points(key: str, batch: int | None = None, first: int = 0):
+    """The point sets behind configs 2-4 (same seeded streams as their cost
+    matrices): (a, b, dim, scale, squared).  Config 3 returns float32
+    (batch, n, 300) arrays, configs 2 and 4 float64 (n, dim)."""
+    lib = _load()
+    if key == "c2":
+        a = np.empty((1024, 2)); b = np.empty((1024, 2))
+        lib.kmb_gen_geometric_points(a, b, 1024, 2)
+        return a, b, 2, 1e6, True
+    if key == "c4":
+        a = np.empty((4096, 3)); b = np.empty((4096, 3))
+        lib.kmb_gen_gmm_points(a, b, 4096, 16, 100.0, 1.0, 4)
+        return a, b, 3, 1e3, True
+    if key == "c3":
+        bt = 4096 if batch is None else batch
+        a = np.empty((bt, 128, 300), np.float32); b = np.empty((bt, 128, 300), np.float32)
+        lib.kmb_gen_embedding_vectors(a, b, first, bt, 128, 300, 3)
+        return a, b, 300, 1e4, False
+    raise KeyError(key)
 
 
 def fnv1a64(a: np.ndarray) -> int:
