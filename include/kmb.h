@@ -87,7 +87,8 @@ typedef struct kmb_stats {
   int64_t stage_ns[6];     /* grid engine, CTA 0's clock (ns): relax, barrier 1,
                               absorb, barrier 2, epoch end, barrier 3;
                               warp engine: SM cycles summed over instances in
-                              relax, min, absorb, epoch end                  */
+                              relax, min, absorb, epoch end (0 unless built
+                              with -DKMB_WARP_STAGE_CLOCKS=1)                */
   int64_t max_instance_cycles; /* batch engines: slowest instance (SM clocks) */
   int64_t sum_instance_cycles; /* batch engines: sum over instances          */
 } kmb_stats;

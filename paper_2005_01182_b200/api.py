@@ -58,7 +58,7 @@ def load_library(path: str | None = None):
     """Load libkmb.so (built in-tree by ``_build.build_lib``).  Fails loudly."""
     global _lib
     if _lib is None:
-        path = path or _build.LIB_SO
+        path = path or os.environ.get("KMB_LIB") or _build.LIB_SO
         if not os.path.exists(path):
             raise KmbUnavailable(f"{path} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
         lib = C.CDLL(path)

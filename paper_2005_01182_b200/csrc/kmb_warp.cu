@@ -57,6 +57,26 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       : "memory");
 }
 
+// Build-time switches (A/B measured on config 3, tools/ab_lib.py):
+//   KMB_WARP_PREFETCH     TMA L2 prefetch of multi-batch relaxes: 1.17 -> 1.33 ms, off
+//   KMB_WARP_CLAMP        short relaxes as one clamped batch: 1.142 -> 1.132 ms, on
+//   KMB_WARP_STAGE_CLOCKS per-stage clock64 accounting (kmb_last_instance_stats
+//                         columns 5-8): costs 2.7%, off unless diagnosing
+#ifndef KMB_WARP_PREFETCH
+#define KMB_WARP_PREFETCH 0
+#endif
+#ifndef KMB_WARP_CLAMP
+#define KMB_WARP_CLAMP 1
+#endif
+#ifndef KMB_WARP_STAGE_CLOCKS
+#define KMB_WARP_STAGE_CLOCKS 0
+#endif
+
+// TMA bulk prefetch of `bytes` (multiple of 16) at a 16-byte aligned address into L2
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\nW_%=:\n"
@@ -240,12 +260,16 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   const long long t_start = clock64();
   long long cyc[4] = {0, 0, 0, 0};  // relax, min, absorb, epoch end
   long long tl = t_start;
+#if KMB_WARP_STAGE_CLOCKS
 #define KMB_WSTAGE(k)                 \
   do {                                \
     const long long t_ = clock64();   \
     cyc[k] += t_ - tl;                \
     tl = t_;                          \
   } while (0)
+#else
+#define KMB_WSTAGE(k) (void)tl
+#endif
   __syncwarp();
 
   while (nfree > 0) {
@@ -312,6 +336,12 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
         r = nrows;
       }
     }
+    if (KMB_WARP_PREFETCH && !SMEM_C && !U16 && nrows - r > RB) {
+      // more than one batch pending (first round, epoch starts): one lane per
+      // row asks TMA to pull the rows into L2 so later batches hit there
+      for (int k = r + RB + lane; k < nrows; k += 32)
+        bulk_prefetch_l2(Cm + static_cast<uint32_t>(rows[k].x) * np, np * 4);
+    }
     for (; r + RB - 1 < nrows; r += RB) {
       int2 e[RB];
       RowVec<CPL> cv[RB];
@@ -326,13 +356,37 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
         for (int q = 0; q < CPL; ++q)
           key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), e[k].x));
     }
-    for (; r < nrows; ++r) {
+    if (!KMB_WARP_CLAMP) {
+      for (; r < nrows; ++r) {
+        const int2 e = rows[r];
+        const RowVec<CPL> cv = load_row<CPL, SMEM_C>(lb + static_cast<uint32_t>(e.x) * np);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          key[q] = KO::kmin(key[q], KO::make(cv.x[q], static_cast<uint32_t>(e.y), e.x));
+      }
+    } else if (nrows - r == 1) {
       const int2 e = rows[r];
       const RowVec<CPL> cv = load_row<CPL, SMEM_C>(lb + static_cast<uint32_t>(e.x) * np);
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
         key[q] = KO::kmin(key[q], KO::make(cv.x[q], static_cast<uint32_t>(e.y), e.x));
+    } else if (r < nrows) {
+      // 2..RB-1 rows: one batch with the last row repeated (the fold is
+      // idempotent), so all loads are in flight together
+      int2 e[RB];
+      RowVec<CPL> cv[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) e[k] = rows[min(r + k, nrows - 1)];
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        cv[k] = load_row<CPL, SMEM_C>(lb + static_cast<uint32_t>(e[k].x) * np);
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), e[k].x));
     }
+    r = nrows;
     rows_scanned += nrows - head;
     head = nrows;
     KMB_WSTAGE(0);
