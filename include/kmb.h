@@ -132,6 +132,31 @@ int kmb_solve_sharded_i32(kmb_context* ctx, const int32_t* slab, int32_t n, int6
                           int32_t col_begin, int32_t ncols, int32_t seed, int32_t* row_to_col,
                           int64_t* u, int64_t* v_slab, int64_t* total_cost, kmb_stats* stats);
 
+/* ---- auction (the reference's other unit-capacity solver, auction.hpp) ---
+ * Gauss-Seidel auction, bit-identical to ot::solve_auction (scaled = 0,
+ * epsilon = AuctionConfig::epsilon) and ot::solve_auction_scaled (scaled = 1,
+ * epsilon = epsilon0, theta, epsilon_final; <= 0 picks the reference's
+ * defaults): same bids, same double prices, same assignment.  `batch`
+ * independent n x n instances back to back (n <= 18000); host or device
+ * pointers; every output optional.  Per instance: prices (n doubles),
+ * row_to_col (n; -1 for rows a budget left unassigned), total_cost of the
+ * assigned pairs, bids (SolveResult::iterations), converged, and the epsilon
+ * of the last round (exact = converged && epsilon * n < 1, auction.cpp:172).
+ * seconds (optional): device time.  Errors: KMB_EINVAL with the reference's
+ * messages for epsilon <= 0 / theta <= 1, KMB_ENEGATIVE for negative costs. */
+typedef struct {
+  int32_t scaled;
+  double epsilon;
+  double theta;
+  double epsilon_final;
+  int64_t max_bids;
+  double time_budget_s;
+} kmb_auction_config;
+int kmb_auction_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, int32_t n,
+                    const kmb_auction_config* cfg, double* prices, int32_t* row_to_col,
+                    int64_t* total_cost, int64_t* bids, int32_t* converged,
+                    double* epsilon_last, double* seconds);
+
 /* ---- cost construction (the caller before the path) -----------------------
  * The reference's build_instance (datasets.cpp:184-214) on the GPU:
  * out[b][i][j] = llround(scale * d(a_b[i], b_b[j])) with d the Euclidean

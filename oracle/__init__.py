@@ -67,6 +67,10 @@ def _load_ref():
         _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
         lib.otref_build_instance.argtypes = [_f64p, C.c_int32, _f64p, C.c_int32, C.c_int32,
                                              C.c_double, _i64p]
+        lib.otref_solve_auction.argtypes = [
+            _i64p, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int64,
+            C.c_double, _f64p, _i32p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+            C.POINTER(C.c_int64), _i32p, C.POINTER(C.c_double)]
         lib.otref_solve_many_i32.argtypes = [
             _i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i64p, C.POINTER(C.c_double)]
         _ref = lib
@@ -95,6 +99,10 @@ def _load_oracle():
             _i32p, C.c_int32, C.c_int32, _i64p, _i64p, _i32p, C.POINTER(C.c_int64),
             C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
             C.POINTER(C.c_int64), C.c_void_p, C.c_int64]
+        lib.kmo_auction.argtypes = [
+            _i64p, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int64,
+            np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS"), _i32p,
+            C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         _orc = lib
     return _orc
 
@@ -123,6 +131,7 @@ class Solution:
     rows_scanned: int = 0
     trace: np.ndarray | None = field(default=None, repr=False)
     chat: np.ndarray | None = field(default=None, repr=False)
+    prices: np.ndarray | None = field(default=None, repr=False)
 
 
 def _sq(cost) -> tuple[np.ndarray, int]:
@@ -185,6 +194,54 @@ def ref_quantize_costs(cost, B: int):
     if rc:
         raise RefError(rc, lib.otref_last_error().decode())
     return chat[: c.size], N.value, bool(ll.value)
+
+
+def ref_solve_auction(cost, epsilon: float = 1.0, max_bids: int = 1000000000,
+                      time_budget_s: float = 0.0) -> Solution:
+    """The reference ``ot::solve_auction`` (auction.cpp:186-199), unmodified.
+    ``iterations`` = bids; ``prices`` = the final column prices."""
+    return _ref_auction(cost, 0, epsilon, 0.0, 0.0, max_bids, time_budget_s)
+
+
+def ref_solve_auction_scaled(cost, epsilon0: float = 0.0, theta: float = 4.0,
+                             epsilon_final: float = 0.0, max_bids: int = 1000000000,
+                             time_budget_s: float = 0.0) -> Solution:
+    """The reference ``ot::solve_auction_scaled`` (auction.cpp:201-229), unmodified."""
+    return _ref_auction(cost, 1, epsilon0, theta, epsilon_final, max_bids, time_budget_s)
+
+
+def _ref_auction(cost, scaled, e0, theta, ef, max_bids, budget) -> Solution:
+    lib = _load_ref()
+    c, n = _sq(np.asarray(cost, dtype=np.int64))
+    p = np.zeros(max(n, 1), np.float64); r2c = np.full(max(n, 1), -1, np.int32)
+    tot = C.c_int64(); obj = C.c_double(); it = C.c_int64(); ec = np.zeros(2, np.int32)
+    wall = C.c_double()
+    rc = lib.otref_solve_auction(c, n, scaled, e0, theta, ef, int(max_bids), budget, p, r2c,
+                                 C.byref(tot), C.byref(obj), C.byref(it), ec, C.byref(wall))
+    if rc:
+        raise RefError(rc, lib.otref_last_error().decode())
+    z = np.zeros(n, np.int64)
+    return Solution(r2c[:n], z, z, tot.value, obj.value, it.value, bool(ec[0]), bool(ec[1]),
+                    wall.value, prices=p[:n])
+
+
+def kmo_auction(cost, scaled: bool = False, epsilon: float = 1.0, theta: float = 4.0,
+                epsilon_final: float = 0.0, max_bids: int = 1000000000) -> Solution:
+    """The C restatement of auction.cpp (oracle/auction_oracle.c).  For
+    ``scaled`` the epsilon argument is epsilon0 (<= 0: default schedule)."""
+    lib = _load_oracle()
+    c, n = _sq(np.asarray(cost, dtype=np.int64))
+    p = np.zeros(n, np.float64); r2c = np.full(n, -1, np.int32)
+    bids = C.c_int64(); comp = C.c_int32(); eps = C.c_double()
+    rc = lib.kmo_auction(c, n, int(scaled), epsilon, theta, epsilon_final, int(max_bids), p, r2c,
+                         C.byref(bids), C.byref(comp), C.byref(eps))
+    if rc:
+        raise ValueError("kmo_auction: invalid arguments")
+    tot = int(sum(int(c[i, r2c[i]]) for i in range(n) if r2c[i] >= 0))
+    z = np.zeros(n, np.int64)
+    done = bool(comp.value)
+    return Solution(r2c, z, z, tot, float(tot), bids.value, done and eps.value * n < 1.0, done,
+                    prices=p)
 
 
 def ref_build_instance(a, b, scale: float) -> np.ndarray:

@@ -8,6 +8,9 @@
 //   ot::solve_km           hungarian.hpp:39-40, hungarian.cpp:55-136
 //   ot::solve_batched_km   hungarian.hpp:53-56, hungarian.cpp:313-381
 //   ot::quantize_costs     hungarian.hpp:35,   hungarian.cpp:33-53
+//   ot::solve_auction      auction.hpp:30-32,  auction.cpp:186-199
+//   ot::solve_auction_scaled auction.hpp:48-50, auction.cpp:201-229
+//   ot::build_instance     datasets.hpp,       datasets.cpp:184-214
 // Errors: std::invalid_argument -> 1, std::logic_error -> 2, other -> 3;
 // the message is kept in a thread-local buffer (otref_last_error).
 
@@ -20,6 +23,7 @@
 #include <atomic>
 #include <vector>
 
+#include "ot/auction.hpp"
 #include "ot/core.hpp"
 #include "ot/datasets.hpp"
 #include "ot/hungarian.hpp"
@@ -159,6 +163,38 @@ int otref_build_instance(const double* a, int32_t n, const double* b, int32_t m,
     if (n != m) throw std::invalid_argument("otref_build_instance: unit weights need n == m");
     const ot::OTInstance inst = ot::build_instance(sa, sb, {scale}, "pts");
     std::memcpy(cost, inst.cost.data(), sizeof(int64_t) * inst.cost.size());
+  });
+}
+
+// ot::solve_auction / ot::solve_auction_scaled (auction.cpp:186-229).
+// scaled = 0: eps0 is AuctionConfig::epsilon (theta, eps_final unused);
+// scaled = 1: AuctionScaledConfig{eps0, theta, eps_final}.  prices: n doubles.
+int otref_solve_auction(const int64_t* cost, int32_t n, int32_t scaled, double eps0, double theta,
+                        double eps_final, int64_t max_bids, double time_budget_s,
+                        double* prices, int32_t* row_to_col, int64_t* total_cost,
+                        double* objective, int64_t* iterations, int32_t* exact_converged,
+                        double* wall) {
+  return guarded([&] {
+    ot::OTInstance inst = make_unit(cost, n);
+    std::vector<double> p;
+    ot::SolveResult res;
+    if (scaled) {
+      ot::AuctionScaledConfig cfg;
+      cfg.epsilon0 = eps0;
+      cfg.theta = theta;
+      cfg.epsilon_final = eps_final;
+      cfg.max_bids = max_bids;
+      cfg.time_budget_s = time_budget_s;
+      res = ot::solve_auction_scaled(inst, cfg, &p);
+    } else {
+      ot::AuctionConfig cfg;
+      cfg.epsilon = eps0;
+      cfg.max_bids = max_bids;
+      cfg.time_budget_s = time_budget_s;
+      res = ot::solve_auction(inst, cfg, &p);
+    }
+    if (prices && !p.empty()) std::memcpy(prices, p.data(), sizeof(double) * p.size());
+    fill(inst, res, {row_to_col, total_cost, objective, iterations, exact_converged, wall});
   });
 }
 

@@ -3,16 +3,22 @@
 
 Layers:
   include/kmb.h               C ABI (the drop-in boundary)
-  csrc/kmb_solver.cu          persistent grid engine (one instance, any n)
-  csrc/kmb_batch.cu           SMEM engine (one CTA per small instance)
+  csrc/kmb_solver.cu          persistent grid / cluster engines (one instance, any n)
+  csrc/kmb_warp.cu            warp engine (one warp per small instance, batches)
+  csrc/kmb_batch.cu           CTA engines (one CTA per small instance)
+  csrc/kmb_shard.cu           column-sharded single instance over ranks (NCCL)
+  csrc/kmb_auction.cu         Gauss-Seidel auction (ot::solve_auction[_scaled])
+  csrc/kmb_costs.cu           cost construction (ot::build_instance)
   csrc/kmb_capi.cu            context, workspace, staging
-  api.py                      Python mirror of ot::solve_km / ot::solve_batched_km
+  api.py                      Python mirror of ot::solve_km / solve_batched_km /
+                              solve_auction / solve_auction_scaled
   workloads.py                seeded inputs for the BASELINE configs
 """
 from .api import (KMB_SEED_BATCHED, KMB_SEED_KM, KmbError, KmbUnavailable, Result, Solver,
-                  calibrate_batch_level, default_solver, load_library, quantize_costs,
-                  solve_batched_km, solve_km)
+                  calibrate_auction_eps, calibrate_batch_level, default_solver, load_library,
+                  quantize_costs, solve_auction, solve_auction_scaled, solve_batched_km, solve_km)
 
 __all__ = ["KMB_SEED_BATCHED", "KMB_SEED_KM", "KmbError", "KmbUnavailable", "Result", "Solver",
-           "calibrate_batch_level", "default_solver", "load_library", "quantize_costs",
-           "solve_batched_km", "solve_km"]
+           "calibrate_auction_eps", "calibrate_batch_level", "default_solver", "load_library",
+           "quantize_costs", "solve_auction", "solve_auction_scaled", "solve_batched_km",
+           "solve_km"]

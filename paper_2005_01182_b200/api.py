@@ -29,8 +29,8 @@ OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_U16 = 1, 2, 3,
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
                "kmb_solve_batch_i32", "kmb_nccl_unique_id", "kmb_shard_init_nccl",
                "kmb_shard_init_callbacks", "kmb_solve_sharded_i32", "kmb_bench_scan",
-               "kmb_last_instance_stats", "kmb_costs_from_points", "kmb_last_error",
-               "kmb_abi_version")
+               "kmb_last_instance_stats", "kmb_costs_from_points", "kmb_auction_i32",
+               "kmb_last_error", "kmb_abi_version")
 
 
 class KmbUnavailable(RuntimeError):
@@ -49,6 +49,13 @@ class Stats(C.Structure):
                 ("converged", C.c_int32), ("engine", C.c_int32), ("rounds", C.c_int64),
                 ("stage_ns", C.c_int64 * 6), ("max_instance_cycles", C.c_int64),
                 ("sum_instance_cycles", C.c_int64)]
+
+
+class AuctionConfig(C.Structure):
+    """``kmb_auction_config`` (include/kmb.h)."""
+    _fields_ = [("scaled", C.c_int32), ("epsilon", C.c_double), ("theta", C.c_double),
+                ("epsilon_final", C.c_double), ("max_bids", C.c_int64),
+                ("time_budget_s", C.c_double)]
 
 
 _lib = None
@@ -76,6 +83,8 @@ def load_library(path: str | None = None):
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
         lib.kmb_costs_from_points.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32,
                                               C.c_int32, C.c_int32, C.c_double, C.c_int32, vp]
+        lib.kmb_auction_i32.argtypes = [vp, vp, C.c_int32, C.c_int32, C.POINTER(AuctionConfig),
+                                        vp, vp, vp, vp, vp, vp, C.POINTER(C.c_double)]
         lib.kmb_last_error.restype = C.c_char_p
         lib.kmb_abi_version.restype = C.c_int
         _lib = lib
@@ -102,6 +111,7 @@ class Result:
     converged: bool = True
     wall_seconds: float = 0.0
     stats: dict = field(default_factory=dict)
+    prices: object = None  # auction: final column prices
 
     @property
     def objective(self) -> float:
@@ -182,6 +192,41 @@ class Solver:
         self._check(self._lib.kmb_bench_scan(self._h, C.c_void_p(_ptr(cost)), n, ld, iters,
                                              C.byref(t), C.byref(g)))
         return t.value, g.value
+
+    def auction_into(self, costs, batch: int, n: int, cfg: AuctionConfig, prices=None,
+                     row_to_col=None, total_cost=None, bids=None, converged=None,
+                     epsilon_last=None) -> float:
+        """Raw ``kmb_auction_i32``; returns the device seconds."""
+        sec = C.c_double()
+        self._check(self._lib.kmb_auction_i32(
+            self._h, C.c_void_p(_ptr(costs)), batch, n, C.byref(cfg), C.c_void_p(_ptr(prices)),
+            C.c_void_p(_ptr(row_to_col)), C.c_void_p(_ptr(total_cost)), C.c_void_p(_ptr(bids)),
+            C.c_void_p(_ptr(converged)), C.c_void_p(_ptr(epsilon_last)), C.byref(sec)))
+        return sec.value
+
+    def auction(self, costs, scaled: bool = True, epsilon: float = 0.0, theta: float = 4.0,
+                epsilon_final: float = 0.0, max_bids: int = 1000000000,
+                time_budget_s: float = 0.0) -> dict:
+        """Batched auction on (n, n) or (batch, n, n) int32 costs (numpy).
+        ``scaled``: solve_auction_scaled (epsilon = epsilon0); else solve_auction."""
+        c = np.ascontiguousarray(costs, dtype=np.int32)
+        single = c.ndim == 2
+        if single:
+            c = c[None]
+        b, n, n2 = c.shape
+        if n != n2:
+            raise ValueError("square cost matrices required")
+        cfg = AuctionConfig(int(bool(scaled)), float(epsilon), float(theta), float(epsilon_final),
+                            int(max_bids), float(time_budget_s))
+        out = dict(prices=np.zeros((b, n)), row_to_col=np.full((b, n), -1, np.int32),
+                   total_cost=np.zeros(b, np.int64), bids=np.zeros(b, np.int64),
+                   converged=np.zeros(b, np.int32), epsilon_last=np.zeros(b))
+        out["seconds"] = self.auction_into(c, b, n, cfg, **{k: out[k] for k in (
+            "prices", "row_to_col", "total_cost", "bids", "converged", "epsilon_last")})
+        if single:
+            for k in ("prices", "row_to_col", "total_cost", "bids", "converged", "epsilon_last"):
+                out[k] = out[k][0]
+        return out
 
     def costs_from_points(self, a, b, scale: float, squared: bool = False, out=None):
         """The reference's build_instance (datasets.cpp:184-214) on the GPU:
@@ -376,6 +421,71 @@ def calibrate_batch_level(cost, exact: float, target_ratio: float = 1.1,
         if r.objective <= target_ratio * exact * (1 + 1e-12):
             return B
         B *= 2
+
+
+def _auction_result(c, o, n: int) -> Result:
+    ok = o["row_to_col"] >= 0
+    rows = np.arange(n)
+    tot = int(np.asarray(c, np.int64)[rows[ok], o["row_to_col"][ok]].sum())
+    conv = bool(o["converged"])
+    return Result(o["row_to_col"], None, None, tot, iterations=int(o["bids"]),
+                  exact=conv and float(o["epsilon_last"]) * n < 1.0, converged=conv,
+                  wall_seconds=o["seconds"], prices=o["prices"])
+
+
+def _auction_costs(cost, supplies, demands, who: str) -> np.ndarray:
+    c = _validate(cost, supplies, demands, who)
+    if (np.asarray(c) < 0).any():
+        raise ValueError(f"{who}: costs must be nonnegative")
+    if np.asarray(c).max() > 2**31 - 1:
+        raise ValueError(f"{who}: cost exceeds the device range [0, 2^31)")
+    return np.asarray(c).astype(np.int32)
+
+
+def solve_auction(cost, epsilon: float = 1.0, max_bids: int = 1000000000,
+                  time_budget_s: float = 0.0, supplies=None, demands=None,
+                  solver: Solver | None = None) -> Result:
+    """``ot::solve_auction`` (auction.cpp:186-199) on the GPU: the same bids, the
+    same double prices (``Result.prices``), the same assignment; ``iterations``
+    counts bids, ``exact`` = converged and n * epsilon < 1."""
+    c = _auction_costs(cost, supplies, demands, "solve_auction")
+    if not epsilon > 0.0:
+        raise ValueError("solve_auction: epsilon must be positive")
+    o = (solver or default_solver()).auction(c, False, epsilon, 4.0, 0.0, max_bids, time_budget_s)
+    return _auction_result(c, o, c.shape[0])
+
+
+def solve_auction_scaled(cost, epsilon0: float = 0.0, theta: float = 4.0,
+                         epsilon_final: float = 0.0, max_bids: int = 1000000000,
+                         time_budget_s: float = 0.0, supplies=None, demands=None,
+                         solver: Solver | None = None) -> Result:
+    """``ot::solve_auction_scaled`` (auction.cpp:201-229) on the GPU: epsilon
+    scaling with prices carried across rounds; defaults as the reference's
+    (epsilon0 <= 0: max_cost / 2; epsilon_final <= 0: 1 / (n + 1), exact)."""
+    c = _auction_costs(cost, supplies, demands, "solve_auction_scaled")
+    if not theta > 1.0:
+        raise ValueError("solve_auction_scaled: theta must exceed 1")
+    o = (solver or default_solver()).auction(c, True, epsilon0, theta, epsilon_final, max_bids,
+                                             time_budget_s)
+    return _auction_result(c, o, c.shape[0])
+
+
+def calibrate_auction_eps(cost, exact_int: int, solver: Solver | None = None) -> float:
+    """Largest epsilon_final on the doubling grid from 1/(n+1) for which the scaled
+    auction still returns the exact objective (bench.cpp:310-326)."""
+    c = np.asarray(cost, dtype=np.int64)
+    N = float(max(int(c.max()) if c.size else 0, 1))
+    eps = 1.0 / (c.shape[0] + 1)
+    best = 0.0
+    while eps <= N:
+        r = solve_auction_scaled(c, epsilon_final=eps, solver=solver)
+        if not r.converged or round(r.objective) != exact_int:
+            break
+        best = eps
+        eps *= 2.0
+    if best == 0.0:
+        raise RuntimeError("auction calibration failed at epsilon = 1/(n+1)")
+    return best
 
 
 def _range_error(who: str):

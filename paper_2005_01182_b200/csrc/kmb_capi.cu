@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "kmb.h"
 #include "kmb_internal.h"
@@ -83,6 +84,8 @@ struct kmb_context {
   DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus, b16, brmin, bimin, bimax;
   // cost construction workspace (host-resident points / output)
   DevBuf pa, pb, pout, pbad;
+  // auction workspace
+  DevBuf aprice, ar2c, atot, abids, acomp, aeps, amin, amax;
   // column-sharded solve: the collective (NCCL or caller callbacks)
   std::unique_ptr<kmb::Exchange> exchange;
   // chunked host-input pipeline of the batch engines
@@ -133,7 +136,8 @@ void kmb_destroy(kmb_context* c) {
   for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
                     &c->obj, &c->bcost, &c->bpad, &c->b16, &c->brmin, &c->bimin, &c->bimax, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
-                    &c->bstatus, &c->pa, &c->pb, &c->pout, &c->pbad})
+                    &c->bstatus, &c->pa, &c->pb, &c->pout, &c->pbad, &c->aprice, &c->ar2c, &c->atot,
+                    &c->abids, &c->acomp, &c->aeps, &c->amin, &c->amax})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -511,6 +515,95 @@ int kmb_last_instance_stats(kmb_context* c, int64_t* out, int64_t capacity, int6
   const int64_t k = capacity < have ? capacity : have;
   *count = have / kmb::KMB_ISTATS;
   if (k > 0) KMB_CUDA(cudaMemcpy(out, c->bstat.p, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost));
+  return KMB_OK;
+}
+
+int kmb_auction_i32(kmb_context* c, const int32_t* costs, int32_t batch, int32_t n,
+                    const kmb_auction_config* cfg, double* prices, int32_t* row_to_col,
+                    int64_t* total_cost, int64_t* bids, int32_t* converged,
+                    double* epsilon_last, double* seconds) {
+  if (!c) return fail(KMB_EINVAL, "kmb_auction_i32: NULL context");
+  if (!cfg) return fail(KMB_EINVAL, "kmb_auction_i32: NULL config");
+  const char* who = cfg->scaled ? "solve_auction_scaled" : "solve_auction";
+  if (batch <= 0 || n <= 0 || !costs) return fail(KMB_EINVAL, std::string(who) + ": bad arguments");
+  // auction.cpp:190-191, 205-206
+  if (!cfg->scaled && !(cfg->epsilon > 0.0))
+    return fail(KMB_EINVAL, "solve_auction: epsilon must be positive");
+  if (cfg->scaled && !(cfg->theta > 1.0))
+    return fail(KMB_EINVAL, "solve_auction_scaled: theta must exceed 1");
+  if (n > kmb::auction_max_n())
+    return fail(KMB_EINVAL, std::string(who) + ": n > " + std::to_string(kmb::auction_max_n()) +
+                                " (prices and owners must fit in shared memory)");
+  KMB_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const size_t nb = static_cast<size_t>(batch) * n;
+  const int32_t* dcost = costs;
+  KMB_CUDA(cudaEventRecord(c->ev0, st));
+  if (!is_device_ptr(costs)) {
+    KMB_CUDA(c->bcost.ensure(nb * n * 4));
+    KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, nb * n * 4, cudaMemcpyHostToDevice, st));
+    dcost = c->bcost.as<int32_t>();
+  }
+  auto dev = [&](void* user, DevBuf& buf, size_t bytes, void** out) -> cudaError_t {
+    if (user && is_device_ptr(user)) {
+      *out = user;
+      return cudaSuccess;
+    }
+    *out = nullptr;
+    if (!user) return cudaSuccess;
+    cudaError_t e = buf.ensure(bytes);
+    *out = buf.p;
+    return e;
+  };
+  void *dp, *dr, *dt, *db, *dc, *de;
+  KMB_CUDA(dev(prices, c->aprice, nb * 8, &dp));
+  KMB_CUDA(dev(row_to_col, c->ar2c, nb * 4, &dr));
+  KMB_CUDA(dev(total_cost, c->atot, batch * 8, &dt));
+  KMB_CUDA(dev(bids, c->abids, batch * 8, &db));
+  KMB_CUDA(dev(converged, c->acomp, batch * 4, &dc));
+  KMB_CUDA(dev(epsilon_last, c->aeps, batch * 8, &de));
+  KMB_CUDA(c->amin.ensure(batch * 8));
+  KMB_CUDA(c->amax.ensure(batch * 8));
+  KMB_CUDA(c->bstatus.ensure(batch * 4));
+  kmb::AuctionArgs a{};
+  a.C = dcost;
+  a.ld = n;
+  a.inst_stride = static_cast<int64_t>(n) * n;
+  a.batch = batch;
+  a.n = n;
+  a.scaled = cfg->scaled ? 1 : 0;
+  a.eps0 = cfg->epsilon;
+  a.theta = cfg->theta;
+  a.eps_final = cfg->epsilon_final;
+  a.max_bids = cfg->max_bids;
+  a.budget_ns = cfg->time_budget_s > 0.0 ? static_cast<int64_t>(cfg->time_budget_s * 1e9) : 0;
+  a.cmin = c->amin.as<long long>();
+  a.cmax = c->amax.as<long long>();
+  a.prices = static_cast<double*>(dp);
+  a.row_to_col = static_cast<int32_t*>(dr);
+  a.total_cost = static_cast<int64_t*>(dt);
+  a.bids = static_cast<int64_t*>(db);
+  a.complete = static_cast<int32_t*>(dc);
+  a.eps_last = static_cast<double*>(de);
+  a.status = c->bstatus.as<int32_t>();
+  KMB_CUDA(kmb::launch_auction(a, c->sm_count, st));
+  KMB_CUDA(cudaEventRecord(c->ev1, st));
+  if (dp != prices) { int r = copy_out(prices, dp, nb * 8, st); if (r) return r; }
+  if (dr != row_to_col) { int r = copy_out(row_to_col, dr, nb * 4, st); if (r) return r; }
+  if (dt != total_cost) { int r = copy_out(total_cost, dt, batch * 8, st); if (r) return r; }
+  if (db != bids) { int r = copy_out(bids, db, batch * 8, st); if (r) return r; }
+  if (dc != converged) { int r = copy_out(converged, dc, batch * 4, st); if (r) return r; }
+  if (de != epsilon_last) { int r = copy_out(epsilon_last, de, batch * 8, st); if (r) return r; }
+  std::vector<int32_t> hs(batch);
+  KMB_CUDA(cudaMemcpyAsync(hs.data(), c->bstatus.p, batch * 4, cudaMemcpyDeviceToHost, st));
+  KMB_CUDA(cudaStreamSynchronize(st));
+  if (seconds) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    *seconds = ms * 1e-3;
+  }
+  for (int32_t b = 0; b < batch; ++b)
+    if (hs[b]) return status_message(hs[b], who);
   return KMB_OK;
 }
 

@@ -116,6 +116,27 @@ cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_
 int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)
 cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int warps_per_sm,
                               cudaStream_t st, int* grid_out);
+// Gauss-Seidel auction (kmb_auction.cu)
+struct AuctionArgs {
+  const int32_t* C;     // batch instances, row stride ld, instance stride inst_stride
+  int64_t ld, inst_stride;
+  int32_t batch, n;
+  int32_t scaled;       // 0: solve_auction (eps0 = epsilon); 1: solve_auction_scaled
+  double eps0, theta, eps_final;
+  int64_t max_bids;
+  int64_t budget_ns;    // 0: no time budget
+  long long *cmin, *cmax;  // batch: workspace (validation, max_cost)
+  double* prices;       // batch x n (may be null)
+  int32_t* row_to_col;  // batch x n (may be null)
+  int64_t* total_cost;  // batch (may be null)
+  int64_t* bids;        // batch (may be null)
+  int32_t* complete;    // batch (may be null)
+  double* eps_last;     // batch (may be null)
+  int32_t* status;      // batch
+};
+size_t auction_smem_bytes(int n);
+int auction_max_n();
+cudaError_t launch_auction(const AuctionArgs& a, int sm_count, cudaStream_t st);
 // cost construction (kmb_costs.cu)
 template <typename P>
 cudaError_t launch_costs(const P* a, const P* b, int32_t batch, int32_t n, int32_t m, int32_t dim,
