@@ -6,6 +6,10 @@
 //
 //   solve_km_b200          == ot::solve_km          (hungarian.hpp:39-40)
 //   solve_batched_km_b200  == ot::solve_batched_km  (hungarian.hpp:53-56)
+//   solve_auction_b200        == ot::solve_auction        (auction.hpp:30-32)
+//   solve_auction_scaled_b200 == ot::solve_auction_scaled (auction.hpp:48-50)
+//     (declared when "ot/auction.hpp" is included first; bit-identical prices,
+//      bids and assignment; costs must fit int32)
 //
 // Same inputs (OTInstance), same outputs (SolveResult built with the
 // reference's own make_result, optional DualPotentials / Matching /
@@ -150,6 +154,59 @@ inline SolveResult solve_batched_km_b200(const OTInstance& inst, const BatchedKM
   res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return res;
 }
+
+#ifdef OT_AUCTION_HPP
+namespace kmb_detail {
+inline SolveResult auction(const OTInstance& inst, const kmb_auction_config& cfg, const char* who,
+                           std::vector<double>* prices_out, Matching* matching_out) {
+  require_unit_square(inst, who);  // require_auctionable (auction.cpp:181-188)
+  const auto t0 = std::chrono::steady_clock::now();
+  const int32_t n = inst.n;
+  std::vector<int32_t> c(inst.cost.size());
+  for (size_t k = 0; k < c.size(); ++k) {
+    if (inst.cost[k] > std::numeric_limits<int32_t>::max())
+      throw std::invalid_argument(std::string(who) + ": cost exceeds the device range [0, 2^31)");
+    c[k] = static_cast<int32_t>(inst.cost[k]);
+  }
+  std::vector<double> prices(n);
+  std::vector<int32_t> r2c(n, -1);
+  int64_t total = 0, bids = 0;
+  int32_t converged = 0;
+  double eps = 0.0;
+  check(kmb_auction_i32(context(), c.data(), 1, n, &cfg, prices.data(), r2c.data(), &total, &bids,
+                        &converged, &eps, nullptr),
+        who);
+  const bool complete = converged != 0;
+  // finish (auction.cpp:161-179)
+  SolveResult res = make_result(inst, matching_flow(n, r2c), bids,
+                                /*exact=*/complete && eps * n < 1.0, complete);
+  res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (prices_out) *prices_out = std::move(prices);
+  if (matching_out) matching_out->row_to_col = std::move(r2c);
+  return res;
+}
+}  // namespace kmb_detail
+
+inline SolveResult solve_auction_b200(const OTInstance& inst, const AuctionConfig& config,
+                                      std::vector<double>* prices_out = nullptr,
+                                      Matching* matching_out = nullptr) {
+  kmb_detail::require_unit_square(inst, "solve_auction");
+  if (!(config.epsilon > 0.0)) throw std::invalid_argument("solve_auction: epsilon must be positive");
+  const kmb_auction_config cfg{0, config.epsilon, 4.0, 0.0, config.max_bids, config.time_budget_s};
+  return kmb_detail::auction(inst, cfg, "solve_auction", prices_out, matching_out);
+}
+
+inline SolveResult solve_auction_scaled_b200(const OTInstance& inst,
+                                             const AuctionScaledConfig& config = {},
+                                             std::vector<double>* prices_out = nullptr) {
+  kmb_detail::require_unit_square(inst, "solve_auction_scaled");
+  if (!(config.theta > 1.0))
+    throw std::invalid_argument("solve_auction_scaled: theta must exceed 1");
+  const kmb_auction_config cfg{1, config.epsilon0, config.theta, config.epsilon_final,
+                               config.max_bids, config.time_budget_s};
+  return kmb_detail::auction(inst, cfg, "solve_auction_scaled", prices_out, nullptr);
+}
+#endif  // OT_AUCTION_HPP
 
 }  // namespace ot
 

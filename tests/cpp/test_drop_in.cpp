@@ -4,10 +4,12 @@
 // the duals.  Built by tests/cpp/build.sh (needs /root/reference headers), run
 // on the GPU by tests/test_cpp_drop_in.py.
 #include <cstdio>
+#include <cstring>
 #include <random>
 #include <stdexcept>
 #include <string>
 
+#include "ot/auction.hpp"
 #include "ot/core.hpp"
 #include "ot/hungarian.hpp"
 #include "kmb_ot.hpp"
@@ -183,6 +185,70 @@ int main() {
     std::string a;
     try { solve_batched_km_b200(unit_2x2(), cfg); } catch (const std::invalid_argument& e) { a = e.what(); }
     CHECK(a == "quantize_costs: B must be positive");
+  }
+  // ---- auction (test_auction.cpp cases; bit-identical prices vs the reference)
+  auto same_bits = [](const std::vector<double>& a, const std::vector<double>& b) {
+    if (a.size() != b.size()) return false;
+    for (size_t k = 0; k < a.size(); ++k)
+      if (std::memcmp(&a[k], &b[k], sizeof(double)) != 0) return false;
+    return true;
+  };
+  {  // small epsilon is exact on the 2x2
+    AuctionConfig cfg;
+    cfg.epsilon = 0.4;
+    const SolveResult res = solve_auction_b200(unit_2x2(), cfg);
+    CHECK(res.objective == 2.0 && res.exact && res.converged);
+  }
+  {  // epsilon-CS instances (seed 41) and random eps: same prices, bids, matching
+    std::mt19937 rng(41);
+    for (double eps : {0.5, 2.5, 10.0}) {
+      const OTInstance inst = random_unit_instance(rng, 30, 100);
+      AuctionConfig cfg;
+      cfg.epsilon = eps;
+      std::vector<double> pa, pb;
+      Matching ma, mb;
+      const SolveResult a = solve_auction_b200(inst, cfg, &pa, &ma);
+      const SolveResult b = solve_auction(inst, cfg, &pb, &mb);
+      CHECK(same_bits(pa, pb));
+      CHECK(ma.row_to_col == mb.row_to_col);
+      CHECK(a.iterations == b.iterations && a.objective == b.objective);
+      CHECK(a.exact == b.exact && a.converged == b.converged);
+    }
+  }
+  {  // scaled auction: default schedule exact, matches the reference (seed 61)
+    std::mt19937 rng(61);
+    for (int t = 0; t < 20; ++t) {
+      const OTInstance inst = random_unit_instance(rng, 25, 800);
+      std::vector<double> pa, pb;
+      const SolveResult a = solve_auction_scaled_b200(inst, {}, &pa);
+      const SolveResult b = solve_auction_scaled(inst, {}, &pb);
+      CHECK(a.converged && a.exact);
+      CHECK(same_bits(pa, pb) && a.iterations == b.iterations && a.objective == b.objective);
+    }
+  }
+  {  // bid budget produces a flagged result (seed 59)
+    std::mt19937 rng(59);
+    const OTInstance inst = random_unit_instance(rng, 40, 1000);
+    AuctionConfig cfg;
+    cfg.epsilon = 0.1;
+    cfg.max_bids = 5;
+    const SolveResult res = solve_auction_b200(inst, cfg);
+    CHECK(!res.converged && !res.exact && res.iterations == 5);
+  }
+  {  // epsilon must be positive; theta must exceed 1 — same messages
+    AuctionConfig cfg;
+    cfg.epsilon = 0.0;
+    std::string a, b;
+    try { solve_auction_b200(unit_2x2(), cfg); } catch (const std::invalid_argument& e) { a = e.what(); }
+    try { solve_auction(unit_2x2(), cfg); } catch (const std::invalid_argument& e) { b = e.what(); }
+    CHECK(!a.empty() && a == b);
+    AuctionScaledConfig sc;
+    sc.theta = 1.0;
+    a.clear();
+    b.clear();
+    try { solve_auction_scaled_b200(unit_2x2(), sc); } catch (const std::invalid_argument& e) { a = e.what(); }
+    try { solve_auction_scaled(unit_2x2(), sc); } catch (const std::invalid_argument& e) { b = e.what(); }
+    CHECK(!a.empty() && a == b);
   }
   std::printf("drop-in: %d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;

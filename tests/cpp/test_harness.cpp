@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "ot/auction.hpp"
 #include "ot/bench.hpp"
 #include "ot/core.hpp"
 #include "ot/datasets.hpp"
@@ -49,6 +50,33 @@ static SolverSpec batched_km_b200_spec(int64_t B) {
     cfg.B = B;
     cfg.time_budget_s = budget;
     return solve_batched_km_b200(inst, cfg);
+  };
+  return s;
+}
+
+static SolverSpec auction_b200_spec(double eps) {  // mirrors make_solver("auction"), bench.cpp:423-435
+  SolverSpec s;
+  s.name = "auction_b200";
+  s.params = "epsilon=" + std::to_string(eps);
+  s.unit_only = true;
+  s.run = [eps](const OTInstance& inst, double budget) {
+    AuctionConfig cfg;
+    cfg.epsilon = eps;
+    cfg.time_budget_s = budget;
+    return solve_auction_b200(inst, cfg);
+  };
+  return s;
+}
+
+static SolverSpec auction_scaled_b200_spec() {  // mirrors make_solver("auction_scaled"), :436-448
+  SolverSpec s;
+  s.name = "auction_scaled_b200";
+  s.params = "epsilon_final=exact";
+  s.unit_only = true;
+  s.run = [](const OTInstance& inst, double budget) {
+    AuctionScaledConfig cfg;
+    cfg.time_budget_s = budget;
+    return solve_auction_scaled_b200(inst, cfg);
   };
   return s;
 }
@@ -111,6 +139,22 @@ int main() {
     std::printf("calibrated B: reference %lld, b200 %lld\n", static_cast<long long>(Bref),
                 static_cast<long long>(Bgpu));
     CHECK(Bref == Bgpu);
+  }
+  // auction specs next to the reference's (uncalibrated: epsilon = 1 / exact schedule)
+  for (const OTInstance& inst : insts) {
+    const std::vector<SolverSpec> roster = {make_solver("auction"), auction_b200_spec(1.0),
+                                            make_solver("auction_scaled"), auction_scaled_b200_spec()};
+    const std::vector<BenchRecord> recs = run_suite({inst}, roster, cfg);
+    CHECK(recs.size() == 4);
+    for (const BenchRecord& r : recs) {
+      std::printf("%-8s %-20s %-22s obj=%.0f exact=%.0f ratio=%.6f t=%.4fs conv=%d\n",
+                  r.instance.c_str(), r.solver.c_str(), r.params.c_str(), r.objective,
+                  r.exact_objective, r.ratio, r.wall_seconds, r.converged ? 1 : 0);
+      CHECK(r.applicable && r.converged);
+    }
+    CHECK(recs[0].objective == recs[1].objective);  // same bids -> same matching
+    CHECK(recs[2].objective == recs[2].exact_objective);
+    CHECK(recs[3].objective == recs[3].exact_objective);
   }
   std::printf("harness: %d failed\n", g_fail);
   return g_fail ? 1 : 0;
