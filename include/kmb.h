@@ -79,7 +79,7 @@ typedef struct kmb_stats {
   int64_t phases;          /* augmentation phases (not a parity target)      */
   int64_t dual_steps;      /* dual adjustments: equals the reference's count */
   int64_t rows_scanned;    /* cost rows streamed by the reduced-cost scan    */
-  int64_t cost_bytes_read; /* 4*n*(rows_scanned + n) (+ reductions)          */
+  int64_t cost_bytes_read; /* 4*n*(rows_scanned + n) + 16*segment_rows       */
   double seconds;          /* device time of the solve (CUDA events)         */
   int32_t converged;       /* 0 when the time budget expired                 */
   int32_t engine;          /* the engine that ran (KMB_OPT_ENGINE numbering) */
@@ -91,6 +91,9 @@ typedef struct kmb_stats {
                               with -DKMB_WARP_STAGE_CLOCKS=1)                */
   int64_t max_instance_cycles; /* batch engines: slowest instance (SM clocks) */
   int64_t sum_instance_cycles; /* batch engines: sum over instances          */
+  int64_t segment_rows;    /* grid/cluster engines: (row, 4-column segment)
+                              pairs of the epoch-start dirty-segment relaxes
+                              (16 B each; rows_scanned counts full rows)     */
 } kmb_stats;
 
 typedef struct kmb_context kmb_context;

@@ -206,8 +206,10 @@ int kmm_solve_incr(const int32_t* C, int32_t n, int32_t seed, int64_t* u, int64_
   int32_t* rows = malloc(sizeof(int32_t) * (size_t)n);  /* reached rows */
   int32_t* nxt_rows = malloc(sizeof(int32_t) * (size_t)n);
   int32_t* found = malloc(sizeof(int32_t) * (size_t)n);
+  char* dmask = malloc((size_t)n);
+  int dirty_only = 0;
   if (!match_col || !key || !w || !dc || !rcol || !rrow || !tree_par || !root_row || !claim ||
-      !claim_col || !rows || !nxt_rows || !found)
+      !claim_col || !rows || !nxt_rows || !found || !dmask)
     return -1;
   for (int32_t i = 0; i < n; ++i) {
     match_row[i] = match_col[i] = -1;
@@ -239,15 +241,21 @@ int kmm_solve_incr(const int32_t* C, int32_t n, int32_t seed, int64_t* u, int64_
   int rc = 0;
   while (nfree > 0) {
     ++rounds;
+    /* epoch start: the survivors only over the dirty columns (keys reset at
+     * the epoch end); every other unreached key is attained at a survivor */
+    if (dirty_only)
+      for (int32_t j = 0; j < n; ++j) dmask[j] = key[j] == UINT64_MAX && !rcol[j];
     for (int32_t r = head; r < nrows; ++r) {
       const int32_t i = rows[r];
       const int32_t* row = C + (size_t)i * n;
       for (int32_t j = 0; j < n; ++j) {
+        if (dirty_only && !dmask[j]) continue;
         const uint64_t k = pack_key((int64_t)row[j] - w[i], i);
         if (k < key[j]) key[j] = k;
       }
     }
-    rows_scanned += nrows - head;
+    if (!dirty_only) rows_scanned += nrows - head;
+    dirty_only = 0;
     head = nrows;
     if (first) {
       for (int32_t j = 0; j < n; ++j) v[j] = key_val(key[j]);
@@ -292,6 +300,17 @@ int kmm_solve_incr(const int32_t* C, int32_t n, int32_t seed, int64_t* u, int64_
       }
     }
     if (!nfound) continue;
+    /* ---- epoch end: relax the rows appended this round over all columns
+     * (the epoch-start re-relax covers dirty columns only), then dissolve ---- */
+    for (int32_t r = head; r < nrows; ++r) {
+      const int32_t i = rows[r];
+      const int32_t* row = C + (size_t)i * n;
+      for (int32_t j = 0; j < n; ++j) {
+        const uint64_t k = pack_key((int64_t)row[j] - w[i], i);
+        if (k < key[j]) key[j] = k;
+      }
+    }
+    rows_scanned += nrows - head;
     /* ---- epoch end: dissolve claimed trees ---- */
     for (int32_t j = 0; j < n; ++j) {
       if (rcol[j]) {
@@ -331,6 +350,7 @@ int kmm_solve_incr(const int32_t* C, int32_t n, int32_t seed, int64_t* u, int64_
     memcpy(rows, nxt_rows, sizeof(int32_t) * (size_t)ns);
     nrows = ns;
     head = 0; /* survivors relax once more for the reset columns */
+    dirty_only = 1;
     ++epochs;
   }
   {
@@ -345,5 +365,6 @@ int kmm_solve_incr(const int32_t* C, int32_t n, int32_t seed, int64_t* u, int64_
 done:
   free(match_col); free(key); free(w); free(dc); free(rcol); free(rrow); free(tree_par);
   free(root_row); free(claim); free(claim_col); free(rows); free(nxt_rows); free(found);
+  free(dmask);
   return rc;
 }

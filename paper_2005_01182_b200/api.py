@@ -48,7 +48,7 @@ class Stats(C.Structure):
                 ("cost_bytes_read", C.c_int64), ("seconds", C.c_double),
                 ("converged", C.c_int32), ("engine", C.c_int32), ("rounds", C.c_int64),
                 ("stage_ns", C.c_int64 * 6), ("max_instance_cycles", C.c_int64),
-                ("sum_instance_cycles", C.c_int64)]
+                ("sum_instance_cycles", C.c_int64), ("segment_rows", C.c_int64)]
 
 
 class AuctionConfig(C.Structure):

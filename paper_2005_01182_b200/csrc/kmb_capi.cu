@@ -496,7 +496,9 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
     stats->phases = h.phases;
     stats->dual_steps = h.dual_steps;
     stats->rows_scanned = h.rows_scanned;
-    stats->cost_bytes_read = 4ll * n * (h.rows_scanned + (seed == KMB_SEED_BATCHED ? n : 0));
+    stats->segment_rows = h.seg_rows;
+    stats->cost_bytes_read =
+        4ll * n * (h.rows_scanned + (seed == KMB_SEED_BATCHED ? n : 0)) + 16ll * h.seg_rows;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     stats->seconds = ms * 1e-3;

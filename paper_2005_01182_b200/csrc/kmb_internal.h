@@ -35,6 +35,7 @@ struct Ctrl {
   int64_t rows_scanned;
   int64_t rounds;
   int64_t stage_ns[6];
+  int64_t seg_rows;  // (row, 4-column segment) pairs of the dirty-only epoch-start relaxes
 };
 
 struct SolverArgs {

@@ -42,6 +42,13 @@
 #include "kmb_common.cuh"
 #include "kmb_internal.h"
 
+#ifndef KMB_SOLVER_FINE
+#define KMB_SOLVER_FINE 0
+#endif
+#if KMB_SOLVER_FINE
+#include <cstdio>
+#endif
+
 namespace kmb {
 
 constexpr int kThreads = 512;
@@ -51,6 +58,7 @@ struct SlabSmem {
   int64_t part[kThreads / 32];
   int64_t m;
   int32_t append_base;
+  int32_t ndseg;  // dirty segments after an epoch end (-1: relax everything)
 };
 
 // ---- K1: row reductions + engine state init (hungarian.cpp:323-327) -------
@@ -168,12 +176,85 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
   }
 }
 
+// ---- K3': the epoch-start relax restricted to the slab's dirty segments -------
+// After an epoch's trees are dissolved, only columns whose key was reset (their
+// argmin row left, or they were reached inside a dissolved tree) can change when
+// the surviving rows are relaxed again: every other unreached key is a minimum
+// attained at a surviving row.  So the survivors are relaxed over
+// the dirty 4-column segments only — the same keys as a full relax, at a few
+// percent of the bytes (c5: ~94% of all relaxed rows are these re-relaxes).
+// segs[0, nd) lists the dirty segments; thread (g, k) handles segs[k] for row
+// group g, with k in [0, np2), np2 = nd rounded up to a power of two (lanes of
+// the same k differ only in high lane bits, so a xor tree merges them).
+__device__ __forceinline__ void relax_sel(const SolverArgs& a, const int32_t* list,
+                                          const int64_t* listw, int head, int tail, int c0,
+                                          const int32_t* segs, int nd, uint64_t* skey) {
+  int np2 = 1;
+  while (np2 < nd) np2 <<= 1;
+  const int R = kThreads / np2;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int k = tid % np2, g = tid / np2;
+  uint64_t best0 = KMB_KEY_INF, best1 = KMB_KEY_INF, best2 = KMB_KEY_INF, best3 = KMB_KEY_INF;
+  const int sg = k < nd ? segs[k] : 0;
+  if (k < nd) {
+    const int32_t* base = a.C + c0 + 4 * sg;
+    int r = head + g;
+    for (; r + (kRelaxBatch - 1) * R < tail; r += kRelaxBatch * R) {
+      int i[kRelaxBatch];
+      uint32_t b[kRelaxBatch];
+      int4 c[kRelaxBatch];
+#pragma unroll
+      for (int q = 0; q < kRelaxBatch; ++q) {
+        i[q] = ldcg(list + r + q * R);
+        b[q] = row_bias(ldcg(listw + r + q * R));
+      }
+#pragma unroll
+      for (int q = 0; q < kRelaxBatch; ++q)
+        c[q] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[q]) * a.pitch));
+#pragma unroll
+      for (int q = 0; q < kRelaxBatch; ++q) {
+        best0 = umin64(best0, pack_key(static_cast<uint32_t>(c[q].x) + b[q], i[q]));
+        best1 = umin64(best1, pack_key(static_cast<uint32_t>(c[q].y) + b[q], i[q]));
+        best2 = umin64(best2, pack_key(static_cast<uint32_t>(c[q].z) + b[q], i[q]));
+        best3 = umin64(best3, pack_key(static_cast<uint32_t>(c[q].w) + b[q], i[q]));
+      }
+    }
+    for (; r < tail; r += R) {
+      const int i = ldcg(list + r);
+      const uint32_t b = row_bias(ldcg(listw + r));
+      const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * a.pitch));
+      best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
+      best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
+      best2 = umin64(best2, pack_key(static_cast<uint32_t>(c.z) + b, i));
+      best3 = umin64(best3, pack_key(static_cast<uint32_t>(c.w) + b, i));
+    }
+  }
+  if (np2 < 32) {
+    for (int o = np2; o < 32; o <<= 1) {
+      best0 = umin64(best0, __shfl_xor_sync(0xffffffffu, best0, o));
+      best1 = umin64(best1, __shfl_xor_sync(0xffffffffu, best1, o));
+      best2 = umin64(best2, __shfl_xor_sync(0xffffffffu, best2, o));
+      best3 = umin64(best3, __shfl_xor_sync(0xffffffffu, best3, o));
+    }
+  }
+  const bool writer = k < nd && (np2 >= 32 || lane < np2);
+  if (writer && best0 != KMB_KEY_INF) {
+    unsigned long long* k4 = reinterpret_cast<unsigned long long*>(skey + 4 * sg);
+    atomicMin(k4 + 0, best0);
+    atomicMin(k4 + 1, best1);
+    atomicMin(k4 + 2, best2);
+    atomicMin(k4 + 3, best3);
+  }
+}
+
 // ---- the persistent engine ---------------------------------------------------
 // Incremental epochs (CPU mirror kmm_solve_incr): the search is
 // never restarted.  When a round absorbs free columns, the trees owning one are
 // augmented and dissolved (their rows/columns finalised and un-reached), columns
-// whose argmin row left are reset, the surviving rows are relaxed once more, and
-// the search goes on at the same D.
+// whose argmin row left are reset, the surviving rows are relaxed once more over
+// the reset ("dirty") columns only — the rows appended in the epoch's last round
+// having been relaxed over the whole slab first — and the search goes on at the
+// same D.
 template <class Barrier>
 __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -182,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   int64_t* vloc = reinterpret_cast<int64_t*>(skey + W);
   int64_t* dcol = vloc + W;
   unsigned char* rch = reinterpret_cast<unsigned char*>(dcol + W);
+  int32_t* dsegs = reinterpret_cast<int32_t*>(rch + W);  // dirty segments (W/4)
   __shared__ SlabSmem sm;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -200,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     rch[c] = (c0 + c < a.n) ? 0 : 1;  // padding columns never count
   }
   __syncthreads();
-  int64_t dual_steps = 0, rows_scanned = 0;
+  int64_t dual_steps = 0, rows_scanned = 0, seg_rows = 0;
   // stage clock (leader only): 0 relax + absorb + local min, 1 B1, 2 dual-step absorb,
   // 3 B2 (dual steps only), 4 epoch end, 5 B3
   long long prof[6] = {0, 0, 0, 0, 0, 0};
@@ -235,12 +317,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   int p = 0, epoch = 0, head = 0, tail = a.n;  // rows list[p][0, tail) are reached
   int nfound = 0;                              // free columns absorbed this epoch
   bool fatal = false, stopped = false;
+  bool dirty_round = false;  // this round re-relaxes survivors over dirty segments only
+  if (tid == 0) sm.ndseg = 0;
+#if KMB_SOLVER_FINE
+  long long fine[4] = {0, 0, 0, 0};  // leader: relax issue->done, sync, absorb, min
+  long long fl = clock64();
+#define KMB_FINE(k)                    \
+  do {                                 \
+    if (leader) {                      \
+      const long long t_ = clock64();  \
+      fine[k] += t_ - fl;              \
+      fl = t_;                         \
+    }                                  \
+  } while (0)
+#else
+#define KMB_FINE(k) (void)0
+#endif
   for (;;) {
     const int32_t* list = a.list_row[p];
     const int64_t* listw = a.list_w[p];
-    relax_slab(a, list, listw, head, tail, c0, W, skey);
-    rows_scanned += tail - head;
+    KMB_FINE(3);
+    if (dirty_round) {
+      dirty_round = false;
+      if (sm.ndseg > 0) relax_sel(a, list, listw, head, tail, c0, dsegs, sm.ndseg, skey);
+      seg_rows += static_cast<int64_t>(tail - head) * sm.ndseg;
+    } else {
+      relax_slab(a, list, listw, head, tail, c0, W, skey);
+      rows_scanned += tail - head;
+    }
+    KMB_FINE(0);
     __syncthreads();
+    KMB_FINE(1);
     if (rounds_total == 0 && a.seed == 1)  // column reduction, hungarian.cpp:328-333
       for (int c = tid; c < W; c += kThreads)
         if (c0 + c < a.n) vloc[c] = key_val(skey[c]);
@@ -294,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     };
     absorb_at(D);
     __syncthreads();
+    KMB_FINE(2);
     // min slack' of the columns still unreached: only used if no CTA progressed
     int64_t lm = KMB_I64_INF;
     for (int c = tid; c < W; c += kThreads)
@@ -347,6 +455,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     if (nfound == 0) continue;
 
     // ---- epoch end: augment and dissolve the trees that reached a free column ----
+    // First relax the rows appended this round over the whole slab (the next
+    // round re-relaxes survivors over dirty segments only, so every survivor
+    // must already be in the keys); a key whose argmin is one of them that gets
+    // dissolved is reset below like any other.
+    relax_slab(a, list, listw, head, tail, c0, W, skey);
+    rows_scanned += tail - head;
+    __syncthreads();
     // columns of the slab: finalise dissolved ones, reset keys whose argmin row leaves
     for (int c = tid; c < W; c += kThreads) {
       const int col = c0 + c;
@@ -362,6 +477,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
         const int32_t root = ldcg(a.root_row + key_row(skey[c]));
         if (claimed_in(ldcg(a.claim + root), epoch)) skey[c] = KMB_KEY_INF;
       }
+    }
+    // dirty segments: 4-column groups holding an unreached column whose key
+    // was just reset (only those change when the survivors are relaxed again)
+    __syncthreads();
+    if (tid == 0) sm.ndseg = 0;
+    __syncthreads();
+    for (int sgi = tid; sgi < (W >> 2); sgi += kThreads) {
+      bool d = false;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = 4 * sgi + q;
+        d |= !rch[c] && skey[c] == KMB_KEY_INF;
+      }
+      if (d) dsegs[atomicAdd(&sm.ndseg, 1)] = sgi;
     }
     // rows: finalise dissolved ones (u = w + D), carry the survivors over
     int* sc = &ctrl->rcnt[(kb + 1) % 3];
@@ -405,6 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     ++epoch;
     head = 0;
     tail = ldcg(&ctrl->rcnt[kb % 3]);  // survivors
+    dirty_round = true;
     nfound = 0;
     if (ldcg(&ctrl->matched) == a.n) break;
     if (ldcg(&ctrl->stop) != 0) {
@@ -423,6 +553,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   (void)fatal;
   for (int c = tid; c < W; c += kThreads)
     if (c0 + c < a.n) a.v[c0 + c] = vloc[c];
+#if KMB_SOLVER_FINE
+  if (leader)
+    printf("k_solve leader fine (cycles/round over %lld rounds): relax %lld, sync %lld, absorb %lld, other %lld\n",
+           rounds_total, fine[0] / rounds_total, fine[1] / rounds_total, fine[2] / rounds_total,
+           fine[3] / rounds_total);
+#endif
+  if (tid == 0 && seg_rows)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl->seg_rows),
+              static_cast<unsigned long long>(seg_rows));
   if (leader) {
     ctrl->free_rows = a.n - ldcg(&ctrl->matched);
     ctrl->dual_steps = dual_steps;
@@ -473,7 +612,7 @@ __global__ void k_objective(const int32_t* C, int64_t pitch, int n, const int32_
   if ((threadIdx.x & 31) == 0) atomicAdd(out, static_cast<unsigned long long>(s));
 }
 
-size_t solver_smem_bytes(int W) { return static_cast<size_t>(W) * (8 + 8 + 8 + 1) + 16; }
+size_t solver_smem_bytes(int W) { return static_cast<size_t>(W) * (8 + 8 + 8 + 1 + 1) + 16; }
 
 cudaError_t launch_solver_init(const SolverArgs& a, cudaStream_t st) {
   k_init_rows<<<256, 256, 0, st>>>(a);
