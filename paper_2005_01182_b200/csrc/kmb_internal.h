@@ -54,7 +54,7 @@ struct SolverArgs {
   int32_t* root_row;   // per row
   uint64_t* claim;     // per row, claim_key(phase, col)
   int32_t* list_row[2];
-  int64_t* list_w[2];
+  int64_t* list_w[2];  // the dual shift D at which each listed row was reached (w = u - D)
   int32_t* found;
   int64_t* partial;    // per CTA
   Ctrl* ctrl;

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
       else if (hi >= (1 << 29)) atomicMax(&a.ctrl->status, 3);  // KMB_ERANGE
       a.u[i] = u0;
       a.list_row[0][i] = i;
-      a.list_w[0][i] = u0;
+      a.list_w[0][i] = 0;  // reached at D = 0: w = u - 0
       a.root_row[i] = i;
       a.claim[i] = KMB_KEY_INF;
       a.match_row[i] = -1;
@@ -130,14 +130,17 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
         int i[kRelaxBatch];
         uint32_t b[kRelaxBatch];
         int4 c[kRelaxBatch];
+        int64_t dr[kRelaxBatch];
 #pragma unroll
         for (int k = 0; k < kRelaxBatch; ++k) {
           i[k] = ldcg(list + r + k * R);
-          b[k] = row_bias(ldcg(listw + r + k * R));
+          dr[k] = ldcg(listw + r + k * R);
         }
 #pragma unroll
-        for (int k = 0; k < kRelaxBatch; ++k)
+        for (int k = 0; k < kRelaxBatch; ++k) {
           c[k] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[k]) * a.pitch));
+          b[k] = row_bias(ldcg(a.u + i[k]) - dr[k]);  // w = u - D at reach
+        }
 #pragma unroll
         for (int k = 0; k < kRelaxBatch; ++k) {
           best0 = umin64(best0, pack_key(static_cast<uint32_t>(c[k].x) + b[k], i[k]));
@@ -148,8 +151,9 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
       }
       for (; r < tail; r += R) {
         const int i = ldcg(list + r);
-        const uint32_t b = row_bias(ldcg(listw + r));
+        const int64_t drr = ldcg(listw + r);
         const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * a.pitch));
+        const uint32_t b = row_bias(ldcg(a.u + i) - drr);
         best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
         best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
         best2 = umin64(best2, pack_key(static_cast<uint32_t>(c.z) + b, i));
@@ -203,14 +207,17 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const int32_t* li
       int i[kRelaxBatch];
       uint32_t b[kRelaxBatch];
       int4 c[kRelaxBatch];
+      int64_t dr[kRelaxBatch];
 #pragma unroll
       for (int q = 0; q < kRelaxBatch; ++q) {
         i[q] = ldcg(list + r + q * R);
-        b[q] = row_bias(ldcg(listw + r + q * R));
+        dr[q] = ldcg(listw + r + q * R);
       }
 #pragma unroll
-      for (int q = 0; q < kRelaxBatch; ++q)
+      for (int q = 0; q < kRelaxBatch; ++q) {
         c[q] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[q]) * a.pitch));
+        b[q] = row_bias(ldcg(a.u + i[q]) - dr[q]);
+      }
 #pragma unroll
       for (int q = 0; q < kRelaxBatch; ++q) {
         best0 = umin64(best0, pack_key(static_cast<uint32_t>(c[q].x) + b[q], i[q]));
@@ -221,8 +228,9 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const int32_t* li
     }
     for (; r < tail; r += R) {
       const int i = ldcg(list + r);
-      const uint32_t b = row_bias(ldcg(listw + r));
+      const int64_t drr = ldcg(listw + r);
       const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * a.pitch));
+      const uint32_t b = row_bias(ldcg(a.u + i) - drr);
       best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
       best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
       best2 = umin64(best2, pack_key(static_cast<uint32_t>(c.z) + b, i));
@@ -361,7 +369,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
         const int c = cb + tid;
         bool newrow = false, newfree = false;
         int32_t i2 = -1, col = c0 + c;
-        int64_t w2 = 0;
         if (c < W && !rch[c] && key_val(skey[c]) - vloc[c] == Dn) {
           rch[c] = 1;
           dcol[c] = Dn;
@@ -373,8 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
             newfree = true;
             atomicMin(reinterpret_cast<unsigned long long*>(a.claim + root), claim_key(epoch, col));
           } else {
-            newrow = true;
-            w2 = ldcg(a.u + i2) - Dn;
+            newrow = true;  // the list keeps D at reach; w = u - Dn is formed by the relax
             a.root_row[i2] = root;
           }
         }
@@ -387,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
           if (newrow) {
             const int pos = tail + base + __popc(rowmask & ((1u << lane) - 1));
             a.list_row[p][pos] = i2;
-            a.list_w[p][pos] = w2;
+            a.list_w[p][pos] = Dn;
           }
         }
         const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
@@ -496,13 +502,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     int* sc = &ctrl->rcnt[(kb + 1) % 3];
     for (int r = gtid; r < tail; r += gthreads) {
       const int32_t i = ldcg(list + r);
-      const int64_t w = ldcg(listw + r);
+      const int64_t dr = ldcg(listw + r);
       if (claimed_in(ldcg(a.claim + ldcg(a.root_row + i)), epoch)) {
-        a.u[i] = w + D;
+        // u = w + D.  (Another CTA's epoch-end relax of this row, if it was
+        // appended this round, may read u before or after this write: either
+        // way every key it could set has this dissolved row as argmin and is
+        // reset by that CTA's column pass.)
+        a.u[i] = ldcg(a.u + i) - dr + D;
       } else {
         const int pos = atomicAdd(sc, 1);
         a.list_row[p ^ 1][pos] = i;
-        a.list_w[p ^ 1][pos] = w;
+        a.list_w[p ^ 1][pos] = dr;
       }
     }
     // flip one parent-pointer path per claimed tree (its smallest free column)
@@ -545,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   if (stopped) {  // time budget: write back the surviving trees' lazy duals
     for (int r = gtid; r < tail; r += gthreads) {
       const int32_t i = ldcg(a.list_row[p] + r);
-      a.u[i] = ldcg(a.list_w[p] + r) + D;
+      a.u[i] = ldcg(a.u + i) - ldcg(a.list_w[p] + r) + D;
     }
     for (int c = tid; c < W; c += kThreads)
       if (rch[c] && c0 + c < a.n) vloc[c] -= D - dcol[c];
