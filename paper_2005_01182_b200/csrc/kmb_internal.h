@@ -45,6 +45,7 @@ struct SolverArgs {
   int32_t W;          // column slab per CTA (power of two >= 4); G*W >= n
   int32_t seed;       // 0: u = v = 0 (solve_km), 1: reductions (solve_batched_km)
   int32_t continue_bfs;
+  int32_t prefetch_rows;  // L2 bulk prefetch of appended rows (matrix larger than L2)
   unsigned long long deadline_ns;  // %globaltimer deadline, 0 = none
   int64_t* u;
   int64_t* v;

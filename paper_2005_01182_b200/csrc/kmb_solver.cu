@@ -45,6 +45,9 @@
 #ifndef KMB_SOLVER_FINE
 #define KMB_SOLVER_FINE 0
 #endif
+#ifndef KMB_SOLVER_PREFETCH  // L2 bulk prefetch of rows appended by the absorb
+#define KMB_SOLVER_PREFETCH 1
+#endif
 #if KMB_SOLVER_FINE
 #include <cstdio>
 #endif
@@ -382,6 +385,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
           } else {
             newrow = true;  // the list keeps D at reach; w = u - Dn is formed by the relax
             a.root_row[i2] = root;
+#if KMB_SOLVER_PREFETCH
+            // every CTA scans this row next round: start pulling it into L2 now,
+            // so the barrier and the list reads hide the DRAM latency
+            if (a.prefetch_rows)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.C + static_cast<int64_t>(i2) * a.pitch),
+                         "r"(static_cast<uint32_t>(a.pitch * 4))
+                         : "memory");
+#endif
           }
         }
         // warp-aggregated appends

@@ -36,8 +36,10 @@ def _llround(x: float) -> int:
     return int(r + 1) if x - r >= 0.5 else int(r)
 
 
-def circle_square(k: int, scale: float = 1e4) -> np.ndarray:
-    """gen_circle_square(k) cost matrix (datasets.cpp:57-112, :184-214)."""
+def circle_square_points(k: int) -> tuple[np.ndarray, np.ndarray]:
+    """gen_circle_square(k)'s two point clouds (datasets.cpp:57-112): the s x s
+    integer square centred at the origin and the k lattice points closest to
+    the origin ordered by (radius^2, angle)."""
     s = int(round(math.sqrt(k)))
     assert s * s == k
     off = (s - 1) // 2
@@ -57,6 +59,12 @@ def circle_square(k: int, scale: float = 1e4) -> np.ndarray:
                 cands.append((r2, a, x, y))
     cands.sort()
     circle = [(float(c[2]), float(c[3])) for c in cands[:k]]
+    return np.array(square, np.float64), np.array(circle, np.float64)
+
+
+def circle_square(k: int, scale: float = 1e4) -> np.ndarray:
+    """gen_circle_square(k) cost matrix (datasets.cpp:57-112, :184-214)."""
+    square, circle = circle_square_points(k)
     c = np.empty((k, k), np.int64)
     for i, (px, py) in enumerate(square):
         for j, (qx, qy) in enumerate(circle):

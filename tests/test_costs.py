@@ -120,3 +120,34 @@ def test_gpu_costs_bad_args(solver):
         solver.costs_from_points(a, a, 0.0)
     with pytest.raises(ValueError):
         solver.costs_from_points(a, np.zeros((4, 3)), 1.0)
+
+
+def test_circle_square_points_match_reference_build_instance():
+    """acceptance.cpp criterion 1's CircleSquare clouds through the reference's
+    own build_instance reproduce the restated cost matrix."""
+    from tests.golden.make_golden import circle_square, circle_square_points
+    sq, ci = circle_square_points(100)
+    np.testing.assert_array_equal(O.ref_build_instance(sq, ci, 1e4), circle_square(100))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,objective", [(100, 732033), (900, 9515106)])
+def test_gpu_circle_square_acceptance(solver, k, objective):
+    """acceptance.cpp criterion 1: cs100 = 732033, cs900 = 9515106,
+    from the point clouds: GPU build_instance -> GPU solve (both seeds), duals
+    equal to the reference's."""
+    from paper_2005_01182_b200 import solve_batched_km, solve_km
+    from tests.golden.make_golden import circle_square, circle_square_points
+    sq, ci = circle_square_points(k)
+    c = solver.costs_from_points(sq, ci, 1e4)
+    np.testing.assert_array_equal(c, circle_square(k))
+    r = solve_batched_km(c, solver=solver)
+    assert r.total_cost == objective
+    ref = O.ref_solve_batched_km(c)
+    np.testing.assert_array_equal(r.u, ref.u)
+    np.testing.assert_array_equal(r.v, ref.v)
+    rk = solve_km(c, solver=solver)
+    assert rk.total_cost == objective
+    refk = O.ref_solve_km(c)
+    np.testing.assert_array_equal(rk.u, refk.u)
+    np.testing.assert_array_equal(rk.v, refk.v)
