@@ -195,6 +195,15 @@ def _gen_c3(first: int, count: int) -> np.ndarray:
     return W.embedding_batch(count, N, 300, 1e4, seed=3, first=first)
 
 
+# engine id (kmb_stats.engine) -> (description, kernel); the auto choice depends on
+# the per-GPU shard: all 4096 instances at 1-2 GPUs run one warp each, the 1024 /
+# 512-instance shards at 4 / 8 GPUs one CTA each
+ENGINES = {4: ("warp engine (one warp per instance, costs streamed from L2)", "k_warp_batch"),
+           6: ("CTA engine (one CTA per instance, thread per column, costs from L2)", "k_cta_batch"),
+           3: ("warp engine, matrices staged in SMEM by TMA", "k_warp_batch"),
+           2: ("CTA engine, matrices staged in SMEM by TMA", "k_cta_batch")}
+
+
 def extras_c5(solver, hbm_peak: float) -> dict:
     """Config 5 (n=16384, 1 GiB, HBM-resident): one warm + timed solves, the
     reduced-cost scan's algorithmic bytes over the device time."""
@@ -306,6 +315,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     phases = 0
+    engine_used = 4
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -315,6 +325,7 @@ def main():
             st = solver.solve_batch_into(dcost, count, N, 1, r2c, du, dv, dtot)
             ev[k][1].record(stream)
             phases = st.phases
+            engine_used = st.engine
         torch.cuda.synchronize()
     barrier(world)
     step_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
@@ -383,10 +394,10 @@ def main():
                        "parallelism": f"instances sharded over {world} rank(s), one per GPU "
                                       f"({_BACKEND} for the max-over-ranks timing)",
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "engine": "warp engine (one warp per instance, costs streamed from L2)"},
+                       "engine": ENGINES.get(engine_used, (str(engine_used), ""))[0]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "k_warp_batch", "peak_source": peak_src,
+                         "kernel": ENGINES.get(engine_used, ("", "?"))[1], "peak_source": peak_src,
                          "note": "L1/L2-resident re-reads: algorithmic bytes are SURVEY 8(d)'s "
                                  "4n^2 per phase (+2 reductions) per instance, mostly served from "
                                  "L2, so achieved can exceed the HBM peak; traffic = ncu DRAM "

@@ -21,6 +21,12 @@
 #include "kmb_common.cuh"
 #include "kmb_internal.h"
 
+// per-stage clock64 accounting (kmb_last_instance_stats columns 5-8): a
+// diagnostic build flag, off in production (it costs a few percent)
+#ifndef KMB_CTA_STAGE_CLOCKS
+#define KMB_CTA_STAGE_CLOCKS 0
+#endif
+
 namespace kmb {
 
 namespace {
@@ -116,12 +122,17 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
   int status = 0;
   long long cyc[4] = {0, 0, 0, 0};  // relax, min (incl. B1), absorb (incl. B2), epoch end
   long long tl = clock64();
+  const long long t_begin = tl;
+#if KMB_CTA_STAGE_CLOCKS
 #define KMB_CSTAGE(k)               \
   do {                              \
     const long long t_ = clock64(); \
     cyc[k] += t_ - tl;              \
     tl = t_;                        \
   } while (0)
+#else
+#define KMB_CSTAGE(k) (void)tl
+#endif
   __syncthreads();
 
   while (nfree > 0) {
@@ -138,9 +149,20 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
 #pragma unroll
       for (int k = 0; k < 8; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
     }
-    for (; r < nrows; ++r) {
+    if (nrows - r == 1) {
       const int2 e = rows[r];
       key = KO::kmin(key, KO::make(ldc<SMEM_C>(colp + e.x * n), static_cast<uint32_t>(e.y), e.x));
+    } else if (r < nrows) {
+      // 2..7 rows: one batch with the last row repeated (the fold is
+      // idempotent), so every load is in flight at once
+      int2 e[8];
+      int32_t c[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e[k] = rows[min(r + k, nrows - 1)];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
     }
     if (rounds == 1 && a.seed == 1 && own) v = KO::val(key);  // column reduction, :328-333
     rows_scanned += nrows - head;
@@ -264,7 +286,7 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
       o[1] = dual_steps;
       o[2] = rows_scanned;
       o[3] = rounds;
-      o[4] = cyc[0] + cyc[1] + cyc[2] + cyc[3];
+      o[4] = KMB_CTA_STAGE_CLOCKS ? cyc[0] + cyc[1] + cyc[2] + cyc[3] : clock64() - t_begin;
       for (int k = 0; k < 4; ++k) o[5 + k] = cyc[k];
     }
   }
@@ -387,6 +409,18 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
 }
 
 int batch_max_n() { return 256; }
+
+int cta_batch_capacity(int n, int sm_count) {  // instances resident at once (L2 variant)
+  if (n < 1 || n > 256) return 0;
+  const int threads = ((n + 31) / 32) * 32;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cta_batch<false>, threads,
+                                                    cta_smem_bytes(n, false)) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return occ * sm_count;
+}
 
 cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warps_per_sm,
                          cudaStream_t st, int* grid_out) {

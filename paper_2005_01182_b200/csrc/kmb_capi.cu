@@ -189,14 +189,21 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   cudaStream_t st = c->stream;
   const size_t cbytes = static_cast<size_t>(batch) * n * n * sizeof(int32_t);
   const int32_t* dcost = costs;
-  if (engine == 0 || engine == 1 || engine == 5) engine = 4;  // auto: warp engine, costs from L2
+  // auto: a batch that fits the CTA engine's residency in one wave (e.g. a
+  // config-3 shard at 4+ GPUs: 1024 or 512 instances per GPU) runs one CTA per
+  // instance (shorter rounds: 0.44 vs 0.67 ms at 512); larger batches one warp
+  // per instance, everything resident (1.12 ms at 4096 vs 2.0 for CTAs)
+  if (engine == 0 || engine == 1 || engine == 5)
+    engine = (batch > 1 && batch <= kmb::cta_batch_capacity(n, c->sm_count)) ? 6 : 4;
   // Host input to the warp engine in its natural pitch: stream the batch in
   // chunks, each chunk's kernel starting as soon as its H2D copy lands, so the
   // PCIe transfer overlaps the solves (the transfer, not the GPU, bounds the
   // end-to-end rate).
   const bool host_in = !is_device_ptr(costs);
-  const bool pipelined = host_in && (engine == 3 || engine == 4) && kmb::warp_pitch(n) == n &&
-                         batch >= 1024;
+  const bool pipelined = host_in && batch >= 256 &&
+                         (((engine == 3 || engine == 4) && kmb::warp_pitch(n) == n) ||
+                          engine == 2 || engine == 6);
+  const int K = std::min(8, batch / 64);  // pipeline chunks
   if (host_in) {
     KMB_CUDA(c->bcost.ensure(cbytes));
     if (!pipelined)
@@ -213,6 +220,15 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8));
   KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
   int grid = 0;
+  auto ensure_aux = [&]() -> cudaError_t {
+    if (c->aux[0]) return cudaSuccess;
+    for (int k = 0; k < kmb_context::kAux; ++k) {
+      cudaError_t e = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
   if (engine == 2 || engine == 6) {
     kmb::BatchArgs a{};
     a.C = dcost;
@@ -227,7 +243,33 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.stats = c->bstat.as<int64_t>();
     a.status = c->bstatus.as<int32_t>();
     KMB_CUDA(cudaEventRecord(c->ev0, st));
-    KMB_CUDA(kmb::launch_batch(a, c->sm_count, engine == 2, static_cast<int>(c->warps_per_sm), st, &grid));
+    if (!pipelined) {
+      KMB_CUDA(kmb::launch_batch(a, c->sm_count, engine == 2, static_cast<int>(c->warps_per_sm), st, &grid));
+    } else {  // chunked H2D, each chunk's solve starting as its copy lands
+      KMB_CUDA(ensure_aux());
+      const int chunk = (batch + K - 1) / K;
+      for (int k = 0; k < K; ++k) {
+        const int lo = k * chunk, cnt = std::min(chunk, batch - lo);
+        if (cnt <= 0) break;
+        cudaStream_t s2 = c->aux[k % kmb_context::kAux];
+        KMB_CUDA(cudaStreamWaitEvent(s2, c->ev0, 0));
+        const size_t off = static_cast<size_t>(lo) * n * n;
+        KMB_CUDA(cudaMemcpyAsync(c->bcost.as<int32_t>() + off, costs + off,
+                                 static_cast<size_t>(cnt) * n * n * 4, cudaMemcpyHostToDevice, s2));
+        kmb::BatchArgs ak = a;
+        ak.C = a.C + off;
+        ak.batch = cnt;
+        ak.row_to_col = a.row_to_col + static_cast<size_t>(lo) * n;
+        ak.u = a.u + static_cast<size_t>(lo) * n;
+        ak.v = a.v + static_cast<size_t>(lo) * n;
+        ak.total_cost = a.total_cost + lo;
+        ak.stats = a.stats + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
+        ak.status = a.status + lo;
+        KMB_CUDA(kmb::launch_batch(ak, c->sm_count, engine == 2, static_cast<int>(c->warps_per_sm), s2, &grid));
+        KMB_CUDA(cudaEventRecord(c->aux_ev[k % kmb_context::kAux], s2));
+        KMB_CUDA(cudaStreamWaitEvent(st, c->aux_ev[k % kmb_context::kAux], 0));
+      }
+    }
   } else {
     const int np = kmb::warp_pitch(n);
     const int32_t* src = dcost;
@@ -275,13 +317,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       KMB_CUDA(pack(a, st));
       KMB_CUDA(kmb::launch_warp_batch(a, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), st, &grid));
     } else {
-      if (!c->aux[0]) {
-        for (int k = 0; k < kmb_context::kAux; ++k) {
-          KMB_CUDA(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
-          KMB_CUDA(cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming));
-        }
-      }
-      const int K = 8;
+      KMB_CUDA(ensure_aux());
       const int chunk = (batch + K - 1) / K;
       for (int k = 0; k < K; ++k) {
         const int lo = k * chunk, cnt = std::min(chunk, batch - lo);

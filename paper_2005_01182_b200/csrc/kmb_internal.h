@@ -113,6 +113,7 @@ struct WarpArgs {
   const int32_t* imax;
 };
 int warp_max_n();
+int cta_batch_capacity(int n, int sm_count);  // CTA/L2 engine: instances resident at once
 cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_t* rmin,
                           int32_t* imin, int32_t* imax, cudaStream_t st);
 int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)
