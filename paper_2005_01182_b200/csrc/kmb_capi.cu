@@ -188,26 +188,25 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
                             int64_t* total_cost, kmb_stats* stats, const char* who, int engine) {
   cudaStream_t st = c->stream;
   const size_t cbytes = static_cast<size_t>(batch) * n * n * sizeof(int32_t);
-  const int32_t* dcost = costs;
-  // auto: a batch that fits the CTA engine's residency in one wave (e.g. a
-  // config-3 shard at 4+ GPUs: 1024 or 512 instances per GPU) runs one CTA per
-  // instance (shorter rounds: 0.44 vs 0.67 ms at 512); larger batches one warp
-  // per instance, everything resident (1.12 ms at 4096 vs 2.0 for CTAs)
-  if (engine == 0 || engine == 1 || engine == 5)
-    engine = (batch > 1 && batch <= kmb::cta_batch_capacity(n, c->sm_count)) ? 6 : 4;
-  // Host input to the warp engine in its natural pitch: stream the batch in
-  // chunks, each chunk's kernel starting as soon as its H2D copy lands, so the
-  // PCIe transfer overlaps the solves (the transfer, not the GPU, bounds the
-  // end-to-end rate).
+  // auto: a batch (or pipeline chunk) that fits the CTA engine's residency in
+  // one wave runs one CTA per instance (shorter rounds: 0.42 vs 0.67 ms for a
+  // 512-instance config-3 shard); larger batches one warp per instance, all
+  // resident (1.12 ms at 4096 vs 1.8 for CTAs)
+  const bool auto_engine = engine == 0 || engine == 1 || engine == 5;
+  const int cap6 = auto_engine ? kmb::cta_batch_capacity(n, c->sm_count) : 0;
+  auto pick = [&](int cnt) { return (cnt > 1 && cnt <= cap6) ? 6 : 4; };
+  if (auto_engine) engine = pick(batch);
+  const int np = kmb::warp_pitch(n);
+  // Host input: stream the batch in chunks, each chunk's kernel starting as soon
+  // as its H2D copy lands and its results leaving as soon as it ends, so the
+  // PCIe transfers overlap the solves (the transfer bounds the end-to-end rate).
   const bool host_in = !is_device_ptr(costs);
-  const bool pipelined = host_in && batch >= 256 &&
-                         (((engine == 3 || engine == 4) && kmb::warp_pitch(n) == n) ||
-                          engine == 2 || engine == 6);
-  const int K = std::min(8, batch / 64);  // pipeline chunks
+  const bool warp_eng = engine == 3 || engine == 4;
+  const bool pipelined = host_in && batch >= 256 && (!warp_eng || np == n);
+  const int K = pipelined ? std::min(8, batch / 64) : 1;
+  const int32_t* dcost = costs;
   if (host_in) {
     KMB_CUDA(c->bcost.ensure(cbytes));
-    if (!pipelined)
-      KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
     dcost = c->bcost.as<int32_t>();
   }
   const size_t nb = static_cast<size_t>(batch) * n;
@@ -219,141 +218,110 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   if (!is_device_ptr(total_cost)) { KMB_CUDA(c->btot.ensure(batch * 8)); dtot = c->btot.as<int64_t>(); }
   KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8));
   KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
+  // U16 mode (warp/L2 engine, 4 or 8 columns per lane): a packing pass writes
+  // 16-bit offsets from the row minima, halving the bytes every relax streams
+  const bool u16 = engine == 4 && c->u16 && (np == 128 || np == 256);
+  if (u16) {
+    KMB_CUDA(c->b16.ensure(nb * np * 2));
+    KMB_CUDA(c->brmin.ensure(nb * 4));
+    KMB_CUDA(c->bimin.ensure(static_cast<size_t>(batch) * 4));
+    KMB_CUDA(c->bimax.ensure(static_cast<size_t>(batch) * 4));
+  }
+  const int32_t* src = dcost;  // warp engines: rows padded to the warp width
   int grid = 0;
-  auto ensure_aux = [&]() -> cudaError_t {
-    if (c->aux[0]) return cudaSuccess;
-    for (int k = 0; k < kmb_context::kAux; ++k) {
-      cudaError_t e = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-  };
-  if (engine == 2 || engine == 6) {
-    kmb::BatchArgs a{};
-    a.C = dcost;
-    a.batch = batch;
-    a.n = n;
-    a.seed = seed;
-    a.continue_bfs = c->continue_bfs;
-    a.row_to_col = dr2c;
-    a.u = du;
-    a.v = dv;
-    a.total_cost = dtot;
-    a.stats = c->bstat.as<int64_t>();
-    a.status = c->bstatus.as<int32_t>();
-    KMB_CUDA(cudaEventRecord(c->ev0, st));
-    if (!pipelined) {
-      KMB_CUDA(kmb::launch_batch(a, c->sm_count, engine == 2, static_cast<int>(c->warps_per_sm), st, &grid));
-    } else {  // chunked H2D, each chunk's solve starting as its copy lands
-      KMB_CUDA(ensure_aux());
-      const int chunk = (batch + K - 1) / K;
-      for (int k = 0; k < K; ++k) {
-        const int lo = k * chunk, cnt = std::min(chunk, batch - lo);
-        if (cnt <= 0) break;
-        cudaStream_t s2 = c->aux[k % kmb_context::kAux];
-        KMB_CUDA(cudaStreamWaitEvent(s2, c->ev0, 0));
-        const size_t off = static_cast<size_t>(lo) * n * n;
-        KMB_CUDA(cudaMemcpyAsync(c->bcost.as<int32_t>() + off, costs + off,
-                                 static_cast<size_t>(cnt) * n * n * 4, cudaMemcpyHostToDevice, s2));
-        kmb::BatchArgs ak = a;
-        ak.C = a.C + off;
-        ak.batch = cnt;
-        ak.row_to_col = a.row_to_col + static_cast<size_t>(lo) * n;
-        ak.u = a.u + static_cast<size_t>(lo) * n;
-        ak.v = a.v + static_cast<size_t>(lo) * n;
-        ak.total_cost = a.total_cost + lo;
-        ak.stats = a.stats + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
-        ak.status = a.status + lo;
-        KMB_CUDA(kmb::launch_batch(ak, c->sm_count, engine == 2, static_cast<int>(c->warps_per_sm), s2, &grid));
-        KMB_CUDA(cudaEventRecord(c->aux_ev[k % kmb_context::kAux], s2));
-        KMB_CUDA(cudaStreamWaitEvent(st, c->aux_ev[k % kmb_context::kAux], 0));
-      }
-    }
-  } else {
-    const int np = kmb::warp_pitch(n);
-    const int32_t* src = dcost;
-    if (np != n) {  // rows padded to the warp width (in-bounds 128-bit loads): pad once
-      KMB_CUDA(c->bpad.ensure(static_cast<size_t>(batch) * n * np * 4));
-      KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4,
-                                 static_cast<size_t>(batch) * n, cudaMemcpyDeviceToDevice, st));
-      src = c->bpad.as<int32_t>();
+  // instances [lo, lo + cnt) on engine eng, stream s
+  auto launch = [&](int lo, int cnt, int eng, cudaStream_t s) -> cudaError_t {
+    const size_t ro = static_cast<size_t>(lo) * n;
+    if (eng == 2 || eng == 6) {
+      kmb::BatchArgs a{};
+      a.C = dcost + ro * n;
+      a.batch = cnt;
+      a.n = n;
+      a.seed = seed;
+      a.continue_bfs = c->continue_bfs;
+      a.row_to_col = dr2c + ro;
+      a.u = du + ro;
+      a.v = dv + ro;
+      a.total_cost = dtot + lo;
+      a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
+      a.status = c->bstatus.as<int32_t>() + lo;
+      return kmb::launch_batch(a, c->sm_count, eng == 2, static_cast<int>(c->warps_per_sm), s, &grid);
     }
     kmb::WarpArgs a{};
-    a.C = src;
-    a.batch = batch;
+    a.C = src + ro * np;
+    a.batch = cnt;
     a.n = n;
     a.pitch = np;
     a.seed = seed;
     a.continue_bfs = c->continue_bfs;
-    a.row_to_col = dr2c;
-    a.u = du;
-    a.v = dv;
-    a.total_cost = dtot;
-    a.stats = c->bstat.as<int64_t>();
-    a.status = c->bstatus.as<int32_t>();
-    // U16 mode (warp/L2 engine, 4 or 8 columns per lane): a packing pass writes
-    // 16-bit offsets from the row minima, halving the bytes every relax streams
-    const bool u16 = engine == 4 && c->u16 && (np == 128 || np == 256);
+    a.row_to_col = dr2c + ro;
+    a.u = du + ro;
+    a.v = dv + ro;
+    a.total_cost = dtot + lo;
+    a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
+    a.status = c->bstatus.as<int32_t>() + lo;
     if (u16) {
-      const size_t rows_all = static_cast<size_t>(batch) * n;
-      KMB_CUDA(c->b16.ensure(rows_all * np * 2));
-      KMB_CUDA(c->brmin.ensure(rows_all * 4));
-      KMB_CUDA(c->bimin.ensure(static_cast<size_t>(batch) * 4));
-      KMB_CUDA(c->bimax.ensure(static_cast<size_t>(batch) * 4));
-      a.C16 = c->b16.as<uint16_t>();
-      a.rmin = c->brmin.as<int32_t>();
-      a.imin = c->bimin.as<int32_t>();
-      a.imax = c->bimax.as<int32_t>();
+      a.C16 = c->b16.as<uint16_t>() + ro * np;
+      a.rmin = c->brmin.as<int32_t>() + ro;
+      a.imin = c->bimin.as<int32_t>() + lo;
+      a.imax = c->bimax.as<int32_t>() + lo;
+      cudaError_t e = kmb::launch_pack16(a, c->sm_count, const_cast<uint16_t*>(a.C16),
+                                         const_cast<int32_t*>(a.rmin), const_cast<int32_t*>(a.imin),
+                                         const_cast<int32_t*>(a.imax), s);
+      if (e != cudaSuccess) return e;
     }
-    auto pack = [&](const kmb::WarpArgs& ak, cudaStream_t s) -> cudaError_t {
-      if (!u16) return cudaSuccess;
-      return kmb::launch_pack16(ak, c->sm_count, const_cast<uint16_t*>(ak.C16),
-                                const_cast<int32_t*>(ak.rmin), const_cast<int32_t*>(ak.imin),
-                                const_cast<int32_t*>(ak.imax), s);
-    };
-    KMB_CUDA(cudaEventRecord(c->ev0, st));
-    if (!pipelined) {
-      KMB_CUDA(pack(a, st));
-      KMB_CUDA(kmb::launch_warp_batch(a, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), st, &grid));
-    } else {
-      KMB_CUDA(ensure_aux());
-      const int chunk = (batch + K - 1) / K;
-      for (int k = 0; k < K; ++k) {
-        const int lo = k * chunk, cnt = std::min(chunk, batch - lo);
-        if (cnt <= 0) break;
-        cudaStream_t s = c->aux[k % kmb_context::kAux];
-        KMB_CUDA(cudaStreamWaitEvent(s, c->ev0, 0));
-        const size_t off = static_cast<size_t>(lo) * n * n;
-        KMB_CUDA(cudaMemcpyAsync(c->bcost.as<int32_t>() + off, costs + off,
-                                 static_cast<size_t>(cnt) * n * n * 4, cudaMemcpyHostToDevice, s));
-        kmb::WarpArgs ak = a;
-        ak.C = a.C + off;
-        ak.batch = cnt;
-        ak.row_to_col = a.row_to_col + static_cast<size_t>(lo) * n;
-        ak.u = a.u + static_cast<size_t>(lo) * n;
-        ak.v = a.v + static_cast<size_t>(lo) * n;
-        ak.total_cost = a.total_cost + lo;
-        ak.stats = a.stats + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
-        ak.status = a.status + lo;
-        if (u16) {
-          ak.C16 = a.C16 + static_cast<size_t>(lo) * n * np;
-          ak.rmin = a.rmin + static_cast<size_t>(lo) * n;
-          ak.imin = a.imin + lo;
-          ak.imax = a.imax + lo;
-        }
-        KMB_CUDA(pack(ak, s));
-        KMB_CUDA(kmb::launch_warp_batch(ak, c->sm_count, engine == 3, static_cast<int>(c->warps_per_sm), s, &grid));
-        KMB_CUDA(cudaEventRecord(c->aux_ev[k % kmb_context::kAux], s));
-        KMB_CUDA(cudaStreamWaitEvent(st, c->aux_ev[k % kmb_context::kAux], 0));
+    return kmb::launch_warp_batch(a, c->sm_count, eng == 3, static_cast<int>(c->warps_per_sm), s, &grid);
+  };
+  // results of instances [lo, lo + cnt) to the caller's host buffers
+  auto results_out = [&](int lo, int cnt, cudaStream_t s) -> cudaError_t {
+    const size_t ro = static_cast<size_t>(lo) * n, rn = static_cast<size_t>(cnt) * n;
+    cudaError_t e = cudaSuccess;
+    if (dr2c != row_to_col && row_to_col)
+      e = cudaMemcpyAsync(row_to_col + ro, dr2c + ro, rn * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && du != u && u) e = cudaMemcpyAsync(u + ro, du + ro, rn * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dv != v && v) e = cudaMemcpyAsync(v + ro, dv + ro, rn * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dtot != total_cost && total_cost)
+      e = cudaMemcpyAsync(total_cost + lo, dtot + lo, static_cast<size_t>(cnt) * 8, cudaMemcpyDeviceToHost, s);
+    return e;
+  };
+  int used = engine;
+  KMB_CUDA(cudaEventRecord(c->ev0, st));
+  if (!pipelined) {
+    if (host_in) KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
+    if (warp_eng && np != n) {  // rows padded to the warp width (in-bounds 128-bit loads): pad once
+      KMB_CUDA(c->bpad.ensure(nb * np * 4));
+      KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4, nb, cudaMemcpyDeviceToDevice, st));
+      src = c->bpad.as<int32_t>();
+    }
+    KMB_CUDA(launch(0, batch, engine, st));
+    KMB_CUDA(cudaEventRecord(c->ev1, st));
+    KMB_CUDA(results_out(0, batch, st));
+  } else {
+    if (!c->aux[0]) {
+      for (int k = 0; k < kmb_context::kAux; ++k) {
+        KMB_CUDA(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
+        KMB_CUDA(cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming));
       }
     }
+    const int chunk = (batch + K - 1) / K;
+    for (int k = 0; k < K; ++k) {
+      const int lo = k * chunk, cnt = std::min(chunk, batch - lo);
+      if (cnt <= 0) break;
+      cudaStream_t s2 = c->aux[k % kmb_context::kAux];
+      KMB_CUDA(cudaStreamWaitEvent(s2, c->ev0, 0));
+      const size_t off = static_cast<size_t>(lo) * n * n;
+      KMB_CUDA(cudaMemcpyAsync(c->bcost.as<int32_t>() + off, costs + off,
+                               static_cast<size_t>(cnt) * n * n * 4, cudaMemcpyHostToDevice, s2));
+      const int eng = auto_engine ? pick(cnt) : engine;  // chunks are small: CTA engine
+      if (k == 0) used = eng;
+      KMB_CUDA(launch(lo, cnt, eng, s2));
+      KMB_CUDA(results_out(lo, cnt, s2));
+      KMB_CUDA(cudaEventRecord(c->aux_ev[k % kmb_context::kAux], s2));
+      KMB_CUDA(cudaStreamWaitEvent(st, c->aux_ev[k % kmb_context::kAux], 0));
+    }
+    KMB_CUDA(cudaEventRecord(c->ev1, st));  // includes the transfers
   }
-  KMB_CUDA(cudaEventRecord(c->ev1, st));
-  if (dr2c != row_to_col) { int r = copy_out(row_to_col, dr2c, nb * 4, st); if (r) return r; }
-  if (du != u) { int r = copy_out(u, du, nb * 8, st); if (r) return r; }
-  if (dv != v) { int r = copy_out(v, dv, nb * 8, st); if (r) return r; }
-  if (dtot != total_cost) { int r = copy_out(total_cost, dtot, batch * 8, st); if (r) return r; }
+  engine = used;
   // status is always checked (one small copy): invalid input must not pass silently
   int32_t* hstatus = new int32_t[batch];
   int64_t* hstat = stats ? new int64_t[static_cast<size_t>(batch) * kmb::KMB_ISTATS] : nullptr;
