@@ -35,9 +35,12 @@
 // stay reached (incremental epochs).  The barrier is a template:
 // GridBarrier (software, any G <= #SMs, cooperative launch) or ClusterBarrier
 // (one thread-block cluster of G <= 16 CTAs, hardware barrier.cluster).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <type_traits>
 
 #include "kmb_common.cuh"
 #include "kmb_internal.h"
@@ -63,6 +66,88 @@ struct SlabSmem {
   int32_t append_base;
   int32_t ndseg;  // dirty segments after an epoch end (-1: relax everything)
 };
+
+// ---- where the per-row / per-column search state lives -----------------------
+// GMem: global memory (grid engine, any G).  DMem: the distributed shared memory
+// of the one thread-block cluster (cluster engine, G a power of two): element i
+// of every array lives in CTA (i mod G) at local index i / G, the append
+// counters in CTA 0 and each CTA's min-slack partial in its own shared memory,
+// so every dependent hop of a round is a DSMEM access instead of an L2 round
+// trip.  The barriers order both (bar.sync + gpu-scope release/acquire, or
+// barrier.cluster release/acquire).
+struct GMem {
+  const SolverArgs* a;
+  __device__ int32_t* list_row(int p, int i) const { return a->list_row[p] + i; }
+  __device__ int64_t* list_w(int p, int i) const { return a->list_w[p] + i; }
+  __device__ int64_t* u(int i) const { return a->u + i; }
+  __device__ int32_t* root_row(int i) const { return a->root_row + i; }
+  __device__ int32_t* match_row(int i) const { return a->match_row + i; }
+  __device__ int32_t* match_col(int i) const { return a->match_col + i; }
+  __device__ int32_t* tree_par(int i) const { return a->tree_par + i; }
+  __device__ uint64_t* claim(int i) const { return a->claim + i; }
+  __device__ int32_t* found(int i) const { return a->found + i; }
+  __device__ int* rcnt(int k) const { return &a->ctrl->rcnt[k]; }
+  __device__ int* fcnt(int k) const { return &a->ctrl->fcnt[k]; }
+  __device__ int64_t* partial(int b) const { return a->partial + b; }
+  template <class T>
+  __device__ static T ld(const T* p) { return ldcg(p); }
+  // tree claims: 64-bit (epoch stamp, column) keys, smaller wins
+  __device__ static uint64_t ckey(int ep, int col) { return claim_key(ep, col); }
+  __device__ static bool claimed(uint64_t c, int ep) { return claimed_in(c, ep); }
+  __device__ void claim_min(int root, uint64_t k) const {
+    atomicMin(reinterpret_cast<unsigned long long*>(a->claim + root), static_cast<unsigned long long>(k));
+  }
+};
+
+struct DMem {
+  int64_t *lw[2], *u_;
+  uint32_t* claim_;  // 32-bit claims: 64-bit atomicMin has no native DSMEM form
+  int32_t *lrow[2], *root_, *mrow_, *mcol_, *tpar_, *found_;
+  int* cnt;       // [0, 3) row appends, [3, 6) free-column appends: CTA 0's are live
+  int64_t* part;  // this CTA's min-slack partial
+  int shift, mask;
+  template <class T>
+  __device__ T* at(T* base, int i) const {
+    return cooperative_groups::this_cluster().map_shared_rank(base + (i >> shift),
+                                                              static_cast<unsigned>(i & mask));
+  }
+  __device__ int32_t* list_row(int p, int i) const { return at(lrow[p], i); }
+  __device__ int64_t* list_w(int p, int i) const { return at(lw[p], i); }
+  __device__ int64_t* u(int i) const { return at(u_, i); }
+  __device__ int32_t* root_row(int i) const { return at(root_, i); }
+  __device__ int32_t* match_row(int i) const { return at(mrow_, i); }
+  __device__ int32_t* match_col(int i) const { return at(mcol_, i); }
+  __device__ int32_t* tree_par(int i) const { return at(tpar_, i); }
+  __device__ uint32_t* claim(int i) const { return at(claim_, i); }
+  __device__ int32_t* found(int i) const { return at(found_, i); }
+  // (stamp, column) in 32 bits: n <= 8192 columns (13 bits), stamp 0x7FFFF - (ep + 1)
+  // decreasing with the epoch; the all-ones initial value matches no epoch
+  __device__ static uint32_t ckey(int ep, int col) {
+    return ((0x7FFFFu - static_cast<uint32_t>(ep + 1)) << 13) | static_cast<uint32_t>(col);
+  }
+  __device__ static bool claimed(uint32_t c, int ep) {
+    return (c >> 13) == 0x7FFFFu - static_cast<uint32_t>(ep + 1);
+  }
+  __device__ void claim_min(int root, uint32_t k) const { atomicMin(claim(root), k); }
+  __device__ int* rcnt(int k) const { return cooperative_groups::this_cluster().map_shared_rank(cnt + k, 0u); }
+  __device__ int* fcnt(int k) const { return cooperative_groups::this_cluster().map_shared_rank(cnt + 3 + k, 0u); }
+  __device__ int64_t* partial(int b) const {
+    return cooperative_groups::this_cluster().map_shared_rank(part, static_cast<unsigned>(b));
+  }
+  template <class T>
+  __device__ static T ld(const T* p) { return *reinterpret_cast<const volatile T*>(p); }
+};
+
+// dynamic shared memory of the slab state (keys, v, Dc, reached, dirty segments)
+__host__ __device__ inline size_t solver_smem_bytes_dev(int W) {
+  return (static_cast<size_t>(W) * (8 + 8 + 8 + 1 + 1) + 16 + 15) & ~static_cast<size_t>(15);
+}
+
+// DSMEM bytes per CTA for n over G CTAs (L = ceil(n / G) elements of each array)
+__host__ __device__ inline size_t dsm_bytes(int n, int G) {
+  const size_t L = (static_cast<size_t>(n) + G - 1) / G;
+  return L * (8 * 3 + 4 * 8) + 16 * 16;  // + per-array 16-byte alignment, counters
+}
 
 // ---- K1: row reductions + engine state init (hungarian.cpp:323-327) -------
 // One warp per row, 128-bit loads; also seeds the phase-0 row list.
@@ -112,9 +197,9 @@ __global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
 // Thread (g, s): segment s = 4 consecutive columns, row group g.  W = 4*S is a
 // power of two, so lanes sharing a segment differ only in their high lane bits
 // (S < 32) and a xor-shuffle tree merges them before the shared atomics.
-__device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* list,
-                                           const int64_t* listw, int head, int tail,
-                                           int c0, int W, uint64_t* skey) {
+template <class Mem>
+__device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, int p, int head,
+                                           int tail, int c0, int W, uint64_t* skey) {
   const int S = W >> 2;
   const int R = kThreads / S > 0 ? kThreads / S : 1;
   const int tid = threadIdx.x;
@@ -136,13 +221,13 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
         int64_t dr[kRelaxBatch];
 #pragma unroll
         for (int k = 0; k < kRelaxBatch; ++k) {
-          i[k] = ldcg(list + r + k * R);
-          dr[k] = ldcg(listw + r + k * R);
+          i[k] = M.ld(M.list_row(p, r + k * R));
+          dr[k] = M.ld(M.list_w(p, r + k * R));
         }
 #pragma unroll
         for (int k = 0; k < kRelaxBatch; ++k) {
           c[k] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[k]) * a.pitch));
-          b[k] = row_bias(ldcg(a.u + i[k]) - dr[k]);  // w = u - D at reach
+          b[k] = row_bias(M.ld(M.u(i[k])) - dr[k]);  // w = u - D at reach
         }
 #pragma unroll
         for (int k = 0; k < kRelaxBatch; ++k) {
@@ -153,10 +238,10 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
         }
       }
       for (; r < tail; r += R) {
-        const int i = ldcg(list + r);
-        const int64_t drr = ldcg(listw + r);
+        const int i = M.ld(M.list_row(p, r));
+        const int64_t drr = M.ld(M.list_w(p, r));
         const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * a.pitch));
-        const uint32_t b = row_bias(ldcg(a.u + i) - drr);
+        const uint32_t b = row_bias(M.ld(M.u(i)) - drr);
         best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
         best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
         best2 = umin64(best2, pack_key(static_cast<uint32_t>(c.z) + b, i));
@@ -193,9 +278,10 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const int32_t* l
 // segs[0, nd) lists the dirty segments; thread (g, k) handles segs[k] for row
 // group g, with k in [0, np2), np2 = nd rounded up to a power of two (lanes of
 // the same k differ only in high lane bits, so a xor tree merges them).
-__device__ __forceinline__ void relax_sel(const SolverArgs& a, const int32_t* list,
-                                          const int64_t* listw, int head, int tail, int c0,
-                                          const int32_t* segs, int nd, uint64_t* skey) {
+template <class Mem>
+__device__ __forceinline__ void relax_sel(const SolverArgs& a, const Mem& M, int p, int head,
+                                          int tail, int c0, const int32_t* segs, int nd,
+                                          uint64_t* skey) {
   int np2 = 1;
   while (np2 < nd) np2 <<= 1;
   const int R = kThreads / np2;
@@ -213,13 +299,13 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const int32_t* li
       int64_t dr[kRelaxBatch];
 #pragma unroll
       for (int q = 0; q < kRelaxBatch; ++q) {
-        i[q] = ldcg(list + r + q * R);
-        dr[q] = ldcg(listw + r + q * R);
+        i[q] = M.ld(M.list_row(p, r + q * R));
+        dr[q] = M.ld(M.list_w(p, r + q * R));
       }
 #pragma unroll
       for (int q = 0; q < kRelaxBatch; ++q) {
         c[q] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[q]) * a.pitch));
-        b[q] = row_bias(ldcg(a.u + i[q]) - dr[q]);
+        b[q] = row_bias(M.ld(M.u(i[q])) - dr[q]);
       }
 #pragma unroll
       for (int q = 0; q < kRelaxBatch; ++q) {
@@ -230,10 +316,10 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const int32_t* li
       }
     }
     for (; r < tail; r += R) {
-      const int i = ldcg(list + r);
-      const int64_t drr = ldcg(listw + r);
+      const int i = M.ld(M.list_row(p, r));
+      const int64_t drr = M.ld(M.list_w(p, r));
       const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * a.pitch));
-      const uint32_t b = row_bias(ldcg(a.u + i) - drr);
+      const uint32_t b = row_bias(M.ld(M.u(i)) - drr);
       best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
       best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
       best2 = umin64(best2, pack_key(static_cast<uint32_t>(c.z) + b, i));
@@ -266,7 +352,7 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const int32_t* li
 // the reset ("dirty") columns only — the rows appended in the epoch's last round
 // having been relaxed over the whole slab first — and the search goes on at the
 // same D.
-template <class Barrier>
+template <class Barrier, bool DSM>
 __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const int W = a.W;
@@ -285,6 +371,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   Ctrl* ctrl = a.ctrl;
   const int gtid = blockIdx.x * kThreads + tid;
   const int gthreads = G * kThreads;
+
+  using Mem = std::conditional_t<DSM, DMem, GMem>;
+  Mem M;
+  if constexpr (DSM) {  // carve the distributed arrays, copy k_init_rows' state in
+    const int L = (a.n + G - 1) / G;
+    unsigned char* q = dyn + solver_smem_bytes_dev(W);
+    auto take = [&](size_t bytes) {
+      unsigned char* r = q;
+      q += (bytes + 15) & ~static_cast<size_t>(15);
+      return r;
+    };
+    M.lw[0] = reinterpret_cast<int64_t*>(take(8ull * L));
+    M.lw[1] = reinterpret_cast<int64_t*>(take(8ull * L));
+    M.u_ = reinterpret_cast<int64_t*>(take(8ull * L));
+    M.claim_ = reinterpret_cast<uint32_t*>(take(4ull * L));
+    M.lrow[0] = reinterpret_cast<int32_t*>(take(4ull * L));
+    M.lrow[1] = reinterpret_cast<int32_t*>(take(4ull * L));
+    M.root_ = reinterpret_cast<int32_t*>(take(4ull * L));
+    M.mrow_ = reinterpret_cast<int32_t*>(take(4ull * L));
+    M.mcol_ = reinterpret_cast<int32_t*>(take(4ull * L));
+    M.tpar_ = reinterpret_cast<int32_t*>(take(4ull * L));
+    M.found_ = reinterpret_cast<int32_t*>(take(4ull * L));
+    M.cnt = reinterpret_cast<int*>(take(8 * 4));
+    M.part = reinterpret_cast<int64_t*>(take(8));
+    M.shift = __ffs(G) - 1;
+    M.mask = G - 1;
+    for (int k = tid; k < L; k += kThreads) {
+      const int i = k * G + static_cast<int>(blockIdx.x);
+      if (i >= a.n) break;
+      M.u_[k] = ldcg(a.u + i);
+      M.claim_[k] = 0xFFFFFFFFu;  // unclaimed (k_init_rows' all-ones)
+      M.lrow[0][k] = ldcg(a.list_row[0] + i);
+      M.lw[0][k] = ldcg(a.list_w[0] + i);
+      M.root_[k] = ldcg(a.root_row + i);
+      M.mrow_[k] = ldcg(a.match_row + i);
+      M.mcol_[k] = ldcg(a.match_col + i);
+    }
+    if (tid < 6) M.cnt[tid] = 0;
+    bar.sync();  // every CTA's copy in place before any remote access
+  } else {
+    M.a = &a;
+  }
 
   if (ldcg(&ctrl->status) != 0) return;  // invalid input (k_init_rows), all CTAs agree
   for (int c = tid; c < W; c += kThreads) {
@@ -320,8 +448,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     bar.sync();
     ++kb;
     if (leader) {
-      ctrl->rcnt[(kb + 2) % 3] = 0;
-      ctrl->fcnt[(kb + 2) % 3] = 0;
+      *M.rcnt((kb + 2) % 3) = 0;
+      *M.fcnt((kb + 2) % 3) = 0;
     }
   };
   int64_t D = 0;
@@ -345,15 +473,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
 #define KMB_FINE(k) (void)0
 #endif
   for (;;) {
-    const int32_t* list = a.list_row[p];
-    const int64_t* listw = a.list_w[p];
     KMB_FINE(3);
     if (dirty_round) {
       dirty_round = false;
-      if (sm.ndseg > 0) relax_sel(a, list, listw, head, tail, c0, dsegs, sm.ndseg, skey);
+      if (sm.ndseg > 0) relax_sel(a, M, p, head, tail, c0, dsegs, sm.ndseg, skey);
       seg_rows += static_cast<int64_t>(tail - head) * sm.ndseg;
     } else {
-      relax_slab(a, list, listw, head, tail, c0, W, skey);
+      relax_slab(a, M, p, head, tail, c0, W, skey);
       rows_scanned += tail - head;
     }
     KMB_FINE(0);
@@ -366,8 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     // absorb the slab's tight columns at the current D (hungarian.cpp:186-199):
     // tightness is a per-column test, no global information needed
     auto absorb_at = [&](int64_t Dn) {
-      int* rc = &ctrl->rcnt[(kb + 1) % 3];
-      int* fc = &ctrl->fcnt[(kb + 1) % 3];
+      int* rc = M.rcnt((kb + 1) % 3);
+      int* fc = M.fcnt((kb + 1) % 3);
       for (int cb = 0; cb < W; cb += kThreads) {
         const int c = cb + tid;
         bool newrow = false, newfree = false;
@@ -376,15 +502,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
           rch[c] = 1;
           dcol[c] = Dn;
           const int32_t par = key_row(skey[c]);
-          a.tree_par[col] = par;
-          const int32_t root = ldcg(a.root_row + par);
-          i2 = ldcg(a.match_col + col);
+          *M.tree_par(col) = par;
+          const int32_t root = M.ld(M.root_row(par));
+          i2 = M.ld(M.match_col(col));
           if (i2 < 0) {
             newfree = true;
-            atomicMin(reinterpret_cast<unsigned long long*>(a.claim + root), claim_key(epoch, col));
+            M.claim_min(root, M.ckey(epoch, col));
           } else {
             newrow = true;  // the list keeps D at reach; w = u - Dn is formed by the relax
-            a.root_row[i2] = root;
+            *M.root_row(i2) = root;
 #if KMB_SOLVER_PREFETCH
             // every CTA scans this row next round: start pulling it into L2 now,
             // so the barrier and the list reads hide the DRAM latency
@@ -403,8 +529,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
           base = __shfl_sync(0xffffffffu, base, 0);
           if (newrow) {
             const int pos = tail + base + __popc(rowmask & ((1u << lane) - 1));
-            a.list_row[p][pos] = i2;
-            a.list_w[p][pos] = Dn;
+            *M.list_row(p, pos) = i2;
+            *M.list_w(p, pos) = Dn;
           }
         }
         const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
@@ -412,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
           int base = 0;
           if (lane == 0) base = atomicAdd(fc, __popc(fmask));
           base = __shfl_sync(0xffffffffu, base, 0);
-          if (newfree) a.found[nfound + base + __popc(fmask & ((1u << lane) - 1))] = col;
+          if (newfree) *M.found(nfound + base + __popc(fmask & ((1u << lane) - 1))) = col;
         }
       }
     };
@@ -432,19 +558,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     if (wid == 0) {
       int64_t x = lane < kThreads / 32 ? sm.part[lane] : KMB_I64_INF;
       x = warp_min_i64(x);
-      if (lane == 0) a.partial[blockIdx.x] = x;
+      if (lane == 0) *M.partial(blockIdx.x) = x;
     }
     KMB_STAGE(0);
     gsync();  // ---------------------------------------------------- B1
     KMB_STAGE(1);
-    int added = ldcg(&ctrl->rcnt[kb % 3]);
-    int fadded = ldcg(&ctrl->fcnt[kb % 3]);
+    int added = M.ld(M.rcnt(kb % 3));
+    int fadded = M.ld(M.fcnt(kb % 3));
     if (added == 0 && fadded == 0) {
       // no tight column anywhere and no pending row: dual step (:201-215)
       if (wid == 0) {
         int64_t x = KMB_I64_INF;
         for (int b = lane; b < G; b += 32) {
-          const int64_t y = ldcg(a.partial + b);
+          const int64_t y = M.ld(M.partial(b));
           x = y < x ? y : x;
         }
         x = warp_min_i64(x);
@@ -463,8 +589,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       KMB_STAGE(2);
       gsync();  // ------------------------------------------------ B2 (dual steps only)
       KMB_STAGE(3);
-      added = ldcg(&ctrl->rcnt[kb % 3]);
-      fadded = ldcg(&ctrl->fcnt[kb % 3]);
+      added = M.ld(M.rcnt(kb % 3));
+      fadded = M.ld(M.fcnt(kb % 3));
     }
     head = tail;
     tail += added;
@@ -476,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     // round re-relaxes survivors over dirty segments only, so every survivor
     // must already be in the keys); a key whose argmin is one of them that gets
     // dissolved is reset below like any other.
-    relax_slab(a, list, listw, head, tail, c0, W, skey);
+    relax_slab(a, M, p, head, tail, c0, W, skey);
     rows_scanned += tail - head;
     __syncthreads();
     // columns of the slab: finalise dissolved ones, reset keys whose argmin row leaves
@@ -484,15 +610,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       const int col = c0 + c;
       if (col >= a.n) continue;
       if (rch[c]) {
-        const int32_t root = ldcg(a.root_row + ldcg(a.tree_par + col));
-        if (claimed_in(ldcg(a.claim + root), epoch)) {
+        const int32_t root = M.ld(M.root_row(M.ld(M.tree_par(col))));
+        if (M.claimed(M.ld(M.claim(root)), epoch)) {
           vloc[c] -= D - dcol[c];
           rch[c] = 0;
           skey[c] = KMB_KEY_INF;
         }
       } else if (skey[c] != KMB_KEY_INF) {
-        const int32_t root = ldcg(a.root_row + key_row(skey[c]));
-        if (claimed_in(ldcg(a.claim + root), epoch)) skey[c] = KMB_KEY_INF;
+        const int32_t root = M.ld(M.root_row(key_row(skey[c])));
+        if (M.claimed(M.ld(M.claim(root)), epoch)) skey[c] = KMB_KEY_INF;
       }
     }
     // dirty segments: 4-column groups holding an unreached column whose key
@@ -510,34 +636,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       if (d) dsegs[atomicAdd(&sm.ndseg, 1)] = sgi;
     }
     // rows: finalise dissolved ones (u = w + D), carry the survivors over
-    int* sc = &ctrl->rcnt[(kb + 1) % 3];
+    int* sc = M.rcnt((kb + 1) % 3);
     for (int r = gtid; r < tail; r += gthreads) {
-      const int32_t i = ldcg(list + r);
-      const int64_t dr = ldcg(listw + r);
-      if (claimed_in(ldcg(a.claim + ldcg(a.root_row + i)), epoch)) {
+      const int32_t i = M.ld(M.list_row(p, r));
+      const int64_t dr = M.ld(M.list_w(p, r));
+      if (M.claimed(M.ld(M.claim(M.ld(M.root_row(i)))), epoch)) {
         // u = w + D.  (Another CTA's epoch-end relax of this row, if it was
         // appended this round, may read u before or after this write: either
         // way every key it could set has this dissolved row as argmin and is
         // reset by that CTA's column pass.)
-        a.u[i] = ldcg(a.u + i) - dr + D;
+        *M.u(i) = M.ld(M.u(i)) - dr + D;
       } else {
         const int pos = atomicAdd(sc, 1);
-        a.list_row[p ^ 1][pos] = i;
-        a.list_w[p ^ 1][pos] = dr;
+        *M.list_row(p ^ 1, pos) = i;
+        *M.list_w(p ^ 1, pos) = dr;
       }
     }
     // flip one parent-pointer path per claimed tree (its smallest free column)
     int won = 0;
     for (int f = gtid; f < nfound; f += gthreads) {
-      int32_t j = ldcg(a.found + f);
-      const int32_t root = ldcg(a.root_row + ldcg(a.tree_par + j));
-      if (ldcg(a.claim + root) != claim_key(epoch, j)) continue;
+      int32_t j = M.ld(M.found(f));
+      const int32_t root = M.ld(M.root_row(M.ld(M.tree_par(j))));
+      if (M.ld(M.claim(root)) != M.ckey(epoch, j)) continue;
       ++won;
       for (;;) {
-        const int32_t i = ldcg(a.tree_par + j);
-        const int32_t nxt = ldcg(a.match_row + i);
-        a.match_row[i] = j;
-        a.match_col[j] = i;
+        const int32_t i = M.ld(M.tree_par(j));
+        const int32_t nxt = M.ld(M.match_row(i));
+        *M.match_row(i) = j;
+        *M.match_col(j) = i;
         if (nxt < 0) break;
         j = nxt;
       }
@@ -554,7 +680,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     p ^= 1;
     ++epoch;
     head = 0;
-    tail = ldcg(&ctrl->rcnt[kb % 3]);  // survivors
+    tail = M.ld(M.rcnt(kb % 3));  // survivors
     dirty_round = true;
     nfound = 0;
     if (ldcg(&ctrl->matched) == a.n) break;
@@ -565,11 +691,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   }
   if (stopped) {  // time budget: write back the surviving trees' lazy duals
     for (int r = gtid; r < tail; r += gthreads) {
-      const int32_t i = ldcg(a.list_row[p] + r);
-      a.u[i] = ldcg(a.u + i) - ldcg(a.list_w[p] + r) + D;
+      const int32_t i = M.ld(M.list_row(p, r));
+      *M.u(i) = M.ld(M.u(i)) - M.ld(M.list_w(p, r)) + D;
     }
     for (int c = tid; c < W; c += kThreads)
       if (rch[c] && c0 + c < a.n) vloc[c] -= D - dcol[c];
+  }
+  if constexpr (DSM) {  // results back to global (u, matching); no remote access after
+    bar.sync();
+    const int L = (a.n + G - 1) / G;
+    for (int k = tid; k < L; k += kThreads) {
+      const int i = k * G + static_cast<int>(blockIdx.x);
+      if (i >= a.n) break;
+      a.u[i] = M.u_[k];
+      a.match_row[i] = M.mrow_[k];
+      a.match_col[i] = M.mcol_[k];
+    }
   }
   (void)fatal;
   for (int c = tid; c < W; c += kThreads)
@@ -603,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan_all(SolverArgs a, uint64_t
   const int W = a.W, c0 = blockIdx.x * W;
   for (int c = threadIdx.x; c < W; c += kThreads) skey[c] = KMB_KEY_INF;
   __syncthreads();
-  relax_slab(a, a.list_row[0], a.list_w[0], 0, a.n, c0, W, skey);
+  relax_slab(a, GMem{&a}, 0, 0, a.n, c0, W, skey);
   __syncthreads();
   for (int c = threadIdx.x; c < W; c += kThreads)
     if (c0 + c < a.n) keys_out[c0 + c] = skey[c];
@@ -633,7 +770,7 @@ __global__ void k_objective(const int32_t* C, int64_t pitch, int n, const int32_
   if ((threadIdx.x & 31) == 0) atomicAdd(out, static_cast<unsigned long long>(s));
 }
 
-size_t solver_smem_bytes(int W) { return static_cast<size_t>(W) * (8 + 8 + 8 + 1 + 1) + 16; }
+size_t solver_smem_bytes(int W) { return solver_smem_bytes_dev(W); }
 
 cudaError_t launch_solver_init(const SolverArgs& a, cudaStream_t st) {
   k_init_rows<<<256, 256, 0, st>>>(a);
@@ -645,7 +782,7 @@ cudaError_t launch_solver(const SolverArgs& a, int G, bool cluster, cudaStream_t
   if (e != cudaSuccess) return e;
   const size_t smem = solver_smem_bytes(a.W);
   if (!cluster) {
-    auto kern = k_solve<GridBarrier>;
+    auto kern = k_solve<GridBarrier, false>;
     if (smem > 48 * 1024) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) return e;
@@ -654,18 +791,23 @@ cudaError_t launch_solver(const SolverArgs& a, int G, bool cluster, cudaStream_t
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(G), dim3(kThreads), params,
                                        smem, st);
   }
-  // one thread-block cluster of G <= 16 CTAs: hardware cluster barriers
-  auto kern = k_solve<ClusterBarrier>;
+  // one thread-block cluster of G <= 16 CTAs: hardware cluster barriers; the
+  // search state in the cluster's distributed shared memory when G is a power
+  // of two (element i -> CTA i mod G) and it fits
+  static const bool no_dsm = getenv("KMB_NO_DSM") != nullptr;  // A/B switch
+  const bool dsm = !no_dsm && (G & (G - 1)) == 0 && smem + dsm_bytes(a.n, G) <= 200 * 1024;
+  auto kern = dsm ? k_solve<ClusterBarrier, true> : k_solve<ClusterBarrier, false>;
+  const size_t csmem = smem + (dsm ? dsm_bytes(a.n, G) : 0);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
-  if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (csmem > 48 * 1024) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(csmem));
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = csmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
