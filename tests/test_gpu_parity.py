@@ -390,3 +390,62 @@ def test_warp_engine_u16_mode_exact(solver):
         assert r.total_cost[t] == ref.total_cost
         np.testing.assert_array_equal(r.u[t], ref.u)
         np.testing.assert_array_equal(r.v[t], ref.v)
+
+
+@pytest.mark.gpu
+def test_concurrent_contexts_on_streams():
+    """The C ABI is re-entrant: independent contexts, each on its own CUDA
+    stream and host thread, solve concurrently (a serving setup) and every
+    result equals the reference's."""
+    import threading
+    import torch
+    from paper_2005_01182_b200 import Solver
+    c = W.CONFIGS["c3"].make(batch=96, first=11)
+    refs = [O.ref_solve_batched_km(c[t]) for t in range(c.shape[0])]
+    out, errs = {}, []
+
+    def work(k):
+        try:
+            s = Solver(0)
+            st = torch.cuda.Stream()
+            s.set_stream(st.cuda_stream)
+            part = c[k::3]
+            r = s.solve_batch(part)
+            out[k] = r
+            s.close()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ths = [threading.Thread(target=work, args=(k,)) for k in range(3)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    for k in range(3):
+        r = out[k]
+        for q, t in enumerate(range(k, c.shape[0], 3)):
+            np.testing.assert_array_equal(r.u[q], refs[t].u)
+            np.testing.assert_array_equal(r.v[q], refs[t].v)
+            assert int(r.total_cost[q]) == refs[t].total_cost
+
+
+@pytest.mark.gpu
+def test_cluster_engine_dsm_and_global_agree(solver):
+    """The cluster engine keeps its search state in distributed shared memory
+    when the cluster size is a power of two (n = 1024: 16 CTAs) and in global
+    memory otherwise (n = 600: 10 CTAs): both bit-exact, deterministic."""
+    rng = np.random.default_rng(77)
+    for n in (600, 1024):
+        c = rng.integers(0, 5000, size=(n, n)).astype(np.int32)
+        ref = O.ref_solve_batched_km(c)
+        solver.set_option(OPT_ENGINE, 5)
+        try:
+            r1 = solver.solve(c, KMB_SEED_BATCHED)
+            r2 = solver.solve(c, KMB_SEED_BATCHED)
+        finally:
+            solver.set_option(OPT_ENGINE, 0)
+        np.testing.assert_array_equal(r1.u, ref.u)
+        np.testing.assert_array_equal(r1.v, ref.v)
+        np.testing.assert_array_equal(r1.row_to_col, r2.row_to_col)
+        assert r1.stats["rounds"] == r2.stats["rounds"]
