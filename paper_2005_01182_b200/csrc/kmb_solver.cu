@@ -194,9 +194,9 @@ __global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
 }
 
 // ---- K3: reduced-cost scan of rows list[head, tail) over one column slab ----
-// Thread (g, s): segment s = 4 consecutive columns, row group g.  W = 4*S is a
-// power of two, so lanes sharing a segment differ only in their high lane bits
-// (S < 32) and a xor-shuffle tree merges them before the shared atomics.
+// Thread (g, s): segment s = 4 consecutive columns, row group g.  When W = 4*S
+// is a power of two, lanes sharing a segment differ only in their high lane
+// bits (S < 32) and a xor-shuffle tree merges them before the shared atomics.
 template <class Mem>
 __device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, int p, int head,
                                            int tail, int c0, int W, uint64_t* skey) {
@@ -248,8 +248,11 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, in
         best3 = umin64(best3, pack_key(static_cast<uint32_t>(c.w) + b, i));
       }
     }
-    // merge lanes of the same segment inside the warp
-    if (Sreal < 32) {
+    // merge lanes of the same segment inside the warp (power-of-two S only:
+    // they then differ in their high lane bits; otherwise every thread's keys
+    // go straight to the shared atomics)
+    const bool merge = Sreal < 32 && (Sreal & (Sreal - 1)) == 0;
+    if (merge) {
       for (int o = Sreal; o < 32; o <<= 1) {
         best0 = umin64(best0, __shfl_xor_sync(0xffffffffu, best0, o));
         best1 = umin64(best1, __shfl_xor_sync(0xffffffffu, best1, o));
@@ -257,7 +260,7 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, in
         best3 = umin64(best3, __shfl_xor_sync(0xffffffffu, best3, o));
       }
     }
-    const bool writer = (g < R) && (Sreal >= 32 || lane < Sreal);
+    const bool writer = (g < R) && (!merge || lane < Sreal);
     if (writer && best0 != KMB_KEY_INF) {
       unsigned long long* k4 = reinterpret_cast<unsigned long long*>(skey + 4 * s);
       atomicMin(k4 + 0, best0);
