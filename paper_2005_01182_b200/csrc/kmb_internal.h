@@ -36,6 +36,9 @@ struct Ctrl {
   int64_t rounds;
   int64_t stage_ns[6];
   int64_t seg_rows;  // (row, 4-column segment) pairs of the dirty-only epoch-start relaxes
+  // counting grid barrier (grid engine): per barrier k % 3, arrivals in bits
+  // 0-15, row appends in 16-39, free-column appends in 40-63
+  unsigned long long cbar[3];
 };
 
 struct SolverArgs {

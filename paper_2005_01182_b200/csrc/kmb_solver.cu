@@ -64,7 +64,9 @@ struct SlabSmem {
   int64_t part[kThreads / 32];
   int64_t m;
   int32_t append_base;
-  int32_t ndseg;  // dirty segments after an epoch end (-1: relax everything)
+  int32_t ndseg;              // dirty segments after an epoch end
+  int32_t my_rows, my_frees;  // this CTA's appends since the last barrier
+  int32_t tot_rows, tot_frees;  // everyone's, delivered by the counting barrier
 };
 
 // ---- where the per-row / per-column search state lives -----------------------
@@ -447,14 +449,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   // after barrier k-1, next used after barrier k+1), so a fast CTA's appends
   // never race a slow CTA's read.
   int kb = 0;
+  // Grid engine: the barrier word also carries the append totals (each CTA
+  // adds 1 | rows << 16 | frees << 40), so nobody re-reads the counters after
+  // it — one L2 round trip less per barrier.  Other engines read the counters.
+  constexpr bool kCounted = std::is_same_v<Barrier, GridBarrier> && !DSM;
+  if (tid == 0) {
+    sm.my_rows = sm.my_frees = 0;
+    sm.tot_rows = sm.tot_frees = 0;
+  }
   auto gsync = [&]() {
-    bar.sync();
+    if constexpr (kCounted) {
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long* w = &ctrl->cbar[(kb + 1) % 3];
+        const unsigned long long add = 1ull | (static_cast<unsigned long long>(sm.my_rows) << 16) |
+                                       (static_cast<unsigned long long>(sm.my_frees) << 40);
+        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(w), "l"(add) : "memory");
+        unsigned long long v;
+        do {
+          v = ld_acquire_u64(w);
+        } while ((v & 0xFFFFull) < static_cast<unsigned long long>(G));
+        sm.tot_rows = static_cast<int32_t>((v >> 16) & 0xFFFFFFull);
+        sm.tot_frees = static_cast<int32_t>(v >> 40);
+        sm.my_rows = sm.my_frees = 0;
+      }
+      __syncthreads();
+    } else {
+      bar.sync();
+    }
     ++kb;
     if (leader) {
       *M.rcnt((kb + 2) % 3) = 0;
       *M.fcnt((kb + 2) % 3) = 0;
+      if constexpr (kCounted) ctrl->cbar[(kb + 2) % 3] = 0;
     }
   };
+  auto got_rows = [&]() { return kCounted ? sm.tot_rows : M.ld(M.rcnt(kb % 3)); };
+  auto got_frees = [&]() { return kCounted ? sm.tot_frees : M.ld(M.fcnt(kb % 3)); };
   int64_t D = 0;
   int p = 0, epoch = 0, head = 0, tail = a.n;  // rows list[p][0, tail) are reached
   int nfound = 0;                              // free columns absorbed this epoch
@@ -528,7 +559,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
         const unsigned rowmask = __ballot_sync(0xffffffffu, newrow);
         if (rowmask) {
           int base = 0;
-          if (lane == 0) base = atomicAdd(rc, __popc(rowmask));
+          if (lane == 0) {
+            base = atomicAdd(rc, __popc(rowmask));
+            if (kCounted) atomicAdd(&sm.my_rows, __popc(rowmask));
+          }
           base = __shfl_sync(0xffffffffu, base, 0);
           if (newrow) {
             const int pos = tail + base + __popc(rowmask & ((1u << lane) - 1));
@@ -539,7 +573,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
         const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
         if (fmask) {
           int base = 0;
-          if (lane == 0) base = atomicAdd(fc, __popc(fmask));
+          if (lane == 0) {
+            base = atomicAdd(fc, __popc(fmask));
+            if (kCounted) atomicAdd(&sm.my_frees, __popc(fmask));
+          }
           base = __shfl_sync(0xffffffffu, base, 0);
           if (newfree) *M.found(nfound + base + __popc(fmask & ((1u << lane) - 1))) = col;
         }
@@ -566,8 +603,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     KMB_STAGE(0);
     gsync();  // ---------------------------------------------------- B1
     KMB_STAGE(1);
-    int added = M.ld(M.rcnt(kb % 3));
-    int fadded = M.ld(M.fcnt(kb % 3));
+    int added = got_rows();
+    int fadded = got_frees();
     if (added == 0 && fadded == 0) {
       // no tight column anywhere and no pending row: dual step (:201-215)
       if (wid == 0) {
@@ -592,8 +629,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
       KMB_STAGE(2);
       gsync();  // ------------------------------------------------ B2 (dual steps only)
       KMB_STAGE(3);
-      added = M.ld(M.rcnt(kb % 3));
-      fadded = M.ld(M.fcnt(kb % 3));
+      added = got_rows();
+      fadded = got_frees();
     }
     head = tail;
     tail += added;
@@ -651,6 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
         *M.u(i) = M.ld(M.u(i)) - dr + D;
       } else {
         const int pos = atomicAdd(sc, 1);
+        if (kCounted) atomicAdd(&sm.my_rows, 1);
         *M.list_row(p ^ 1, pos) = i;
         *M.list_w(p ^ 1, pos) = dr;
       }
@@ -683,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     p ^= 1;
     ++epoch;
     head = 0;
-    tail = M.ld(M.rcnt(kb % 3));  // survivors
+    tail = got_rows();  // survivors
     dirty_round = true;
     nfound = 0;
     if (ldcg(&ctrl->matched) == a.n) break;
