@@ -14,7 +14,7 @@ if [ ! -f "$REF/include/ot/hungarian.hpp" ]; then
   echo "reference headers absent; keeping prebuilt binary" ; exit 0
 fi
 mkdir -p "$HERE/build"
-g++ -O2 -std=c++20 -I"$REF/include" -I"$ROOT/include" "$HERE/test_drop_in.cpp" \
+g++ -O2 -std=c++20 -I"$REF/include" -I"$REF/tests" -I"$ROOT/include" "$HERE/test_drop_in.cpp" \
   -L"$ROOT/oracle/_ref" -lotref -L"$ROOT/paper_2005_01182_b200" -lkmb \
   -Wl,-rpath,'$ORIGIN/../../../oracle/_ref' -Wl,-rpath,'$ORIGIN/../../../paper_2005_01182_b200' \
   -o "$HERE/build/test_drop_in"

@@ -13,8 +13,11 @@
 #include "ot/core.hpp"
 #include "ot/hungarian.hpp"
 #include "kmb_ot.hpp"
+#include "testutil.hpp"  // the reference's own fixtures (proj/tests/testutil.hpp)
 
 using namespace ot;
+using ot::testing::color_style_pair;
+using ot::testing::random_unit_instance;
 
 static int g_checks = 0, g_fail = 0;
 #define CHECK(cond)                                                          \
@@ -25,17 +28,6 @@ static int g_checks = 0, g_fail = 0;
       std::fprintf(stderr, "%s:%d: CHECK(%s) failed\n", __FILE__, __LINE__, #cond); \
     }                                                                        \
   } while (0)
-
-static OTInstance random_unit_instance(std::mt19937& rng, int32_t n, int64_t max_cost) {
-  std::uniform_int_distribution<int64_t> cost(0, max_cost);
-  OTInstance inst;
-  inst.n = inst.m = n;
-  inst.cost.resize(static_cast<size_t>(n) * n);
-  for (int64_t& c : inst.cost) c = cost(rng);
-  inst.supplies.assign(n, 1);
-  inst.demands.assign(n, 1);
-  return inst;
-}
 
 static OTInstance unit_2x2() {
   OTInstance inst;
@@ -185,6 +177,21 @@ int main() {
     std::string a;
     try { solve_batched_km_b200(unit_2x2(), cfg); } catch (const std::invalid_argument& e) { a = e.what(); }
     CHECK(a == "quantize_costs: B must be positive");
+  }
+  {  // batched: iterations count phases plus dual adjustments (:191-198, seed 29)
+    std::mt19937 rng(29);
+    const OTInstance inst = random_unit_instance(rng, 30, 1000);
+    const SolveResult res = solve_batched_km_b200(inst);
+    CHECK(res.iterations >= 1);
+    CHECK(res.iterations <= static_cast<int64_t>(inst.n) * (inst.n + 1));
+  }
+  {  // km on the color-style instance (:207-212): the reference's objective and duals
+    const OTInstance inst = color_style_pair(9, "color_check");
+    DualPotentials d1, d2;
+    const SolveResult a = solve_km_b200(inst, &d1);
+    const SolveResult b = solve_km(inst, &d2);
+    CHECK(a.objective == b.objective);
+    CHECK(d1.u == d2.u && d1.v == d2.v);
   }
   // ---- auction (test_auction.cpp cases; bit-identical prices vs the reference)
   auto same_bits = [](const std::vector<double>& a, const std::vector<double>& b) {
