@@ -21,7 +21,7 @@ g++ -O2 -std=c++20 -I"$REF/include" -I"$REF/tests" -I"$ROOT/include" "$HERE/test
 # the reference harness (run_suite, make_solver, calibration rule) with the B200
 # solvers registered as SolverSpecs: the reference library is compiled from its
 # own sources for this test
-g++ -O2 -std=c++20 -I"$REF/include" -I"$ROOT/include" "$HERE/test_harness.cpp" \
+g++ -O2 -std=c++20 -I"$REF/include" -I"$REF/tests" -I"$ROOT/include" "$HERE/test_harness.cpp" \
   "$REF/src/bench.cpp" "$REF/src/core.cpp" "$REF/src/hungarian.cpp" "$REF/src/netsimplex.cpp" \
   "$REF/src/auction.cpp" "$REF/src/scaling.cpp" "$REF/src/datasets.cpp" "$REF/src/io.cpp" \
   -L"$ROOT/paper_2005_01182_b200" -lkmb \

@@ -16,7 +16,10 @@
 #include "ot/core.hpp"
 #include "ot/datasets.hpp"
 #include "ot/hungarian.hpp"
+#include "ot/netsimplex.hpp"
 #include "kmb_ot.hpp"
+#include "oracle.hpp"    // the reference's exhaustive oracles (proj/tests/oracle.hpp)
+#include "testutil.hpp"  // and fixtures (proj/tests/testutil.hpp)
 
 using namespace ot;
 
@@ -155,6 +158,53 @@ int main() {
     CHECK(recs[0].objective == recs[1].objective);  // same bids -> same matching
     CHECK(recs[2].objective == recs[2].exact_objective);
     CHECK(recs[3].objective == recs[3].exact_objective);
+  }
+  // acceptance.cpp criterion 2 (:132-159, seed 2026): every third draw a unit
+  // square; the B200 solvers' objectives equal exhaustive enumeration
+  {
+    std::mt19937 rng(2026);
+    int unit_checked = 0;
+    for (int t = 0; t < 200; ++t) {
+      const OTInstance inst =
+          t % 3 == 0 ? ot::testing::random_unit_instance(rng, 1 + static_cast<int32_t>(rng() % 4), 9)
+                     : ot::testing::random_instance(rng, 4, 9, 3);
+      const int64_t opt = ot::testing::brute_force_optimum(inst);
+      CHECK(objective_int(inst, solve_network_simplex(inst).flow) == opt);
+      if (!inst.unit_caps()) continue;
+      ++unit_checked;
+      CHECK(objective_int(inst, solve_km_b200(inst).flow) == opt);
+      BatchedKMConfig bcfg;
+      bcfg.B = std::max<int64_t>(inst.max_cost(), 1) * inst.n;
+      CHECK(objective_int(inst, solve_batched_km_b200(inst, bcfg).flow) == opt);
+      AuctionConfig acfg;
+      acfg.epsilon = 0.9 / inst.n;
+      CHECK(objective_int(inst, solve_auction_b200(inst, acfg).flow) == opt);
+    }
+    std::printf("criterion 2: 200 instances, %d unit squares checked\n", unit_checked);
+  }
+  // acceptance.cpp criterion 9 (:417-470) certificates at n = 200, costs <= 1e5:
+  // KM duals feasible and tight on the matching; batched KM (B = 64) the same
+  // against the quantized costs
+  {
+    std::mt19937 rng(909);
+    const OTInstance unit = ot::testing::random_unit_instance(rng, 200, 100000);
+    DualPotentials duals;
+    const SolveResult res = solve_km_b200(unit, &duals);
+    for (int32_t i = 0; i < unit.n; ++i)
+      for (int32_t j = 0; j < unit.n; ++j) CHECK(duals.u[i] + duals.v[j] <= unit.cost_at(i, j));
+    for (const Flow::Entry& e : res.flow.entries())
+      CHECK(duals.u[e.i] + duals.v[e.j] == unit.cost_at(e.i, e.j));
+    BatchedKMConfig cfg;
+    cfg.B = 64;
+    DualPotentials bd;
+    QuantizedCosts q;
+    const SolveResult br = solve_batched_km_b200(unit, cfg, &bd, &q);
+    for (int32_t i = 0; i < unit.n; ++i)
+      for (int32_t j = 0; j < unit.n; ++j)
+        CHECK(bd.u[i] + bd.v[j] <= q.chat[static_cast<size_t>(i) * unit.n + j]);
+    for (const Flow::Entry& e : br.flow.entries())
+      CHECK(bd.u[e.i] + bd.v[e.j] == q.chat[static_cast<size_t>(e.i) * unit.n + e.j]);
+    std::printf("criterion 9: km / batched km certificates at n = 200\n");
   }
   std::printf("harness: %d failed\n", g_fail);
   return g_fail ? 1 : 0;
