@@ -194,7 +194,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // resident (1.12 ms at 4096 vs 1.8 for CTAs)
   const bool auto_engine = engine == 0 || engine == 1 || engine == 5;
   const int cap6 = auto_engine ? kmb::cta_batch_capacity(n, c->sm_count) : 0;
-  auto pick = [&](int cnt) { return (cnt > 1 && cnt <= cap6) ? 6 : 4; };
+  auto pick = [&](int cnt) { return cnt <= cap6 ? 6 : 4; };
   if (auto_engine) engine = pick(batch);
   const int np = kmb::warp_pitch(n);
   // Host input: stream the batch in chunks, each chunk's kernel starting as soon
@@ -455,10 +455,10 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   cudaStream_t st = c->stream;
 
   int engine = c->engine;
-  // auto: one warp per instance up to n = 256 (no time budget there), one
-  // thread-block cluster up to n = 8192, the whole-GPU grid beyond (measured
-  // crossovers)
-  if (engine == 0) engine = (n <= 256 && time_budget_s <= 0.0) ? 4 : (n <= 8192 ? 5 : 1);
+  // auto: one CTA per instance up to n = 256 (no time budget there; c1 0.22 ms
+  // vs 0.55 for one warp), one thread-block cluster up to n = 8192, the
+  // whole-GPU grid beyond (measured crossovers)
+  if (engine == 0) engine = (n <= 256 && time_budget_s <= 0.0) ? 6 : (n <= 8192 ? 5 : 1);
   if ((engine == 2 || engine == 6) && n > kmb::batch_max_n()) engine = 1;
   if ((engine == 3 || engine == 4) && n > kmb::warp_max_n()) engine = 1;
   if ((engine >= 2 && engine <= 4) || engine == 6) {
