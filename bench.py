@@ -384,6 +384,9 @@ def main():
             cpu = {"value": None, "unit": "solves/s", "cores": threads, "kind": "reference",
                    "sample": f"unavailable: {e!r}"}
 
+    # the ncu DRAM bytes were captured on the 4096-instance warp-engine launch
+    traffic_used = traffic if (engine_used == 4 and count == BATCH) else None
+    dram_gbs = traffic_used / (step_ms * 1e-3) / 1e9 if traffic_used else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
@@ -396,12 +399,15 @@ def main():
                        "l2": "flushed (256 MiB write) before every timed step",
                        "engine": ENGINES.get(engine_used, (str(engine_used), ""))[0]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "frac": achieved / hbm_peak, "traffic": traffic_used,
                          "kernel": ENGINES.get(engine_used, ("", "?"))[1], "peak_source": peak_src,
+                         "dram_gbs": dram_gbs, "dram_frac": (dram_gbs / hbm_peak) if dram_gbs else None,
                          "note": "L1/L2-resident re-reads: algorithmic bytes are SURVEY 8(d)'s "
                                  "4n^2 per phase (+2 reductions) per instance, mostly served from "
                                  "L2, so achieved can exceed the HBM peak; traffic = ncu DRAM "
-                                 "bytes of one launch (profiles/ncu_batch_summary.json)"},
+                                 "bytes of one launch of this kernel on this shard "
+                                 "(profiles/ncu_batch_summary.json), dram_gbs = traffic / the "
+                                 "live per-launch time: the HBM view of the same launch"},
             "cpu_baseline": cpu,
             "e2e": {"value": BATCH / (e2e_ms * 1e-3), "unit": "solves/s",
                     "h2d_bytes_per_step": int(host.nbytes),

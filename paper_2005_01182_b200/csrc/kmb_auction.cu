@@ -35,6 +35,7 @@
 
 #include "kmb_common.cuh"
 #include "kmb_internal.h"
+#include "kmb_launch.h"
 
 #ifndef KMB_AUCTION_CLOCKS  // diagnostics: per-stage SM cycles of block 0, printed
 #define KMB_AUCTION_CLOCKS 0
@@ -660,7 +661,7 @@ template <int CPL>
 cudaError_t launch_warp(const AuctionArgs& a, int sm_count, cudaStream_t st) {
   auto k = k_auction_warp<CPL>;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, 0);
+  cudaError_t e = prepare_launch(reinterpret_cast<const void*>(k), 32, 0, -1, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const int grid = static_cast<int>(std::min<int64_t>(a.batch, static_cast<int64_t>(per_sm) * sm_count));
@@ -698,13 +699,8 @@ __global__ void __launch_bounds__(256) k_auction_minmax(const int32_t* __restric
 template <int NT>
 cudaError_t launch_nt(const AuctionArgs& a, int sm_count, size_t smem, cudaStream_t st) {
   auto k = k_auction<NT>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, smem);
+  cudaError_t e = prepare_launch(reinterpret_cast<const void*>(k), NT, smem, -1, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const int grid = static_cast<int>(std::min<int64_t>(a.batch, static_cast<int64_t>(per_sm) * sm_count));

@@ -20,6 +20,7 @@
 
 #include "kmb_common.cuh"
 #include "kmb_internal.h"
+#include "kmb_launch.h"
 
 // per-stage clock64 accounting (kmb_last_instance_stats columns 5-8): a
 // diagnostic build flag, off in production (it costs a few percent)
@@ -413,6 +414,8 @@ int batch_max_n() { return 256; }
 // Shared-memory carveout (percent) for the L2 variant: just enough for the
 // register-limited number of resident CTAs; the rest of the unified cache is L1.
 static int cta_carveout(int n) {
+  static int cache[257] = {};  // per n (0: not computed yet); benign race: same value
+  if (n >= 1 && n <= 256 && cache[n]) return cache[n];
   cudaFuncAttributes fa{};
   if (cudaFuncGetAttributes(&fa, k_cta_batch<false>) != cudaSuccess) {
     cudaGetLastError();
@@ -423,18 +426,73 @@ static int cta_carveout(int n) {
   int ctas = 65536 / (threads * (regs > 0 ? regs : 1));
   ctas = ctas < 1 ? 1 : (ctas > 32 ? 32 : ctas);
   const size_t need = static_cast<size_t>(ctas) * (cta_smem_bytes(n, false) + fa.sharedSizeBytes + 1024);
-  const int pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024));
-  return pct > 100 ? 100 : pct;
+  int pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+  pct = pct > 100 ? 100 : pct;
+  if (n >= 1 && n <= 256) cache[n] = pct;
+  return pct;
+}
+
+// ---- batch summary: per-instance stats and status folded on the device -------
+// out[0] = status of the first failing instance (0 if none), [1..4] sums of
+// epochs, dual steps, rows scanned, rounds, [5] sum and [6] max of SM cycles,
+// [7..10] summed stage cycles.  One block; replaces a batch x 11 int64 copy.
+__global__ void __launch_bounds__(1024) k_batch_summary(const int64_t* __restrict__ stats,
+                                                        const int32_t* __restrict__ status,
+                                                        int32_t batch, int64_t* __restrict__ out) {
+  constexpr int V = 11;
+  __shared__ int64_t part[32][V];
+  int64_t acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0;
+  int64_t first_bad = INT64_MAX;
+  for (int b = threadIdx.x; b < batch; b += blockDim.x) {
+    if (status[b] != 0 && b < first_bad) first_bad = b;
+    const int64_t* o = stats + static_cast<int64_t>(KMB_ISTATS) * b;
+    acc[1] += o[0];
+    acc[2] += o[1];
+    acc[3] += o[2];
+    acc[4] += o[3];
+    acc[5] += o[4];
+    acc[6] = o[4] > acc[6] ? o[4] : acc[6];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[7 + k] += o[5 + k];
+  }
+  acc[0] = first_bad;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    int64_t x = acc[k];
+    for (int off = 16; off > 0; off >>= 1) {
+      const int64_t y = __shfl_xor_sync(0xffffffffu, x, off);
+      x = (k == 0) ? (y < x ? y : x) : (k == 6 ? (y > x ? y : x) : x + y);
+    }
+    if (lane == 0) part[wid][k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < V) {
+    const int k = threadIdx.x;
+    int64_t x = part[0][k];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      const int64_t y = part[w][k];
+      x = (k == 0) ? (y < x ? y : x) : (k == 6 ? (y > x ? y : x) : x + y);
+    }
+    if (k == 0) x = x == INT64_MAX ? 0 : status[x];
+    out[k] = x;
+  }
+}
+
+cudaError_t launch_batch_summary(const int64_t* stats, const int32_t* status, int32_t batch,
+                                 int64_t* out, cudaStream_t st) {
+  k_batch_summary<<<1, 1024, 0, st>>>(stats, status, batch, out);
+  return cudaGetLastError();
 }
 
 int cta_batch_capacity(int n, int sm_count) {  // instances resident at once (L2 variant)
   if (n < 1 || n > 256) return 0;
   const int threads = ((n + 31) / 32) * 32;
   int occ = 0;
-  cudaFuncSetAttribute(k_cta_batch<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cta_carveout(n));
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cta_batch<false>, threads,
-                                                    cta_smem_bytes(n, false)) != cudaSuccess) {
+  if (prepare_launch(reinterpret_cast<const void*>(k_cta_batch<false>), threads,
+                     cta_smem_bytes(n, false), cta_carveout(n), &occ) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -448,15 +506,11 @@ cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warp
   if (smem_c && cta_smem_bytes(a.n, true) > 200 * 1024) smem_c = false;
   const size_t smem = cta_smem_bytes(a.n, smem_c);
   auto kern = smem_c ? k_cta_batch<true> : k_cta_batch<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  if (!smem_c) {  // L2 variant: leave the unified cache to L1 (0.442 -> 0.413 ms at 512)
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cta_carveout(a.n));
-    if (e != cudaSuccess) return e;
-  }
+  // L2 variant: leave the unified cache to L1 beyond the resident CTAs' state
+  // (0.442 -> 0.413 ms at 512)
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  cudaError_t e = prepare_launch(reinterpret_cast<const void*>(kern), threads, smem,
+                                 smem_c ? -1 : cta_carveout(a.n), &occ);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int wpc = threads / 32;

@@ -86,6 +86,9 @@ struct kmb_context {
   DevBuf pa, pb, pout, pbad;
   // auction workspace
   DevBuf aprice, ar2c, atot, abids, acomp, aeps, amin, amax;
+  // batch summary (device fold + pinned host copy)
+  DevBuf bsum;
+  int64_t* hsum = nullptr;
   // column-sharded solve: the collective (NCCL or caller callbacks)
   std::unique_ptr<kmb::Exchange> exchange;
   // chunked host-input pipeline of the batch engines
@@ -137,8 +140,9 @@ void kmb_destroy(kmb_context* c) {
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
                     &c->obj, &c->bcost, &c->bpad, &c->b16, &c->brmin, &c->bimin, &c->bimax, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
                     &c->bstatus, &c->pa, &c->pb, &c->pout, &c->pbad, &c->aprice, &c->ar2c, &c->atot,
-                    &c->abids, &c->acomp, &c->aeps, &c->amin, &c->amax})
+                    &c->abids, &c->acomp, &c->aeps, &c->amin, &c->amax, &c->bsum})
     b->release();
+  if (c->hsum) cudaFreeHost(c->hsum);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (int k = 0; k < kmb_context::kAux; ++k) {
@@ -322,34 +326,27 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     KMB_CUDA(cudaEventRecord(c->ev1, st));  // includes the transfers
   }
   engine = used;
-  // status is always checked (one small copy): invalid input must not pass silently
-  int32_t* hstatus = new int32_t[batch];
-  int64_t* hstat = stats ? new int64_t[static_cast<size_t>(batch) * kmb::KMB_ISTATS] : nullptr;
-  cudaError_t e = cudaMemcpyAsync(hstatus, c->bstatus.p, batch * 4, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && hstat)
-    e = cudaMemcpyAsync(hstat, c->bstat.p, static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8,
-                        cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) {
-    delete[] hstatus;
-    delete[] hstat;
-    return cuda_fail(e, who);
+  // status is always checked: invalid input must not pass silently.  Status and
+  // per-instance stats are folded on the device; one small copy comes back.
+  KMB_CUDA(c->bsum.ensure(16 * 8));
+  if (!c->hsum) KMB_CUDA(cudaMallocHost(&c->hsum, 16 * 8));
+  KMB_CUDA(kmb::launch_batch_summary(c->bstat.as<int64_t>(), c->bstatus.as<int32_t>(), batch,
+                                     c->bsum.as<int64_t>(), st));
+  KMB_CUDA(cudaMemcpyAsync(c->hsum, c->bsum.p, 11 * 8, cudaMemcpyDeviceToHost, st));
+  {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, who);
   }
-  int bad = 0;
-  for (int32_t b = 0; b < batch && !bad; ++b) bad = hstatus[b];
-  delete[] hstatus;
+  const int64_t* h = c->hsum;
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
-    for (int32_t b = 0; b < batch; ++b) {
-      const int64_t* o = hstat + kmb::KMB_ISTATS * static_cast<size_t>(b);
-      stats->phases += o[0];
-      stats->dual_steps += o[1];
-      stats->rows_scanned += o[2];
-      stats->rounds += o[3];
-      stats->sum_instance_cycles += o[4];
-      if (o[4] > stats->max_instance_cycles) stats->max_instance_cycles = o[4];
-      for (int k = 0; k < 4; ++k) stats->stage_ns[k] += o[5 + k];  // batch: SM cycles, summed
-    }
+    stats->phases = h[1];
+    stats->dual_steps = h[2];
+    stats->rows_scanned = h[3];
+    stats->rounds = h[4];
+    stats->sum_instance_cycles = h[5];
+    stats->max_instance_cycles = h[6];
+    for (int k = 0; k < 4; ++k) stats->stage_ns[k] = h[7 + k];  // batch: SM cycles, summed
     stats->cost_bytes_read = static_cast<int64_t>(batch) * n * n * 4;  // HBM: each matrix once
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
@@ -357,8 +354,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     stats->converged = 1;
     stats->engine = engine;
   }
-  delete[] hstat;
-  if (bad) return status_message(bad, who);
+  if (h[0]) return status_message(static_cast<int>(h[0]), who);
   return KMB_OK;
 }
 

@@ -117,6 +117,9 @@ struct WarpArgs {
 };
 int warp_max_n();
 int cta_batch_capacity(int n, int sm_count);  // CTA/L2 engine: instances resident at once
+// folds per-instance stats + status into 11 int64 (kmb_batch.cu)
+cudaError_t launch_batch_summary(const int64_t* stats, const int32_t* status, int32_t batch,
+                                 int64_t* out, cudaStream_t st);
 cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_t* rmin,
                           int32_t* imin, int32_t* imax, cudaStream_t st);
 int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)

@@ -28,6 +28,7 @@
 
 #include "kmb_common.cuh"
 #include "kmb_internal.h"
+#include "kmb_launch.h"
 
 namespace kmb {
 
@@ -758,19 +759,15 @@ static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, int warps_
                             cudaStream_t st, int* grid_out) {
   auto kern = k_warp_batch<CPL, SMEM_C>;
   const size_t smem = warp_smem_per_warp(a.n, a.pitch, SMEM_C) * wpb;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
   // the per-warp state lives in shared memory: ask for the largest carveout so
   // residency is set by registers, not by an L1-favouring split
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           cudaSharedmemCarveoutMaxShared);
-  if (e != cudaSuccess) return e;
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * wpb, smem);
+  cudaError_t e = prepare_launch(reinterpret_cast<const void*>(kern), 32 * wpb, smem,
+                                 cudaSharedmemCarveoutMaxShared, &occ);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
-  if (getenv("KMB_DEBUG_OCC")) {
+  static const bool debug_occ = getenv("KMB_DEBUG_OCC") != nullptr;
+  if (debug_occ) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, kern);
     fprintf(stderr, "k_warp_batch<%d,%d>: %d CTAs/SM x %d warps, dyn smem %zu B, regs %d, static smem %zu, local %zu, maxthr %d\n",
