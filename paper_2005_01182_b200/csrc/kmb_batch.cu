@@ -413,23 +413,26 @@ int batch_max_n() { return 256; }
 
 // Shared-memory carveout (percent) for the L2 variant: just enough for the
 // register-limited number of resident CTAs; the rest of the unified cache is L1.
-static int cta_carveout(int n) {
-  static int cache[257] = {};  // per n (0: not computed yet); benign race: same value
-  if (n >= 1 && n <= 256 && cache[n]) return cache[n];
-  cudaFuncAttributes fa{};
-  if (cudaFuncGetAttributes(&fa, k_cta_batch<false>) != cudaSuccess) {
-    cudaGetLastError();
-    return 100;
+// Shared-memory carveout (percent) for the L2 variant holding `want` resident
+// CTAs (capped by the register limit); the rest of the unified cache is L1.
+static int cta_carveout(int n, int want) {
+  static int regs_cached = 0;  // benign race: every thread computes the same value
+  if (!regs_cached) {
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k_cta_batch<false>) != cudaSuccess) {
+      cudaGetLastError();
+      return 100;
+    }
+    regs_cached = fa.numRegs > 0 ? fa.numRegs : 1;
   }
   const int threads = ((n + 31) / 32) * 32;
-  const int regs = ((fa.numRegs + 7) / 8) * 8;
-  int ctas = 65536 / (threads * (regs > 0 ? regs : 1));
+  const int regs = ((regs_cached + 7) / 8) * 8;
+  int ctas = 65536 / (threads * regs);
   ctas = ctas < 1 ? 1 : (ctas > 32 ? 32 : ctas);
-  const size_t need = static_cast<size_t>(ctas) * (cta_smem_bytes(n, false) + fa.sharedSizeBytes + 1024);
-  int pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024));
-  pct = pct > 100 ? 100 : pct;
-  if (n >= 1 && n <= 256) cache[n] = pct;
-  return pct;
+  if (want > 0 && want < ctas) ctas = want;
+  const size_t need = static_cast<size_t>(ctas) * (cta_smem_bytes(n, false) + 2048);
+  const int pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+  return pct > 100 ? 100 : (pct < 1 ? 1 : pct);
 }
 
 // ---- batch summary: per-instance stats and status folded on the device -------
@@ -492,7 +495,7 @@ int cta_batch_capacity(int n, int sm_count) {  // instances resident at once (L2
   const int threads = ((n + 31) / 32) * 32;
   int occ = 0;
   if (prepare_launch(reinterpret_cast<const void*>(k_cta_batch<false>), threads,
-                     cta_smem_bytes(n, false), cta_carveout(n), &occ) != cudaSuccess) {
+                     cta_smem_bytes(n, false), cta_carveout(n, 0), &occ) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -509,8 +512,9 @@ cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warp
   // L2 variant: leave the unified cache to L1 beyond the resident CTAs' state
   // (0.442 -> 0.413 ms at 512)
   int occ = 0;
+  const int want = (a.batch + sm_count - 1) / sm_count;  // CTAs per SM this batch needs
   cudaError_t e = prepare_launch(reinterpret_cast<const void*>(kern), threads, smem,
-                                 smem_c ? -1 : cta_carveout(a.n), &occ);
+                                 smem_c ? -1 : cta_carveout(a.n, want), &occ);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int wpc = threads / 32;
