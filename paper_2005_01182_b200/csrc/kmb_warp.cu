@@ -69,6 +69,9 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
 #ifndef KMB_WARP_CLAMP
 #define KMB_WARP_CLAMP 1
 #endif
+#ifndef KMB_WARP_RB4  // rows per relax batch for <= 4 columns per lane
+#define KMB_WARP_RB4 5  // A/B on c3 (tools/ab_lib.py): 4: 1.09, 5: 1.065, 6-8: 1.12, 12: 1.19 ms
+#endif
 #ifndef KMB_WARP_STAGE_CLOCKS
 #define KMB_WARP_STAGE_CLOCKS 0
 #endif
@@ -278,7 +281,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     // ---- relax rows[head, nrows)  (hungarian.cpp:164-172) ----
     int r = head;
     // RB rows in flight: entries, then all row loads, then the folds
-    constexpr int RB = CPL <= 4 ? 8 : 4;
+    constexpr int RB = CPL <= 4 ? KMB_WARP_RB4 : 4;
     if constexpr (U16) {
       // offsets arrive pre-shifted: key = min(key, (d << 8) + tag'); the last
       // short batch repeats its last row (idempotent) instead of a serial tail
