@@ -24,6 +24,9 @@
 
 // per-stage clock64 accounting (kmb_last_instance_stats columns 5-8): a
 // diagnostic build flag, off in production (it costs a few percent)
+#ifndef KMB_CTA_RB  // rows per relax batch
+#define KMB_CTA_RB 4  // A/B (tools/ab_cta.py, 512-shard): 2: .449, 3: .399, 4: .386, 5: .415, 8: .399, 16: .473 ms
+#endif
 #ifndef KMB_CTA_STAGE_CLOCKS
 #define KMB_CTA_STAGE_CLOCKS 0
 #endif
@@ -140,30 +143,30 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
     ++rounds;
     // ---- relax rows[head, nrows) for column j (hungarian.cpp:164-172) ----
     int r = head;
-    for (; r + 7 < nrows; r += 8) {
-      int2 e[8];
-      int32_t c[8];
+    for (; r + KMB_CTA_RB - 1 < nrows; r += KMB_CTA_RB) {
+      int2 e[KMB_CTA_RB];
+      int32_t c[KMB_CTA_RB];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) e[k] = rows[r + k];
+      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[r + k];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
+      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
     }
     if (nrows - r == 1) {
       const int2 e = rows[r];
       key = KO::kmin(key, KO::make(ldc<SMEM_C>(colp + e.x * n), static_cast<uint32_t>(e.y), e.x));
     } else if (r < nrows) {
-      // 2..7 rows: one batch with the last row repeated (the fold is
+      // 2..KMB_CTA_RB-1 rows: one batch with the last row repeated (the fold is
       // idempotent), so every load is in flight at once
-      int2 e[8];
-      int32_t c[8];
+      int2 e[KMB_CTA_RB];
+      int32_t c[KMB_CTA_RB];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) e[k] = rows[min(r + k, nrows - 1)];
+      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[min(r + k, nrows - 1)];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
+      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
     }
     if (rounds == 1 && a.seed == 1 && own) v = KO::val(key);  // column reduction, :328-333
     rows_scanned += nrows - head;
