@@ -58,7 +58,15 @@
 namespace kmb {
 
 constexpr int kThreads = 512;
-constexpr int kRelaxBatch = 8;  // rows in flight per thread in the scan
+#ifndef KMB_SOLVER_RB
+#define KMB_SOLVER_RB 6  // A/B: 4: c5 111.5 c4 143.4 c2 23.9; 6: 109.6 142.2 24.2; 8: 109.0 149.4 25.1 ms
+#endif
+constexpr int kSolveBatch = KMB_SOLVER_RB;  // rows in flight per thread in the solve's relax
+constexpr int kRelaxBatch = kSolveBatch;
+#ifndef KMB_SCAN_RB
+#define KMB_SCAN_RB 16  // A/B c5 full pass: 8: 5.53, 12: 6.08, 16: 6.12 TB/s
+#endif
+constexpr int kScanBatch = KMB_SCAN_RB;    // ... in the full-frontier scan (bandwidth-bound)
 
 struct SlabSmem {
   int64_t part[kThreads / 32];
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
 // Thread (g, s): segment s = 4 consecutive columns, row group g.  When W = 4*S
 // is a power of two, lanes sharing a segment differ only in their high lane
 // bits (S < 32) and a xor-shuffle tree merges them before the shared atomics.
-template <class Mem>
+template <class Mem, int kRelaxBatch = kSolveBatch>
 __device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, int p, int head,
                                            int tail, int c0, int W, uint64_t* skey) {
   const int S = W >> 2;
@@ -781,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan_all(SolverArgs a, uint64_t
   const int W = a.W, c0 = blockIdx.x * W;
   for (int c = threadIdx.x; c < W; c += kThreads) skey[c] = KMB_KEY_INF;
   __syncthreads();
-  relax_slab(a, GMem{&a}, 0, 0, a.n, c0, W, skey);
+  relax_slab<GMem, kScanBatch>(a, GMem{&a}, 0, 0, a.n, c0, W, skey);
   __syncthreads();
   for (int c = threadIdx.x; c < W; c += kThreads)
     if (c0 + c < a.n) keys_out[c0 + c] = skey[c];
