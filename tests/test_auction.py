@@ -212,3 +212,18 @@ def test_gpu_calibrate_matches_reference_procedure(solver):
         return best
 
     assert calibrate_auction_eps(c, exact, solver=solver) == ref_calibrate()
+
+
+@pytest.mark.gpu
+def test_gpu_time_budget_partial_result(solver):
+    """auction.cpp:140-144: the clock is checked every 1024 bids and an expired
+    budget returns the partial matching with converged = false.  (Where the
+    clock starts differs — the reference's host clock before the run, the
+    kernel's at instance start — so the stopping bid is not compared.)"""
+    c = W.CONFIGS["c2"].make()
+    full = O.ref_solve_auction(c, 1.0)
+    o = solver.auction(c, False, 1.0, time_budget_s=1e-7)
+    assert not o["converged"]
+    assert int(o["bids"]) % 1024 == 0 and int(o["bids"]) < full.iterations
+    r2c = o["row_to_col"][o["row_to_col"] >= 0]
+    assert len(np.unique(r2c)) == len(r2c)  # a partial matching
