@@ -10,7 +10,7 @@
  * The reference interface is C++ (OTInstance in, SolveResult + optional
  * DualPotentials / Matching out, exceptions on bad input); this ABI carries the
  * same data as plain pointers and sizes so any FFI can bind it, and
- * include/kmb.hpp rebuilds the reference's C++ signatures on top of it.
+ * include/kmb_ot.hpp rebuilds the reference's C++ signatures on top of it.
  *
  * Semantics (identical to the reference on the same inputs):
  *   cost         n x n int32, row-major with leading dimension ld (>= n),
@@ -28,10 +28,10 @@
  *   time_budget_s  0 = none; checked once per phase on the device
  *                (hungarian.cpp:341-346); on expiry stats->converged = 0 and the
  *                partial matching is returned (row_to_col = -1 for free rows).
- * Pointers may be host or device memory (detected per call).  A call whose
- * pointers are all device memory and whose stats pointer is NULL is
- * asynchronous on the context's stream; otherwise it returns after the result
- * reached the caller's buffers.
+ * Pointers may be host or device memory (detected per call).  Work runs on the
+ * context's stream (kmb_set_stream); every call returns after the results
+ * reached the caller's buffers and the device status was checked, like the
+ * reference's synchronous functions.
  *
  * Return value: 0 ok; > 0 invalid input (message via kmb_last_error(), the
  * reference's std::invalid_argument cases); < 0 CUDA / internal error.

@@ -4,7 +4,7 @@
 and ``ot::solve_batched_km`` (hungarian.cpp:313-381): cost matrix in; assignment,
 total cost and row/column duals out; the same exceptions with the same
 messages (``ValueError`` standing in for ``std::invalid_argument``).  The C++
-mirror with the reference's exact types is ``include/kmb.hpp``; this module is
+mirror with the reference's exact types is ``include/kmb_ot.hpp``; this module is
 what the tests and ``bench.py`` use.
 
 Every call goes through ``libkmb.so`` (CUDA, sm_100a).  There is no CPU path:
