@@ -166,7 +166,8 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
     case KMB_OPT_WARPS_PER_SM: c->warps_per_sm = value; return KMB_OK;
     case KMB_OPT_U16: c->u16 = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_ENGINE:
-      if (value < 0 || value > 6) return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..6");
+      if (value < 0 || value > 8 || value == 7)
+        return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..6 or 8");
       c->engine = static_cast<int>(value);
       return KMB_OK;
     default: return fail(KMB_EINVAL, "kmb_set_option: unknown option");
@@ -187,9 +188,13 @@ static int status_message(int status, const char* who) {
                                  std::to_string(status) + ")");
 }
 
+// instance status of a time budget that expired (single-CTA engine): not an error
+constexpr int64_t kStopped = 4;
+
 static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch, int32_t n,
                             int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
-                            int64_t* total_cost, kmb_stats* stats, const char* who, int engine) {
+                            int64_t* total_cost, kmb_stats* stats, const char* who, int engine,
+                            double time_budget_s = 0.0) {
   cudaStream_t st = c->stream;
   const size_t cbytes = static_cast<size_t>(batch) * n * n * sizeof(int32_t);
   // auto: a batch (or pipeline chunk) that fits the CTA engine's residency in
@@ -198,7 +203,8 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // resident (1.12 ms at 4096 vs 1.8 for CTAs)
   const bool auto_engine = engine == 0 || engine == 1 || engine == 5;
   const int cap6 = auto_engine ? kmb::cta_batch_capacity(n, c->sm_count) : 0;
-  auto pick = [&](int cnt) { return cnt <= cap6 ? 6 : 4; };
+  // n > 256: one 1024-thread CTA per instance (single-CTA engine, n <= 4096)
+  auto pick = [&](int cnt) { return n > kmb::warp_max_n() ? 8 : (cnt <= cap6 ? 6 : 4); };
   if (auto_engine) engine = pick(batch);
   const int np = kmb::warp_pitch(n);
   // Host input: stream the batch in chunks, each chunk's kernel starting as soon
@@ -236,6 +242,23 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // instances [lo, lo + cnt) on engine eng, stream s
   auto launch = [&](int lo, int cnt, int eng, cudaStream_t s) -> cudaError_t {
     const size_t ro = static_cast<size_t>(lo) * n;
+    if (eng == 8) {
+      kmb::BigArgs a{};
+      a.C = dcost + ro * n;
+      a.ld = n;
+      a.inst_stride = static_cast<int64_t>(n) * n;
+      a.batch = cnt;
+      a.n = n;
+      a.seed = seed;
+      a.deadline_ns = time_budget_s > 0.0 ? static_cast<int64_t>(time_budget_s * 1e9) : 0;
+      a.row_to_col = dr2c + ro;
+      a.u = du + ro;
+      a.v = dv + ro;
+      a.total_cost = dtot + lo;
+      a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
+      a.status = c->bstatus.as<int32_t>() + lo;
+      return kmb::launch_big(a, c->sm_count, s);
+    }
     if (eng == 2 || eng == 6) {
       kmb::BatchArgs a{};
       a.C = dcost + ro * n;
@@ -351,10 +374,10 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     stats->seconds = ms * 1e-3;
-    stats->converged = 1;
+    stats->converged = h[0] == kStopped ? 0 : 1;
     stats->engine = engine;
   }
-  if (h[0]) return status_message(static_cast<int>(h[0]), who);
+  if (h[0] && h[0] != kStopped) return status_message(static_cast<int>(h[0]), who);
   return KMB_OK;
 }
 
@@ -366,9 +389,11 @@ int kmb_solve_batch_i32(kmb_context* c, const int32_t* costs, int32_t batch, int
   if (batch <= 0 || n <= 0) return fail(KMB_EINVAL, "kmb_solve_batch_i32: dimensions must be positive");
   if (!costs) return fail(KMB_EINVAL, "kmb_solve_batch_i32: costs is NULL");
   if (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED) return fail(KMB_EINVAL, "kmb_solve_batch_i32: bad seed");
-  if (n > kmb::warp_max_n())
-    return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > " + std::to_string(kmb::warp_max_n()) +
+  if (n > kmb::big_max_n())
+    return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > " + std::to_string(kmb::big_max_n()) +
                                 " (use kmb_solve_i32 per instance)");
+  if (n > kmb::warp_max_n() && c->engine != 0 && c->engine != 8)
+    return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > 256 needs the single-CTA engine (8)");
   KMB_CUDA(cudaSetDevice(c->device));
   return solve_batch_impl(c, costs, batch, n, seed, row_to_col, u, v, total_cost, stats, who,
                           c->engine);
@@ -451,14 +476,18 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   cudaStream_t st = c->stream;
 
   int engine = c->engine;
-  // auto: one CTA per instance up to n = 256 (no time budget there; c1 0.22 ms
-  // vs 0.55 for one warp), one thread-block cluster up to n = 8192, the
-  // whole-GPU grid beyond (measured crossovers)
-  if (engine == 0) engine = (n <= 256 && time_budget_s <= 0.0) ? 6 : (n <= 8192 ? 5 : 1);
+  // auto (measured crossovers): one CTA per instance up to
+  // n = 256 (no time budget there; c1 0.20 ms vs 0.55 for one warp), one
+  // 1024-thread CTA up to n = 3072 (c2 10 ms vs 24 on a cluster), one
+  // thread-block cluster up to n = 8192 (c4: 129 vs 159 ms on one CTA), the
+  // whole-GPU grid beyond
+  if (engine == 0)
+    engine = (n <= 256 && time_budget_s <= 0.0) ? 6 : n <= 3072 ? 8 : (n <= 8192 ? 5 : 1);
   if ((engine == 2 || engine == 6) && n > kmb::batch_max_n()) engine = 1;
   if ((engine == 3 || engine == 4) && n > kmb::warp_max_n()) engine = 1;
-  if ((engine >= 2 && engine <= 4) || engine == 6) {
-    if (time_budget_s > 0.0)
+  if (engine == 8 && n > kmb::big_max_n()) engine = 1;
+  if ((engine >= 2 && engine <= 4) || engine == 6 || engine == 8) {
+    if (time_budget_s > 0.0 && engine != 8)
       return fail(KMB_EINVAL, "kmb_solve_i32: the per-instance engines have no time budget; use engine 1");
     const int32_t* src = cost;
     if (ld != n) {  // compact into the batch buffer
@@ -466,7 +495,8 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
       KMB_CUDA(cudaMemcpy2DAsync(c->bcost.p, n * 4, cost, ld * 4, n * 4, n, cudaMemcpyDefault, st));
       src = c->bcost.as<int32_t>();
     }
-    return solve_batch_impl(c, src, 1, n, seed, row_to_col, u, v, total_cost, stats, who, engine);
+    return solve_batch_impl(c, src, 1, n, seed, row_to_col, u, v, total_cost, stats, who, engine,
+                            time_budget_s);
   }
 
   const bool cluster = engine == 5;

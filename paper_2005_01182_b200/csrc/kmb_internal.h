@@ -125,6 +125,23 @@ cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_
 int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)
 cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int warps_per_sm,
                               cudaStream_t st, int* grid_out);
+// single-CTA engine for 256 < n <= 4096 (kmb_big.cu)
+struct BigArgs {
+  const int32_t* C;     // batch instances, row stride ld, instance stride inst_stride
+  int64_t ld, inst_stride;
+  int32_t batch, n, seed;
+  int64_t deadline_ns;  // per-instance time budget (0: none)
+  int32_t* row_to_col;  // batch x n
+  int64_t* u;           // batch x n
+  int64_t* v;           // batch x n
+  int64_t* total_cost;  // batch
+  int64_t* stats;       // batch x KMB_ISTATS (may be null)
+  int32_t* status;      // batch
+  int32_t* converged;   // batch (may be null)
+};
+size_t big_smem_bytes(int n);
+int big_max_n();
+cudaError_t launch_big(const BigArgs& a, int sm_count, cudaStream_t st);
 // Gauss-Seidel auction (kmb_auction.cu)
 struct AuctionArgs {
   const int32_t* C;     // batch instances, row stride ld, instance stride inst_stride

@@ -108,7 +108,7 @@ def test_known_constant(solver):  # :133-142: constant 6x6 cost 4 -> 24, one pha
     assert r.stats["dual_steps"] == 0
 
 
-@pytest.mark.parametrize("engine", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("engine", [1, 2, 3, 4, 5, 6, 8])
 @pytest.mark.parametrize("seed", [KMB_SEED_KM, KMB_SEED_BATCHED])
 def test_random_small_vs_reference(solver, engine, seed):
     rng = np.random.default_rng(100 + 10 * engine + seed)
@@ -126,8 +126,9 @@ def test_random_small_vs_reference(solver, engine, seed):
         solver.set_option(OPT_ENGINE, 0)
 
 
-@pytest.mark.parametrize("engine", [1, 5])
-@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 13, 31, 33, 127, 129, 200, 255, 257, 300, 513, 1000, 1001])
+@pytest.mark.parametrize("engine", [1, 5, 8])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 13, 31, 33, 127, 129, 200, 255, 257, 300, 513, 1000, 1001,
+                               1025, 2049, 3000])
 def test_ragged_sizes_grid(solver, n, engine):
     rng = np.random.default_rng(n)
     c = rng.integers(0, 5000, size=(n, n)).astype(np.int32)
@@ -176,7 +177,7 @@ def test_matching_equals_mirror(solver):
         n = int(rng.integers(2, 300))
         c = rng.integers(0, 20, size=(n, n)).astype(np.int32)
         mi = O.mirror_solve_incr(c, 1)
-        engines = [1, 5] + ([2, 3, 4, 6] if n <= 256 else [])
+        engines = [1, 5, 8] + ([2, 3, 4, 6] if n <= 256 else [])
         for engine in engines:
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, KMB_SEED_BATCHED)
@@ -211,7 +212,7 @@ def test_out_of_device_range_rejected(solver):
     check_against(solver.solve(c, KMB_SEED_BATCHED), ref, c)
 
 
-@pytest.mark.parametrize("engine", [1, 5])
+@pytest.mark.parametrize("engine", [1, 5, 8])
 def test_time_budget(solver, engine):
     c = W.CONFIGS["c2"].make()
     solver.set_option(OPT_ENGINE, engine)
@@ -449,3 +450,18 @@ def test_cluster_engine_dsm_and_global_agree(solver):
         np.testing.assert_array_equal(r1.v, ref.v)
         np.testing.assert_array_equal(r1.row_to_col, r2.row_to_col)
         assert r1.stats["rounds"] == r2.stats["rounds"]
+
+
+@pytest.mark.gpu
+def test_batch_mid_size_instances(solver):
+    """kmb_solve_batch_i32 with 256 < n <= 4096: one 1024-thread CTA per
+    instance (engine 8); every instance equals the reference."""
+    rng = np.random.default_rng(31)
+    for n, hi in ((300, 1000), (1100, 10**6)):
+        c = rng.integers(0, hi, size=(5, n, n)).astype(np.int32)
+        r = solver.solve_batch(c)
+        for t in range(c.shape[0]):
+            ref = O.ref_solve_batched_km(c[t])
+            np.testing.assert_array_equal(r.u[t], ref.u)
+            np.testing.assert_array_equal(r.v[t], ref.v)
+            assert int(r.total_cost[t]) == ref.total_cost
