@@ -1,4 +1,4 @@
-// Single-CTA engine ("big CTA", KMB_OPT_ENGINE 8): one 1024-thread CTA solves
+// Single-CTA engine ("big CTA", KMB_OPT_ENGINE 8): one 512-thread CTA solves
 // one instance with 256 < n <= 4096 — configs 2 and 4 — entirely inside one SM.
 //
 // Why: those instances are latency-bound (c2: 6,709 rounds relaxing ~2 rows
@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kmb_common.cuh"
@@ -48,7 +49,6 @@ namespace kmb {
 namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
-constexpr int kT = 1024;
 
 // packed key: ((c - w + 2^30) << 32) | row — min = smallest reduced cost, ties
 // to the smallest row (kmb_common.cuh)
@@ -78,7 +78,7 @@ struct BigShared {
   unsigned long long tot;
 };
 
-template <int CPT>
+template <int CPT, int kT>
 __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BigShared sm;
@@ -450,22 +450,45 @@ size_t big_smem_bytes(int n) { return static_cast<size_t>(n) * (8 + 8 + 4 * 10);
 
 int big_max_n() { return 4096; }
 
-cudaError_t launch_big(const BigArgs& a, int sm_count, cudaStream_t st) {
-  if (a.n < 1 || a.n > big_max_n()) return cudaErrorInvalidValue;
-  const size_t smem = big_smem_bytes(a.n);
-  const int cpt = (a.n + kT - 1) / kT;
-  const void* k = cpt <= 1 ? reinterpret_cast<const void*>(k_big<1>)
-                 : cpt <= 2 ? reinterpret_cast<const void*>(k_big<2>)
-                            : reinterpret_cast<const void*>(k_big<4>);
+template <int CPT, int NT>
+static cudaError_t launch_nt(const BigArgs& a, int sm_count, size_t smem, cudaStream_t st) {
+  const void* k = reinterpret_cast<const void*>(k_big<CPT, NT>);
   int occ = 0;
-  cudaError_t e = prepare_launch(k, kT, smem, 100, &occ);
+  cudaError_t e = prepare_launch(k, NT, smem, 100, &occ);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int grid = static_cast<int>(std::min<int64_t>(a.batch, static_cast<int64_t>(occ) * sm_count));
-  if (cpt <= 1) k_big<1><<<grid, kT, smem, st>>>(a);
-  else if (cpt <= 2) k_big<2><<<grid, kT, smem, st>>>(a);
-  else k_big<4><<<grid, kT, smem, st>>>(a);
+  k_big<CPT, NT><<<grid, NT, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_big(const BigArgs& a, int sm_count, cudaStream_t st) {
+  if (a.n < 1 || a.n > big_max_n()) return cudaErrorInvalidValue;
+  const size_t smem = big_smem_bytes(a.n);
+  // threads per CTA: a lone SM is issue-bound, so columns per thread trade
+  // per-warp overhead against per-thread work.  Measured (c2 / c4 / uniform
+  // n=2048 / geometric n=3072, ms): 1024 threads 8.88 / 158 / 16.2 / 107,
+  // 512: 8.85 / 157 / 14.1 / 103, 256: 10.9 / 214 / 17.2 / 135.
+  // KMB_BIG_THREADS (256 / 512 / 1024) overrides for A/B runs.
+  static const int nt_env = getenv("KMB_BIG_THREADS") ? atoi(getenv("KMB_BIG_THREADS")) : 0;
+  int nt = nt_env ? nt_env : 512;
+  const int cpt = (a.n + nt - 1) / nt;
+  if (nt == 256) {
+    if (cpt <= 1) return launch_nt<1, 256>(a, sm_count, smem, st);
+    if (cpt <= 2) return launch_nt<2, 256>(a, sm_count, smem, st);
+    if (cpt <= 4) return launch_nt<4, 256>(a, sm_count, smem, st);
+    if (cpt <= 8) return launch_nt<8, 256>(a, sm_count, smem, st);
+    return launch_nt<16, 256>(a, sm_count, smem, st);
+  }
+  if (nt == 512) {
+    if (cpt <= 1) return launch_nt<1, 512>(a, sm_count, smem, st);
+    if (cpt <= 2) return launch_nt<2, 512>(a, sm_count, smem, st);
+    if (cpt <= 4) return launch_nt<4, 512>(a, sm_count, smem, st);
+    return launch_nt<8, 512>(a, sm_count, smem, st);
+  }
+  if (cpt <= 1) return launch_nt<1, 1024>(a, sm_count, smem, st);
+  if (cpt <= 2) return launch_nt<2, 1024>(a, sm_count, smem, st);
+  return launch_nt<4, 1024>(a, sm_count, smem, st);
 }
 
 }  // namespace kmb
