@@ -240,6 +240,40 @@ def extras_c5(solver, hbm_peak: float) -> dict:
             "segment_rows": st.segment_rows}
 
 
+def extras_single(solver) -> dict:
+    """Configs 1, 2 and 4 (single instances, device-resident): best of 3 solves
+    on the auto-selected engine, total cost checked against the committed golden."""
+    import torch
+    from paper_2005_01182_b200 import workloads as W
+    names = {6: "CTA", 8: "single-CTA (512 threads)", 5: "cluster (DSMEM state)", 1: "grid"}
+    golden = {}
+    gp = os.path.join(ROOT, "tests", "golden", "configs.json")
+    if os.path.exists(gp):
+        with open(gp) as f:
+            golden = json.load(f)
+    out = {}
+    for key in ("c1", "c2", "c4"):
+        c = W.CONFIGS[key].make()
+        n = c.shape[0]
+        dc = torch.from_numpy(c).cuda()
+        r2c = torch.empty(n, dtype=torch.int32, device="cuda")
+        u = torch.empty(n, dtype=torch.int64, device="cuda")
+        v = torch.empty(n, dtype=torch.int64, device="cuda")
+        tot = torch.empty(1, dtype=torch.int64, device="cuda")
+        best, st = None, None
+        for _ in range(3):
+            st = solver.solve_into(dc, n, n, 1, r2c, u, v, tot)
+            best = st.seconds if best is None else min(best, st.seconds)
+        g = golden.get(key, {})
+        ok = None
+        if "total_cost" in g and "u_fnv" in g and "v_fnv" in g:  # reference's cost and duals
+            ok = (int(tot[0]) == int(g["total_cost"])
+                  and W.fnv1a64(u.cpu().numpy()) == g["u_fnv"] and W.fnv1a64(v.cpu().numpy()) == g["v_fnv"])
+        out[key] = {"n": n, "solve_ms": 1e3 * best, "engine": names.get(st.engine, str(st.engine)),
+                    "rounds": st.rounds, "total_cost": int(tot[0]), "matches_reference_golden": ok}
+    return out
+
+
 def extras_auction(solver) -> dict:
     """Config-3 batch through the GPU auction (ot::solve_auction_scaled, exact
     schedule; device-resident costs), and the unmodified reference auction on
@@ -368,6 +402,7 @@ def main():
         if not args.no_extras:
             extras = {}
             for key, fn in (("c5", lambda: extras_c5(solver, hbm_peak)),
+                            ("single_instances", lambda: extras_single(solver)),
                             ("auction_c3", lambda: extras_auction(solver))):
                 try:
                     extras[key] = fn()
