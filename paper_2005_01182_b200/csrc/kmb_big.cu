@@ -30,6 +30,12 @@
 #include "kmb_internal.h"
 #include "kmb_launch.h"
 
+// survivor rows in flight per thread in the dirty-column recompute.  More does
+// not help (c4: 8: 156, 16: 168, 32: 191 ms): the gathers are 4-byte loads
+// from scattered sectors, bound by the SM's L1 request rate, not latency.
+#ifndef KMB_BIG_GB
+#define KMB_BIG_GB 8
+#endif
 #ifndef KMB_BIG_CLOCKS  // diagnostics: thread 0's stage cycles, printed per instance
 #define KMB_BIG_CLOCKS 0
 #endif
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
             const int k = item % nd, g = item / nd;
             const int col = dlist[k];
             uint64_t best = ~0ull;
-            constexpr int GB = 8;
+            constexpr int GB = KMB_BIG_GB;
             for (int r = g; r < nrows; r += groups * GB) {
               int2 e[GB];
               int32_t c[GB];
