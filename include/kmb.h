@@ -63,10 +63,14 @@ enum kmb_status {
 enum kmb_option {
   KMB_OPT_MAX_CTAS = 1,     /* grid engine: upper bound on CTAs (0 = #SMs)      */
   KMB_OPT_CONTINUE_BFS = 2, /* 1: exhaust the tight closure before augmenting   */
-  KMB_OPT_ENGINE = 3,       /* 0 auto (warp n<=256, cluster n<=8192, grid),
+  KMB_OPT_ENGINE = 3,       /* 0 auto: single instances CTA n<=256, single-CTA
+                               n<=3072, cluster n<=8192, grid beyond; batches
+                               warp or CTA (n<=256, by residency), single-CTA
+                               (n<=4096);
                                1 grid (persistent), 2 CTA/SMEM, 6 CTA/L2,
                                3 warp/SMEM, 4 warp/L2 (2,3,4,6: n <= 256),
-                               5 cluster (grid engine on one <=16-CTA cluster);
+                               5 cluster (grid engine on one <=16-CTA cluster),
+                               8 single-CTA (one 512-thread CTA, n <= 4096);
                                stats->engine 7 = column-sharded              */
   KMB_OPT_WARPS_PER_SM = 4, /* warp engine: resident instances per SM (0 = max);
                                bounds the L2 working set of streamed matrices   */
@@ -109,7 +113,8 @@ int kmb_solve_i32(kmb_context* ctx, const int32_t* cost, int32_t n, int64_t ld, 
                   double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
                   int64_t* total_cost, kmb_stats* stats);
 
-/* `batch` independent n x n instances stored back to back (config 3).
+/* `batch` independent n x n instances stored back to back (config 3); n <= 4096
+ * (one warp or one CTA per instance for n <= 256, one 512-thread CTA above).
  * row_to_col, u, v: batch*n entries; total_cost: batch entries; stats (optional)
  * receives the sums over the batch. */
 int kmb_solve_batch_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, int32_t n,
