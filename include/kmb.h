@@ -64,7 +64,7 @@ enum kmb_option {
   KMB_OPT_MAX_CTAS = 1,     /* grid engine: upper bound on CTAs (0 = #SMs)      */
   KMB_OPT_CONTINUE_BFS = 2, /* 1: exhaust the tight closure before augmenting   */
   KMB_OPT_ENGINE = 3,       /* 0 auto: single instances CTA n<=256, single-CTA
-                               n<=3072, cluster n<=8192, grid beyond; batches
+                               n<=3072, cluster n<=5120, grid beyond; batches
                                warp or CTA (n<=256, by residency), single-CTA
                                (n<=4096);
                                1 grid (persistent), 2 CTA/SMEM, 6 CTA/L2,

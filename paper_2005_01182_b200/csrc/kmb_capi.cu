@@ -478,11 +478,12 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   int engine = c->engine;
   // auto (measured crossovers): one CTA per instance up to
   // n = 256 (no time budget there; c1 0.20 ms vs 0.55 for one warp), one
-  // 1024-thread CTA up to n = 3072 (c2 10 ms vs 24 on a cluster), one
-  // thread-block cluster up to n = 8192 (c4: 129 vs 159 ms on one CTA), the
-  // whole-GPU grid beyond
+  // 512-thread CTA up to n = 3072 (c2 8.9 ms vs 24 on a cluster), one
+  // thread-block cluster up to n = 5120 (c4: 129 ms vs 157 on one CTA, 160 on
+  // the grid), the whole-GPU grid beyond (n = 6144: 64 vs 78 ms uniform,
+  // 269 vs 298 geometric)
   if (engine == 0)
-    engine = (n <= 256 && time_budget_s <= 0.0) ? 6 : n <= 3072 ? 8 : (n <= 8192 ? 5 : 1);
+    engine = (n <= 256 && time_budget_s <= 0.0) ? 6 : n <= 3072 ? 8 : (n <= 5120 ? 5 : 1);
   if ((engine == 2 || engine == 6) && n > kmb::batch_max_n()) engine = 1;
   if ((engine == 3 || engine == 4) && n > kmb::warp_max_n()) engine = 1;
   if (engine == 8 && n > kmb::big_max_n()) engine = 1;
