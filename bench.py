@@ -48,31 +48,65 @@ def peaks() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region.  NVML is
+    polled every ~2 ms from a thread (the timed regions last tens of ms, too short
+    for nvidia-smi's ~100 ms per query); nvidia-smi is the fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.samples: list[list[str]] = []
+        self.samples: list[tuple[float, float, tuple]] = []
+        self.source = "nvidia-smi"
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            self._nvml = pynvml
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        return float(sm), float(mx), tuple(bool(r & b) for b in bits)
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5)
+        if out.returncode != 0 or not out.stdout.strip():
+            return None
+        s = [x.strip() for x in out.stdout.strip().split(",")]
+        return float(s[0]), float(s[1]), tuple(x.lower() == "active" for x in s[2:6])
 
     def _run(self):
-        while not self._stop.is_set():
+        while True:
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+                smp = self._sample_nvml() if self._nvml else self._sample_smi()
+                if smp:
+                    self.samples.append(smp)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            if self._stop.wait(0.002 if self._nvml else 0.2):
+                break
 
-    def __enter__(self):
+    def __enter__(self):  # re-enterable: samples of every region accumulate
+        self._stop.clear()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -85,14 +119,10 @@ class ClockSampler:
     def summary(self) -> dict:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        reasons = sorted({self.NAMES[k] for s in self.samples for k in range(4) if s[2][k]})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": self.source}
 
 
 _BACKEND = "gloo"
@@ -308,7 +338,7 @@ def extras_auction(solver) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-extras", action="store_true")
@@ -352,7 +382,8 @@ def main():
     engine_used = 4
     barrier(world)
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    clk = ClockSampler(local)
+    with clk:
         for k in range(args.steps):
             flush.fill_(k)
             ev[k][0].record(stream)
@@ -373,12 +404,13 @@ def main():
               for _ in range(args.steps)]
     barrier(world)
     torch.cuda.synchronize()
-    for k in range(args.steps):
-        flush.fill_(k)
-        e2e_ev[k][0].record(stream)
-        solver.solve_batch_into(hcost, count, N, 1, hr2c, hu, hv, htot, stats=False)
-        e2e_ev[k][1].record(stream)
-    torch.cuda.synchronize()
+    with clk:
+        for k in range(args.steps):
+            flush.fill_(k)
+            e2e_ev[k][0].record(stream)
+            solver.solve_batch_into(hcost, count, N, 1, hr2c, hu, hv, htot, stats=False)
+            e2e_ev[k][1].record(stream)
+        torch.cuda.synchronize()
     e2e_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in e2e_ev), world)
     ok_e2e = bool(torch.equal(hr2c, r2c.cpu())) and bool(torch.equal(htot, dtot.cpu()))
 

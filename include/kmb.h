@@ -74,9 +74,17 @@ enum kmb_option {
                                stats->engine 7 = column-sharded              */
   KMB_OPT_WARPS_PER_SM = 4, /* warp engine: resident instances per SM (0 = max);
                                bounds the L2 working set of streamed matrices   */
-  KMB_OPT_U16 = 5           /* warp/L2 engine (n in 65..256): stream 16-bit
+  KMB_OPT_U16 = 5,          /* warp/L2 engine (n in 65..256): stream 16-bit
                                offsets from the row minima, exact (rows with an
                                offset >= 65535 fall back to int32); 0 = default */
+  KMB_OPT_PIPELINE = 6      /* host-input batches (>= 256 instances): chunks the
+                               H2D copy is split into so solves overlap it.
+                               0 = auto (tapered: min(8, batch/128) equal
+                               chunks, the last one split by halving so the
+                               solve after the final copy is short; measured
+                               on config 3, tools/e2e_probe.py);
+                               k > 0: k equal chunks (<= 64);
+                               k < 0: tapered from |k| equal chunks            */
 };
 
 typedef struct kmb_stats {

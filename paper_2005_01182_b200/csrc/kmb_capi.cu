@@ -75,6 +75,7 @@ struct kmb_context {
   int64_t max_ctas = 0;
   int64_t warps_per_sm = 0;  // warp engine residency bound (0 = occupancy limit)
   int64_t u16 = 0;           // warp/L2 engine: 16-bit row-offset packing (opt-in)
+  int64_t pipeline = 0;      // host-input batches: chunk schedule (0 = tapered auto)
   int continue_bfs = 0;
   int engine = 0;
   // grid-engine workspace
@@ -92,9 +93,11 @@ struct kmb_context {
   // column-sharded solve: the collective (NCCL or caller callbacks)
   std::unique_ptr<kmb::Exchange> exchange;
   // chunked host-input pipeline of the batch engines
-  static constexpr int kAux = 4;
+  static constexpr int kAux = 4, kMaxChunks = 64;
   cudaStream_t aux[kAux] = {};
   cudaEvent_t aux_ev[kAux] = {};
+  cudaStream_t cin = nullptr;             // H2D copies of the chunks, in order
+  cudaEvent_t in_ev[kMaxChunks] = {};     // chunk k landed
 };
 
 namespace kmb {
@@ -149,6 +152,9 @@ void kmb_destroy(kmb_context* c) {
     if (c->aux_ev[k]) cudaEventDestroy(c->aux_ev[k]);
     if (c->aux[k]) cudaStreamDestroy(c->aux[k]);
   }
+  for (int k = 0; k < kmb_context::kMaxChunks; ++k)
+    if (c->in_ev[k]) cudaEventDestroy(c->in_ev[k]);
+  if (c->cin) cudaStreamDestroy(c->cin);
   delete c;
 }
 
@@ -165,6 +171,11 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
     case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_WARPS_PER_SM: c->warps_per_sm = value; return KMB_OK;
     case KMB_OPT_U16: c->u16 = value ? 1 : 0; return KMB_OK;
+    case KMB_OPT_PIPELINE:
+      if (value < -(kmb_context::kMaxChunks / 2) || value > kmb_context::kMaxChunks)
+        return fail(KMB_EINVAL, "kmb_set_option: pipeline chunk count out of range");
+      c->pipeline = value;
+      return KMB_OK;
     case KMB_OPT_ENGINE:
       if (value < 0 || value > 8 || value == 7)
         return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..6 or 8");
@@ -213,7 +224,32 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   const bool host_in = !is_device_ptr(costs);
   const bool warp_eng = engine == 3 || engine == 4;
   const bool pipelined = host_in && batch >= 256 && (!warp_eng || np == n);
-  const int K = pipelined ? std::min(8, batch / 64) : 1;
+  // chunk schedule [lo, lo + cnt): K equal chunks, and (tapered) the last one
+  // split by halving down to 32 instances, so the solve left after the final
+  // copy lands is a short one
+  std::vector<std::pair<int, int>> sched;
+  if (pipelined) {
+    const int64_t opt = c->pipeline;
+    const int K = opt > 0 ? static_cast<int>(std::min<int64_t>(opt, batch))
+                          : opt < 0 ? std::min<int>(static_cast<int>(-opt), batch / 64)
+                                    : std::max(2, std::min(8, batch / 128));
+    const bool taper = opt <= 0;
+    const int chunk = (batch + K - 1) / K;
+    int lo = 0;
+    for (int k = 0; k < K && lo < batch; ++k) {
+      int cnt = std::min(chunk, batch - lo);
+      if (taper && lo + cnt >= batch) {  // the last chunk: halve it down
+        while (cnt > 64 && static_cast<int>(sched.size()) < kmb_context::kMaxChunks - 1) {
+          const int h = cnt / 2;
+          sched.emplace_back(lo, h);
+          lo += h;
+          cnt -= h;
+        }
+      }
+      sched.emplace_back(lo, cnt);
+      lo += cnt;
+    }
+  }
   const int32_t* dcost = costs;
   if (host_in) {
     KMB_CUDA(c->bcost.ensure(cbytes));
@@ -330,21 +366,34 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
         KMB_CUDA(cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming));
       }
     }
-    const int chunk = (batch + K - 1) / K;
-    for (int k = 0; k < K; ++k) {
-      const int lo = k * chunk, cnt = std::min(chunk, batch - lo);
-      if (cnt <= 0) break;
-      cudaStream_t s2 = c->aux[k % kmb_context::kAux];
-      KMB_CUDA(cudaStreamWaitEvent(s2, c->ev0, 0));
+    if (!c->cin) {
+      KMB_CUDA(cudaStreamCreateWithFlags(&c->cin, cudaStreamNonBlocking));
+      for (int k = 0; k < kmb_context::kMaxChunks; ++k)
+        KMB_CUDA(cudaEventCreateWithFlags(&c->in_ev[k], cudaEventDisableTiming));
+    }
+    // copies in order on one stream; chunk k's solve and result copies on an
+    // auxiliary stream once its copy has landed (solves of successive chunks
+    // may overlap each other; the D2H engine runs beside the H2D one)
+    KMB_CUDA(cudaStreamWaitEvent(c->cin, c->ev0, 0));
+    for (size_t k = 0; k < sched.size(); ++k) {
+      const int lo = sched[k].first, cnt = sched[k].second;
       const size_t off = static_cast<size_t>(lo) * n * n;
       KMB_CUDA(cudaMemcpyAsync(c->bcost.as<int32_t>() + off, costs + off,
-                               static_cast<size_t>(cnt) * n * n * 4, cudaMemcpyHostToDevice, s2));
+                               static_cast<size_t>(cnt) * n * n * 4, cudaMemcpyHostToDevice, c->cin));
+      KMB_CUDA(cudaEventRecord(c->in_ev[k], c->cin));
+    }
+    for (size_t k = 0; k < sched.size(); ++k) {
+      const int lo = sched[k].first, cnt = sched[k].second;
+      cudaStream_t s2 = c->aux[k % kmb_context::kAux];
+      KMB_CUDA(cudaStreamWaitEvent(s2, c->in_ev[k], 0));
       const int eng = auto_engine ? pick(cnt) : engine;  // chunks are small: CTA engine
       if (k == 0) used = eng;
       KMB_CUDA(launch(lo, cnt, eng, s2));
       KMB_CUDA(results_out(lo, cnt, s2));
-      KMB_CUDA(cudaEventRecord(c->aux_ev[k % kmb_context::kAux], s2));
-      KMB_CUDA(cudaStreamWaitEvent(st, c->aux_ev[k % kmb_context::kAux], 0));
+    }
+    for (int k = 0; k < kmb_context::kAux; ++k) {
+      KMB_CUDA(cudaEventRecord(c->aux_ev[k], c->aux[k]));
+      KMB_CUDA(cudaStreamWaitEvent(st, c->aux_ev[k], 0));
     }
     KMB_CUDA(cudaEventRecord(c->ev1, st));  // includes the transfers
   }

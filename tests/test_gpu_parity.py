@@ -465,3 +465,33 @@ def test_batch_mid_size_instances(solver):
             np.testing.assert_array_equal(r.u[t], ref.u)
             np.testing.assert_array_equal(r.v[t], ref.v)
             assert int(r.total_cost[t]) == ref.total_cost
+
+
+@pytest.mark.parametrize("pipe", [1, 3, 7, 64, -2, -5])
+def test_host_pipeline_schedules(solver, pipe):
+    """Host-buffer batches are copied in chunks (KMB_OPT_PIPELINE): every chunk
+    schedule, ragged ones included, returns the same results as the auto one."""
+    from paper_2005_01182_b200.api import OPT_PIPELINE
+    c = W.CONFIGS["c3"].make(batch=700)
+    base = solver.solve_batch(c, KMB_SEED_BATCHED)
+    solver.set_option(OPT_PIPELINE, pipe)
+    try:
+        r = solver.solve_batch(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_PIPELINE, 0)
+    np.testing.assert_array_equal(r.total_cost, base.total_cost)
+    np.testing.assert_array_equal(r.u, base.u)
+    np.testing.assert_array_equal(r.v, base.v)
+    np.testing.assert_array_equal(r.row_to_col, base.row_to_col)
+    for t in (0, 349, 699):
+        ref = O.ref_solve_batched_km(c[t])
+        assert r.total_cost[t] == ref.total_cost
+        np.testing.assert_array_equal(r.u[t], ref.u)
+
+
+def test_pipeline_option_range(solver):
+    from paper_2005_01182_b200.api import OPT_PIPELINE
+    with pytest.raises(KmbError):
+        solver.set_option(OPT_PIPELINE, 65)
+    with pytest.raises(KmbError):
+        solver.set_option(OPT_PIPELINE, -33)
