@@ -129,6 +129,17 @@ int kmb_solve_batch_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, i
                         int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
                         int64_t* total_cost, kmb_stats* stats);
 
+/* One process, several GPUs (BASELINE config 3 "instances sharded across
+ * GPUs" without one process per GPU): the batch is split into nctx contiguous
+ * slices of equal size (+-1) and slice k is solved by kmb_solve_batch_i32 on
+ * ctxs[k] (normally one context per device), all slices concurrently, one host
+ * thread per extra context.  When the contexts span several devices the five
+ * buffers must be host memory (pinned for copy/solve overlap).  stats: sums
+ * over the slices, seconds = the slowest slice.  Errors name the slice. */
+int kmb_solve_batch_multi_i32(kmb_context* const* ctxs, int32_t nctx, const int32_t* costs,
+                              int32_t batch, int32_t n, int32_t seed, int32_t* row_to_col,
+                              int64_t* u, int64_t* v, int64_t* total_cost, kmb_stats* stats);
+
 /* ---- column-sharded single instance across ranks/GPUs (config 5) ----------
  * Rank r owns columns [col_begin, col_begin + ncols) of the n x n matrix
  * (`slab`: n rows x ncols, leading dimension ld).  Every rank calls

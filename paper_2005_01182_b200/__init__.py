@@ -16,9 +16,11 @@ Layers:
 """
 from .api import (KMB_SEED_BATCHED, KMB_SEED_KM, KmbError, KmbUnavailable, Result, Solver,
                   calibrate_auction_eps, calibrate_batch_level, default_solver, load_library,
-                  quantize_costs, solve_auction, solve_auction_scaled, solve_batched_km, solve_km)
+                  quantize_costs, solve_auction, solve_auction_scaled, solve_batch_multi,
+                  solve_batched_km, solve_km)
 
 __all__ = ["KMB_SEED_BATCHED", "KMB_SEED_KM", "KmbError", "KmbUnavailable", "Result", "Solver",
            "calibrate_auction_eps", "calibrate_batch_level", "default_solver", "load_library",
-           "quantize_costs", "solve_auction", "solve_auction_scaled", "solve_batched_km",
+           "quantize_costs", "solve_auction", "solve_auction_scaled", "solve_batch_multi",
+           "solve_batched_km",
            "solve_km"]

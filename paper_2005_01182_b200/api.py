@@ -27,7 +27,8 @@ OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_U16, OPT_PIPEL
 
 # every symbol include/kmb.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
-               "kmb_solve_batch_i32", "kmb_nccl_unique_id", "kmb_shard_init_nccl",
+               "kmb_solve_batch_i32", "kmb_solve_batch_multi_i32", "kmb_nccl_unique_id",
+               "kmb_shard_init_nccl",
                "kmb_shard_init_callbacks", "kmb_solve_sharded_i32", "kmb_bench_scan",
                "kmb_last_instance_stats", "kmb_costs_from_points", "kmb_auction_i32",
                "kmb_last_error", "kmb_abi_version")
@@ -79,6 +80,8 @@ def load_library(path: str | None = None):
                                       vp, vp, vp, vp, C.POINTER(Stats)]
         lib.kmb_solve_batch_i32.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32,
                                             vp, vp, vp, vp, C.POINTER(Stats)]
+        lib.kmb_solve_batch_multi_i32.argtypes = [C.POINTER(vp), C.c_int32, vp, C.c_int32, C.c_int32,
+                                                  C.c_int32, vp, vp, vp, vp, C.POINTER(Stats)]
         lib.kmb_bench_scan.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
         lib.kmb_costs_from_points.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32,
@@ -297,6 +300,35 @@ class Solver:
         wall = time.perf_counter() - t0
         return Result(r2c, u, v, tot, iterations=int(st.phases + st.dual_steps),
                       wall_seconds=wall, stats=_stats_dict(st))
+
+
+def solve_batch_multi(solvers, costs, seed: int = KMB_SEED_BATCHED) -> Result:
+    """A batch split over several contexts (normally one ``Solver`` per GPU)
+    through ``kmb_solve_batch_multi_i32``: contiguous equal slices, solved
+    concurrently, results in batch order.  Host (numpy) buffers."""
+    solvers = list(solvers)
+    if not solvers:
+        raise ValueError("solve_batch_multi: no solvers")
+    lib = solvers[0]._lib
+    c = np.ascontiguousarray(costs, dtype=np.int32)
+    b, n, n2 = c.shape
+    if n != n2:
+        raise ValueError("square cost matrices required")
+    r2c = np.full((b, n), -1, np.int32)
+    u = np.zeros((b, n), np.int64)
+    v = np.zeros((b, n), np.int64)
+    tot = np.zeros(b, np.int64)
+    hs = (C.c_void_p * len(solvers))(*[s._h for s in solvers])
+    st = Stats()
+    t0 = time.perf_counter()
+    rc = lib.kmb_solve_batch_multi_i32(hs, len(solvers), C.c_void_p(c.ctypes.data), b, n, seed,
+                                       C.c_void_p(r2c.ctypes.data), C.c_void_p(u.ctypes.data),
+                                       C.c_void_p(v.ctypes.data), C.c_void_p(tot.ctypes.data),
+                                       C.byref(st))
+    wall = time.perf_counter() - t0
+    solvers[0]._check(rc)
+    return Result(r2c, u, v, tot, iterations=int(st.phases + st.dual_steps),
+                  wall_seconds=wall, stats=_stats_dict(st))
 
 
 def _stats_dict(st: Stats) -> dict:

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kmb.h"
@@ -446,6 +447,67 @@ int kmb_solve_batch_i32(kmb_context* c, const int32_t* costs, int32_t batch, int
   KMB_CUDA(cudaSetDevice(c->device));
   return solve_batch_impl(c, costs, batch, n, seed, row_to_col, u, v, total_cost, stats, who,
                           c->engine);
+}
+
+// Several contexts (normally one per GPU): contiguous slices of the batch, each
+// solved by kmb_solve_batch_i32 on its own context, concurrently (one host
+// thread per extra context).  Across devices the buffers must be host memory.
+int kmb_solve_batch_multi_i32(kmb_context* const* ctxs, int32_t nctx, const int32_t* costs,
+                              int32_t batch, int32_t n, int32_t seed, int32_t* row_to_col,
+                              int64_t* u, int64_t* v, int64_t* total_cost, kmb_stats* stats) {
+  const char* who = "kmb_solve_batch_multi_i32";
+  if (!ctxs || nctx <= 0) return fail(KMB_EINVAL, std::string(who) + ": no contexts");
+  for (int k = 0; k < nctx; ++k)
+    if (!ctxs[k]) return fail(KMB_EINVAL, std::string(who) + ": NULL context");
+  if (batch <= 0 || n <= 0) return fail(KMB_EINVAL, std::string(who) + ": dimensions must be positive");
+  if (!costs) return fail(KMB_EINVAL, std::string(who) + ": costs is NULL");
+  bool one_device = true;
+  for (int k = 1; k < nctx; ++k) one_device &= ctxs[k]->device == ctxs[0]->device;
+  if (!one_device) {
+    cudaSetDevice(ctxs[0]->device);
+    for (const void* p : {static_cast<const void*>(costs), static_cast<const void*>(row_to_col),
+                          static_cast<const void*>(u), static_cast<const void*>(v),
+                          static_cast<const void*>(total_cost)})
+      if (p && is_device_ptr(p))
+        return fail(KMB_EINVAL, std::string(who) + ": contexts on several devices need host buffers");
+  }
+  const int parts = std::min<int>(nctx, batch);
+  std::vector<int> lo(parts + 1);
+  for (int k = 0; k <= parts; ++k) lo[k] = static_cast<int>(static_cast<int64_t>(batch) * k / parts);
+  std::vector<int> rc(parts, KMB_OK);
+  std::vector<std::string> msg(parts);
+  std::vector<kmb_stats> st(parts);
+  auto run = [&](int k) {
+    const size_t o = static_cast<size_t>(lo[k]) * n;
+    rc[k] = kmb_solve_batch_i32(ctxs[k], costs + o * n, lo[k + 1] - lo[k], n, seed,
+                                row_to_col ? row_to_col + o : nullptr, u ? u + o : nullptr,
+                                v ? v + o : nullptr, total_cost ? total_cost + lo[k] : nullptr,
+                                &st[k]);
+    if (rc[k] != KMB_OK) msg[k] = g_err;
+  };
+  std::vector<std::thread> th;
+  th.reserve(parts - 1);
+  for (int k = 1; k < parts; ++k) th.emplace_back(run, k);
+  run(0);
+  for (auto& t : th) t.join();
+  for (int k = 0; k < parts; ++k)
+    if (rc[k] != KMB_OK) return fail(rc[k], msg[k] + " (slice " + std::to_string(k) + ")");
+  if (stats) {
+    *stats = st[0];
+    for (int k = 1; k < parts; ++k) {
+      stats->phases += st[k].phases;
+      stats->dual_steps += st[k].dual_steps;
+      stats->rows_scanned += st[k].rows_scanned;
+      stats->cost_bytes_read += st[k].cost_bytes_read;
+      stats->rounds += st[k].rounds;
+      stats->seconds = std::max(stats->seconds, st[k].seconds);
+      stats->converged = stats->converged && st[k].converged;
+      for (int q = 0; q < 6; ++q) stats->stage_ns[q] += st[k].stage_ns[q];
+      stats->max_instance_cycles = std::max(stats->max_instance_cycles, st[k].max_instance_cycles);
+      stats->sum_instance_cycles += st[k].sum_instance_cycles;
+    }
+  }
+  return KMB_OK;
 }
 
 // Grid engine staging: slab width W (power of two) and CTA count G, pitched

@@ -88,3 +88,12 @@ def test_bench_sharding_covers_batch():
         assert sum(c for _, c in spans) == bench.BATCH
         for (f0, c0), (f1, _) in zip(spans, spans[1:]):
             assert f0 + c0 == f1
+
+
+def test_multi_null_contexts_error():
+    lib = api.load_library()
+    assert lib.kmb_solve_batch_multi_i32(None, 0, None, 1, 4, 1, None, None, None, None, None) == 1
+    assert b"no contexts" in lib.kmb_last_error()
+    hs = (C.c_void_p * 2)(None, None)
+    assert lib.kmb_solve_batch_multi_i32(hs, 2, None, 1, 4, 1, None, None, None, None, None) == 1
+    assert b"NULL context" in lib.kmb_last_error()

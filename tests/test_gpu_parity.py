@@ -495,3 +495,40 @@ def test_pipeline_option_range(solver):
         solver.set_option(OPT_PIPELINE, 65)
     with pytest.raises(KmbError):
         solver.set_option(OPT_PIPELINE, -33)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3])
+def test_batch_multi_context_split(parts):
+    """kmb_solve_batch_multi_i32: the batch in contiguous slices over several
+    contexts (one per GPU in production; here several on cuda:0) gives the
+    single-context results, in batch order."""
+    from paper_2005_01182_b200 import Solver, solve_batch_multi
+    c = W.CONFIGS["c3"].make(batch=301)
+    solvers = [Solver(0) for _ in range(parts)]
+    try:
+        r = solve_batch_multi(solvers, c)
+        base = solvers[0].solve_batch(c, KMB_SEED_BATCHED)
+    finally:
+        for s in solvers:
+            s.close()
+    np.testing.assert_array_equal(r.total_cost, base.total_cost)
+    np.testing.assert_array_equal(r.u, base.u)
+    np.testing.assert_array_equal(r.v, base.v)
+    np.testing.assert_array_equal(r.row_to_col, base.row_to_col)
+    assert r.stats["dual_steps"] == base.stats["dual_steps"]
+    for t in (0, 150, 300):
+        ref = O.ref_solve_batched_km(c[t])
+        assert r.total_cost[t] == ref.total_cost
+
+
+def test_batch_multi_error_names_slice():
+    from paper_2005_01182_b200 import Solver, solve_batch_multi
+    c = W.CONFIGS["c3"].make(batch=8)
+    c[6, 1, 2] = -1  # invalid cost in the second slice
+    solvers = [Solver(0), Solver(0)]
+    try:
+        with pytest.raises(KmbError, match="slice 1"):
+            solve_batch_multi(solvers, c)
+    finally:
+        for s in solvers:
+            s.close()
