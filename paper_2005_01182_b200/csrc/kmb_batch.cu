@@ -27,6 +27,18 @@
 #ifndef KMB_CTA_RB  // rows per relax batch
 #define KMB_CTA_RB 4  // A/B (tools/ab_cta.py, 512-shard): 2: .449, 3: .399, 4: .386, 5: .415, 8: .399, 16: .473 ms
 #endif
+// epoch start: recompute only the reset ("dirty") columns, threads split over
+// (dirty column, survivor-row group) pairs, instead of re-relaxing every
+// survivor row over all columns (~80% of the rows relaxed on config 3)
+#ifndef KMB_CTA_DIRTY
+#define KMB_CTA_DIRTY 1
+#endif
+// (A/B, tools/ab_cta.py, 512-shard / 1024-shard / c1 ms: full re-relax .433 /
+// .581 / .231; dirty GB=1 .403 / .511 / .217, GB=2 .389 / .481 / .203, GB=3
+// .389 / .485 / .204, GB=4 .400 / .511 / .212, GB=8 .403 / .496 / .208)
+#ifndef KMB_CTA_GB  // survivor rows in flight per thread in the dirty recompute
+#define KMB_CTA_GB 2
+#endif
 #ifndef KMB_CTA_STAGE_CLOCKS
 #define KMB_CTA_STAGE_CLOCKS 0
 #endif
@@ -78,10 +90,15 @@ __device__ __forceinline__ bool cclaimed(uint32_t c, int epoch) {
 
 struct CtaShared {
   uint64_t bar;  // mbarrier of the TMA bulk copy
-  int32_t nrows, nfound, ns, won;
+  int32_t nrows, nfound, ns, won, nd;
   int32_t lo_all, hi_all;
   int32_t red[8];  // per-warp min slack' / partial sums
 };
+
+__device__ __forceinline__ void shared_min(uint32_t* p, uint32_t x) { atomicMin(p, x); }
+__device__ __forceinline__ void shared_min(uint64_t* p, uint64_t x) {
+  atomicMin(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(x));
+}
 
 template <bool SMEM_C>
 __device__ __forceinline__ int32_t ldc(const int32_t* p) {
@@ -92,10 +109,10 @@ __device__ __forceinline__ int32_t ldc(const int32_t* p) {
 }  // namespace
 
 // dynamic smem: [Cs n*n (SMEM_C)] | rows[2][n] (int2) | u w root_row match_row
-// match_col tree_par found (int32 x n) | claim (u32 x n)
+// match_col tree_par found (int32 x n) | claim (u32 x n) | dlist (int32 x n)
 __host__ __device__ inline size_t cta_smem_bytes(int n, bool smem_c) {
   const size_t cs = smem_c ? ((static_cast<size_t>(n) * n * 4 + 15) & ~static_cast<size_t>(15)) : 0;
-  return cs + static_cast<size_t>(n) * (2 * 8 + 8 * 4);
+  return cs + static_cast<size_t>(n) * (2 * 8 + 9 * 4);
 }
 
 template <bool SMEM_C, bool NARROW>
@@ -103,7 +120,7 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
                                          CtaShared& sm, int2* rows, int2* spare, int32_t* u,
                                          int32_t* w, int32_t* root_row, int32_t* match_row,
                                          int32_t* match_col, int32_t* tree_par, int32_t* found,
-                                         uint32_t* claim) {
+                                         uint32_t* claim, int32_t* dlist) {
   using KO = CKeys<NARROW>;
   using K = typename KO::K;
   constexpr uint32_t FULL = 0xffffffffu;
@@ -120,6 +137,35 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
   K key = KO::INF;
   int32_t v = 0, dc = 0;
   bool rch = !own;
+  bool dirty_round = false;
+  int dirty_k = -1;  // this column's slot in dlist while it is dirty
+  auto relax = [&](int r, int end) {
+    for (; r + KMB_CTA_RB - 1 < end; r += KMB_CTA_RB) {
+      int2 e[KMB_CTA_RB];
+      int32_t c[KMB_CTA_RB];
+#pragma unroll
+      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[r + k];
+#pragma unroll
+      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+#pragma unroll
+      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
+    }
+    if (end - r == 1) {
+      const int2 e = rows[r];
+      key = KO::kmin(key, KO::make(ldc<SMEM_C>(colp + e.x * n), static_cast<uint32_t>(e.y), e.x));
+    } else if (r < end) {
+      // 2..KMB_CTA_RB-1 rows: one batch with the last row repeated (the fold is
+      // idempotent), so every load is in flight at once
+      int2 e[KMB_CTA_RB];
+      int32_t c[KMB_CTA_RB];
+#pragma unroll
+      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[min(r + k, end - 1)];
+#pragma unroll
+      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+#pragma unroll
+      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
+    }
+  };
   int nrows = n, head = 0, nfree = n;
   int32_t D = 0;
   int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
@@ -142,35 +188,46 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
   while (nfree > 0) {
     ++rounds;
     // ---- relax rows[head, nrows) for column j (hungarian.cpp:164-172) ----
-    int r = head;
-    for (; r + KMB_CTA_RB - 1 < nrows; r += KMB_CTA_RB) {
-      int2 e[KMB_CTA_RB];
-      int32_t c[KMB_CTA_RB];
+    if (!dirty_round) {
+      relax(head, nrows);
+      rows_scanned += nrows - head;
+    } else {
+      // epoch start: only the dirty columns' keys change (every other unreached
+      // key's argmin row survived, and every survivor is already folded in).
+      // Threads split (dirty column, survivor-row group) pairs; the old row
+      // list (spare after the swap) is dead and holds the partial minima.
+      dirty_round = false;
+      const int nd = sm.nd;
+      K* dkey = reinterpret_cast<K*>(spare);
+      for (int k = j; k < nd; k += T) dkey[k] = KO::INF;
+      __syncthreads();
+      const int groups = nd > 0 ? max(1, T / nd) : 1;
+      for (int item = j; nrows > 0 && item < nd * groups; item += T) {
+        const int k = item % nd, g = item / nd;
+        const int col = dlist[k];
+        K best = KO::INF;
+        constexpr int GB = KMB_CTA_GB;
+        for (int r = g; r < nrows; r += groups * GB) {
+          int2 e[GB];
+          int32_t c[GB];
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[r + k];
+          for (int b = 0; b < GB; ++b) {
+            const int rr = r + b * groups;
+            e[b] = rows[rr < nrows ? rr : nrows - 1];  // repeat: the fold is idempotent
+          }
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+          for (int b = 0; b < GB; ++b) c[b] = ldc<SMEM_C>(Cm + e[b].x * n + col);
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
+          for (int b = 0; b < GB; ++b) best = KO::kmin(best, KO::make(c[b], static_cast<uint32_t>(e[b].y), e[b].x));
+        }
+        shared_min(dkey + k, best);
+      }
+      __syncthreads();
+      if (dirty_k >= 0) key = dkey[dirty_k];
+      dirty_k = -1;
     }
-    if (nrows - r == 1) {
-      const int2 e = rows[r];
-      key = KO::kmin(key, KO::make(ldc<SMEM_C>(colp + e.x * n), static_cast<uint32_t>(e.y), e.x));
-    } else if (r < nrows) {
-      // 2..KMB_CTA_RB-1 rows: one batch with the last row repeated (the fold is
-      // idempotent), so every load is in flight at once
-      int2 e[KMB_CTA_RB];
-      int32_t c[KMB_CTA_RB];
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[min(r + k, nrows - 1)];
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
-    }
-    if (rounds == 1 && a.seed == 1 && own) v = KO::val(key);  // column reduction, :328-333
-    rows_scanned += nrows - head;
     head = nrows;
+    if (rounds == 1 && a.seed == 1 && own) v = KO::val(key);  // column reduction, :328-333
     KMB_CSTAGE(0);
     // ---- min unreached slack' (hungarian.cpp:203-206): REDUX + one exchange ----
     const int32_t s = rch ? 0x7fffffff : KO::val(key) - v;
@@ -212,7 +269,20 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
     KMB_CSTAGE(2);
     if (nfound == 0) continue;
 
-    // ---- epoch end: augment and dissolve the trees that reached a free column
+    // ---- epoch end: augment and dissolve the trees that reached a free column.
+    // Dirty-column mode: the rows appended this round are relaxed over all
+    // columns first, so every survivor is folded into the surviving keys.
+    if (KMB_CTA_DIRTY) {
+      relax(head, nrows);
+      rows_scanned += nrows - head;
+      head = nrows;
+    }
+    if (j == 0) {
+      sm.ns = 0;
+      sm.won = 0;
+      sm.nd = 0;
+    }
+    __syncthreads();
     if (own) {
       if (rch) {
         if (cclaimed(claim[root_row[tree_par[j]]], epochs)) {
@@ -223,12 +293,11 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
       } else if (key != KO::INF && cclaimed(claim[root_row[KO::row(key)]], epochs)) {
         key = KO::INF;
       }
+      if (KMB_CTA_DIRTY && !rch && key == KO::INF) {  // dirty: recomputed next round
+        dirty_k = atomicAdd(&sm.nd, 1);
+        dlist[dirty_k] = j;
+      }
     }
-    if (j == 0) {
-      sm.ns = 0;
-      sm.won = 0;
-    }
-    __syncthreads();
     for (int q = j; q < nrows; q += T) {
       const int2 e = rows[q];
       if (cclaimed(claim[root_row[e.x]], epochs)) u[e.x] = w[e.x] + D;
@@ -253,7 +322,8 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
     int2* t = rows;
     rows = spare;
     spare = t;
-    head = 0;  // survivors relax once more for the reset columns
+    head = KMB_CTA_DIRTY ? nrows : 0;  // else survivors relax once more over all columns
+    dirty_round = KMB_CTA_DIRTY;
     ++epochs;
     __syncthreads();
     if (j == 0) {
@@ -315,6 +385,7 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
   int32_t* tree_par = match_col + n;
   int32_t* found = tree_par + n;
   uint32_t* claim = reinterpret_cast<uint32_t*>(found + n);
+  int32_t* dlist = reinterpret_cast<int32_t*>(claim + n);
   const bool bulk = SMEM_C && ((static_cast<int64_t>(n) * n) & 3) == 0;
   if (bulk && j == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&sm.bar)));
@@ -402,10 +473,10 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
       if (j == 0) a.total_cost[inst] = 0;
     } else if (hi_all < (1 << 21)) {
       status = cta_solve<SMEM_C, true>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
-                                       match_col, tree_par, found, claim);
+                                       match_col, tree_par, found, claim, dlist);
     } else {
       status = cta_solve<SMEM_C, false>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
-                                        match_col, tree_par, found, claim);
+                                        match_col, tree_par, found, claim, dlist);
     }
     if (j == 0) a.status[inst] = status;
     __syncthreads();
