@@ -12,6 +12,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     if eng: s.set_option(OPT_ENGINE, eng)
     c = W.CONFIGS[key].make()
     if c.ndim == 2: c = c[None]
+    if os.environ.get("BATCH"): c = np.ascontiguousarray(c[:int(os.environ["BATCH"])])
     b, n, _ = c.shape
     dc = torch.from_numpy(c).cuda()
     r2c = torch.empty((b, n), dtype=torch.int32, device="cuda"); u = torch.empty((b, n), dtype=torch.int64, device="cuda")
@@ -21,7 +22,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
         st = (s.solve_batch_into(dc, b, n, 1, r2c, u, v, tot) if b > 1 else s.solve_into(dc, n, n, 1, r2c, u, v, tot))
         ts.append(st.seconds)
     ts = sorted(ts[2:])
-    print(json.dumps({"lib": os.environ.get("KMB_LIB", "default"), "cfg": key, "median_ms": ts[len(ts) // 2] * 1e3, "min_ms": ts[0] * 1e3, "tot0": int(tot[0])}))
+    print(json.dumps({"lib": os.environ.get("KMB_LIB", "default"), "cfg": key, "median_ms": ts[len(ts) // 2] * 1e3, "min_ms": ts[0] * 1e3, "tot0": int(tot[0]),
+                      "hash": W.fnv1a64(np.concatenate([tot.cpu().numpy(), u.cpu().numpy().ravel(), r2c.cpu().numpy().ravel().astype(np.int64)]))}))
 else:
     for lib in sys.argv[1:]:
         env = dict(os.environ, KMB_LIB=os.path.abspath(lib))
