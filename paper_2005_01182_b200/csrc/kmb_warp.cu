@@ -129,10 +129,12 @@ __device__ __forceinline__ RowVec<CPL> load_row(const int32_t* p) {
 
 }  // namespace
 
-// Per-warp shared state (n <= 256), in 32-bit words: u, w, root_row,
-// match_row, match_col, tree_par, claim, found (8n) + two row lists of
-// (row, tag) pairs (4n).
-__host__ __device__ constexpr int warp_state_words(int n) { return 13 * n; }
+// Per-warp shared state (n <= 256), in 32-bit words: two row lists of (row,
+// tag) pairs (4n; the free columns found in an epoch live in the idle list) +
+// u, w, root_row, match_row, match_col, tree_par, claim (7n) + the U16 row
+// minima (n, U16 mode only).  Kept small: what the CTAs per SM do not take of
+// the unified cache is L1 for the streamed matrices.
+__host__ __device__ constexpr int warp_state_words(int n, bool u16) { return (u16 ? 12 : 11) * n; }
 
 // Column keys.  Wide: ((c - w + 2^30) << 32) | row (any n, costs < 2^29).
 // Narrow (n <= 256, costs < 2^21): ((c - w + 2^22) << 8) | row in 32 bits, so a
@@ -173,7 +175,7 @@ struct Keys<true> {
 };
 
 struct WarpSmem {
-  int32_t *u, *w, *root_row, *match_row, *match_col, *tree_par, *found;
+  int32_t *u, *w, *root_row, *match_row, *match_col, *tree_par;
   int32_t* rmin;  // U16 mode: row minimum | (wide row << 31)
   int32_t* ctr;  // [0] rows tail, [1] free columns found this epoch
   uint32_t* claim;
@@ -236,9 +238,9 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   int32_t* const match_col = S.match_col;
   int32_t* const tree_par = S.tree_par;
   uint32_t* const claim = S.claim;
-  int32_t* const found = S.found;
   int2* rows = S.rows;
   int2* spare = S.spare;
+  int32_t* found = reinterpret_cast<int32_t*>(spare);  // idle row list during an epoch
 
   const uint16_t* const lb16 = U16 ? a.C16 + static_cast<int64_t>(inst) * n * np + c0 : nullptr;
   for (int k = lane; k < n; k += 32)
@@ -471,22 +473,6 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
         key[q] = KO::INF;
       }
     }
-    // rows: finalise dissolved ones (u = w + D), compact the survivors
-    int ns = 0;
-    for (int rb = 0; rb < nrows; rb += 32) {
-      const int rr = rb + lane;
-      bool keep = false;
-      int2 e = make_int2(0, 0);
-      if (rr < nrows) {
-        e = rows[rr];
-        if (wclaimed_in(claim[root_row[e.x]], epochs)) u[e.x] = w[e.x] + D;
-        else keep = true;
-      }
-      const uint32_t km = __ballot_sync(FULL, keep);
-      if (keep) spare[ns + __popc(km & ((1u << lane) - 1))] = e;
-      ns += __popc(km);
-    }
-    __syncwarp();
     // flip one parent-pointer path per claimed tree (its smallest free column)
     int won = 0;
     for (int fb = 0; fb < nfound; fb += 32) {
@@ -508,6 +494,22 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       }
       won += __popc(__ballot_sync(FULL, winner));
     }
+    __syncwarp();  // found[] (the idle list) is read; the compaction overwrites it
+    // rows: finalise dissolved ones (u = w + D), compact the survivors
+    int ns = 0;
+    for (int rb = 0; rb < nrows; rb += 32) {
+      const int rr = rb + lane;
+      bool keep = false;
+      int2 e = make_int2(0, 0);
+      if (rr < nrows) {
+        e = rows[rr];
+        if (wclaimed_in(claim[root_row[e.x]], epochs)) u[e.x] = w[e.x] + D;
+        else keep = true;
+      }
+      const uint32_t km = __ballot_sync(FULL, keep);
+      if (keep) spare[ns + __popc(km & ((1u << lane) - 1))] = e;
+      ns += __popc(km);
+    }
     if (lane == 0) {
       S.ctr[0] = ns;
       S.ctr[1] = 0;
@@ -517,6 +519,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     int2* t = rows;
     rows = spare;
     spare = t;
+    found = reinterpret_cast<int32_t*>(spare);
     nrows = ns;
     head = 0;  // survivors relax once more for the reset columns
     ++epochs;
@@ -563,7 +566,9 @@ __global__ void __launch_bounds__(128, 7) k_warp_batch(WarpArgs a) {
 
   // carve this warp's slice: [mbarrier | C (SMEM_C) | state]
   const size_t cbytes = SMEM_C ? static_cast<size_t>(n) * np * 4 : 0;
-  const size_t wbytes = cbytes + static_cast<size_t>(warp_state_words(n)) * 4 + 16;
+  constexpr bool kU16able = !SMEM_C && (CPL == 4 || CPL == 8);
+  const bool use16 = kU16able && a.C16 != nullptr;
+  const size_t wbytes = cbytes + static_cast<size_t>(warp_state_words(n, use16)) * 4 + 16;
   unsigned char* base = dyn + wib * ((wbytes + 15) & ~static_cast<size_t>(15));
   uint64_t* bar = reinterpret_cast<uint64_t*>(base);
   int32_t* ctr = reinterpret_cast<int32_t*>(base + 8);  // 2 counters after the mbarrier
@@ -579,11 +584,8 @@ __global__ void __launch_bounds__(128, 7) k_warp_batch(WarpArgs a) {
   S.match_col = S.match_row + n;
   S.tree_par = S.match_col + n;
   S.claim = reinterpret_cast<uint32_t*>(S.tree_par + n);
-  S.found = reinterpret_cast<int32_t*>(S.claim + n);
-  S.rmin = S.found + n;
+  S.rmin = use16 ? reinterpret_cast<int32_t*>(S.claim + n) : nullptr;
   S.ctr = ctr;
-  constexpr bool kU16able = !SMEM_C && (CPL == 4 || CPL == 8);
-  const bool use16 = kU16able && a.C16 != nullptr;
 
   if (SMEM_C && lane == 0) mbar_init1(bar);
   __syncwarp();
@@ -753,16 +755,16 @@ cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_
 
 int warp_max_n() { return 256; }
 
-size_t warp_smem_per_warp(int n, int pitch, bool smem_c) {
+size_t warp_smem_per_warp(int n, int pitch, bool smem_c, bool u16) {
   const size_t c = smem_c ? static_cast<size_t>(n) * pitch * 4 : 0;
-  return (c + static_cast<size_t>(warp_state_words(n)) * 4 + 16 + 15) & ~static_cast<size_t>(15);
+  return (c + static_cast<size_t>(warp_state_words(n, u16)) * 4 + 16 + 15) & ~static_cast<size_t>(15);
 }
 
 template <int CPL, bool SMEM_C>
 static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, int warps_per_sm,
                             cudaStream_t st, int* grid_out) {
   auto kern = k_warp_batch<CPL, SMEM_C>;
-  const size_t smem = warp_smem_per_warp(a.n, a.pitch, SMEM_C) * wpb;
+  const size_t smem = warp_smem_per_warp(a.n, a.pitch, SMEM_C, a.C16 != nullptr) * wpb;
   // Shared-memory carveout: just the state of the CTAs per SM this launch
   // needs (all instances resident in one wave, at most the register limit),
   // +1 KiB reserved per CTA; the rest of the unified cache is L1, which keeps
@@ -816,7 +818,7 @@ cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int 
                               cudaStream_t st, int* grid_out) {
   if (a.n < 1 || a.n > 256 || a.pitch != warp_pitch(a.n)) return cudaErrorInvalidValue;
   const int cpl = a.pitch / 32;
-  if (smem_c && warp_smem_per_warp(a.n, a.pitch, true) > 227 * 1024) smem_c = false;
+  if (smem_c && warp_smem_per_warp(a.n, a.pitch, true, false) > 227 * 1024) smem_c = false;
   const int wpb = smem_c ? 1 : 4;
 #define KMB_L(C)                                                                          \
   return smem_c ? launch_t<C, true>(a, sm_count, wpb, warps_per_sm, st, grid_out)         \
