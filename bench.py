@@ -440,6 +440,10 @@ def main():
                     extras[key] = fn()
                 except Exception as e:  # reported, never silently dropped
                     extras[key] = {"error": repr(e)}
+                # hand the freed 1 GiB c5 segment back: a later matrix carved out
+                # of torch's cached segment solved ~10% slower (c4: 129 vs 142 ms,
+                # tools/ex_probe.py), an address-placement effect of the harness
+                torch.cuda.empty_cache()
         threads = os.cpu_count() or 1
         try:
             rate, done, wall = cpu_reference_rate(host, args.cpu_seconds, threads)
