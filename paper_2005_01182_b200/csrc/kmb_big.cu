@@ -456,11 +456,22 @@ size_t big_smem_bytes(int n) { return static_cast<size_t>(n) * (8 + 8 + 4 * 10);
 
 int big_max_n() { return 4096; }
 
+#ifndef KMB_BIG_CARVE
+#define KMB_BIG_CARVE 1
+#endif
+
 template <int CPT, int NT>
 static cudaError_t launch_nt(const BigArgs& a, int sm_count, size_t smem, cudaStream_t st) {
   const void* k = reinterpret_cast<const void*>(k_big<CPT, NT>);
+  // carveout: the shared memory of the CTAs per SM this batch needs (+1 KiB
+  // each, one CTA per SM for a single instance); the rest of the unified cache
+  // is L1 for the cost rows
+  const int64_t want = std::max<int64_t>(1, std::min<int64_t>(227 * 1024 / (smem + 1024),
+                                                              (a.batch + sm_count - 1) / sm_count));
+  const int carve = static_cast<int>(std::min<int64_t>(
+      100, (want * static_cast<int64_t>(smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
   int occ = 0;
-  cudaError_t e = prepare_launch(k, NT, smem, 100, &occ);
+  cudaError_t e = prepare_launch(k, NT, smem, KMB_BIG_CARVE ? carve : 100, &occ);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int grid = static_cast<int>(std::min<int64_t>(a.batch, static_cast<int64_t>(occ) * sm_count));
