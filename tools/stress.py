@@ -1,6 +1,7 @@
 """Randomised stress: engines x sizes x value ranges x seeds against the
 reference (duals, total cost) and against themselves (determinism: the same
-matching and round count twice).  Usage: python tools/stress.py [seconds]"""
+matching and round count twice).  Usage: python tools/stress.py [seconds]
+(BATCH=1: random batches through every batch engine instead)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -12,8 +13,23 @@ s = Solver(0)
 rng = np.random.default_rng(int(os.environ.get("SEED", "12345")))
 t0 = time.time(); cases = 0; bad = 0
 while time.time() - t0 < budget:
-    n = int(rng.choice([rng.integers(1, 64), rng.integers(64, 300), rng.integers(300, 1500), rng.integers(1500, 3000)]))
     hi = int(rng.choice([2, 10, 1000, 10**6, 2**29 - 1]))
+    if os.environ.get("BATCH"):  # batch engines: warp (SMEM / L2), CTA (SMEM / L2), single-CTA
+        n = int(rng.integers(1, 300)); b = int(rng.integers(1, 40))
+        cb = rng.integers(0, hi, size=(b, n, n)).astype(np.int32)
+        seed = int(rng.choice([KMB_SEED_BATCHED, KMB_SEED_KM]))
+        refs = [O.ref_solve_batched_km(x) if seed == KMB_SEED_BATCHED else O.ref_solve_km(x) for x in cb]
+        for eng in ([2, 3, 4, 6] if n <= 256 else []) + [8, 0]:
+            s.set_option(OPT_ENGINE, eng)
+            r = s.solve_batch(cb, seed)
+            ok = all(np.array_equal(r.u[t], refs[t].u) and np.array_equal(r.v[t], refs[t].v)
+                     and r.total_cost[t] == refs[t].total_cost for t in range(b))
+            cases += 1
+            if not ok:
+                bad += 1
+                print(f"MISMATCH batch b={b} n={n} hi={hi} seed={seed} engine={eng}", flush=True)
+        continue
+    n = int(rng.choice([rng.integers(1, 64), rng.integers(64, 300), rng.integers(300, 1500), rng.integers(1500, 3000)]))
     c = rng.integers(0, hi, size=(n, n)).astype(np.int32)
     seed = int(rng.choice([KMB_SEED_BATCHED, KMB_SEED_KM]))
     ref = O.ref_solve_batched_km(c) if seed == KMB_SEED_BATCHED else O.ref_solve_km(c)
