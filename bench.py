@@ -484,7 +484,9 @@ def main():
                     "h2d_bytes_per_step": int(host.nbytes),
                     "d2h_bytes_per_step": int(count * N * (4 + 8 + 8) + count * 8 + count * 4),
                     "matches_device_run": ok_e2e},
-            "gpu_launches": args.steps,
+            # per timed step of the value leg: the engine kernel + k_batch_summary
+            # (the per-instance stats/status fold) — profiles/r01_bench_launches.csv
+            "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
             "extras": extras,
         }
