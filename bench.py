@@ -8,9 +8,12 @@ solver timed beside it.
 
 A step = one batched solve of this rank's shard of the 4096 instances
 (strong scaling: the job total is fixed).  ``value`` = 4096 / (max over ranks
-of the mean device time per step) with inputs resident in HBM; ``e2e`` is the
-same through the C ABI with pinned HOST buffers (H2D of the costs and D2H of
-assignment + duals + totals inside the timed region).  L2 is flushed (a
+of the mean device time per step) with inputs resident in HBM, through the
+stream-ordered call kmb_solve_batch_async_i32 (statuses checked after the timed
+region; the synchronous kmb_solve_batch_i32 is reported beside it as
+``sync_call``); ``e2e`` is the same through the synchronous C ABI call with
+pinned HOST buffers (H2D of the costs and D2H of assignment + duals + totals
+inside the timed region).  L2 is flushed (a
 256 MiB write) before every timed step.  At N=1, rank 0 also runs the
 config-5 (n=16384, 1 GiB) single-instance solve, whose reduced-cost scan is the
 HBM-bound kernel, and reports its roofline under ``extras`` (disable with
@@ -374,44 +377,48 @@ def main():
     hv = torch.empty((count, N), dtype=torch.int64).pin_memory()
     htot = torch.empty(count, dtype=torch.int64).pin_memory()
 
-    for _ in range(args.warmup):
-        solver.solve_batch_into(dcost, count, N, 1, r2c, du, dv, dtot)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    dstatus = torch.full((count,), -1, dtype=torch.int32, device=dev)
     phases = 0
     engine_used = 4
-    barrier(world)
+    for _ in range(args.warmup):
+        st = solver.solve_batch_into(dcost, count, N, 1, r2c, du, dv, dtot)
+        phases = st.phases
+        engine_used = st.engine
+        solver.solve_batch_async(dcost, count, N, 1, r2c, du, dv, dtot, dstatus)
     torch.cuda.synchronize()
-    clk = ClockSampler(local)
-    with clk:
-        for k in range(args.steps):
-            flush.fill_(k)
-            ev[k][0].record(stream)
-            st = solver.solve_batch_into(dcost, count, N, 1, r2c, du, dv, dtot)
-            ev[k][1].record(stream)
-            phases = st.phases
-            engine_used = st.engine
+
+    def timed_steps(call) -> float:
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        barrier(world)
         torch.cuda.synchronize()
-    barrier(world)
-    step_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
+        with clk:
+            for k in range(args.steps):
+                flush.fill_(k)
+                ev[k][0].record(stream)
+                call()
+                ev[k][1].record(stream)
+            torch.cuda.synchronize()
+        barrier(world)
+        return statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
+
+    clk = ClockSampler(local)
+    # value: the stream-ordered call (kmb_solve_batch_async_i32), one batch per
+    # step, statuses checked after the timed region
+    dstatus.fill_(-1)
+    step_ms = timed_steps(lambda: solver.solve_batch_async(dcost, count, N, 1, r2c, du, dv, dtot, dstatus))
+    if int(dstatus.abs().sum()) != 0:
+        raise RuntimeError("bench: an instance reported a nonzero status")
     step_ms_max = max_over_ranks(step_ms, world)
     value = BATCH / (step_ms_max * 1e-3)
+    # the synchronous call (status fold + host wait per step), reported beside it
+    sync_ms = max_over_ranks(timed_steps(lambda: solver.solve_batch_into(dcost, count, N, 1, r2c, du, dv, dtot)), world)
 
     # end to end through the C ABI with host buffers (H2D + kernel + D2H)
     for _ in range(max(1, args.warmup)):
         solver.solve_batch_into(hcost, count, N, 1, hr2c, hu, hv, htot, stats=False)
-    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-    barrier(world)
-    torch.cuda.synchronize()
-    with clk:
-        for k in range(args.steps):
-            flush.fill_(k)
-            e2e_ev[k][0].record(stream)
-            solver.solve_batch_into(hcost, count, N, 1, hr2c, hu, hv, htot, stats=False)
-            e2e_ev[k][1].record(stream)
-        torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in e2e_ev), world)
+    e2e_ms = max_over_ranks(timed_steps(
+        lambda: solver.solve_batch_into(hcost, count, N, 1, hr2c, hu, hv, htot, stats=False)), world)
     ok_e2e = bool(torch.equal(hr2c, r2c.cpu())) and bool(torch.equal(htot, dtot.cpu()))
 
     hbm_peak, peak_src = peaks()
@@ -468,6 +475,9 @@ def main():
                        "parallelism": f"instances sharded over {world} rank(s), one per GPU "
                                       f"({_BACKEND} for the max-over-ranks timing)",
                        "l2": "flushed (256 MiB write) before every timed step",
+                       "api": "value: kmb_solve_batch_async_i32 (stream-ordered, device buffers, "
+                              "statuses checked after the timed region); e2e: kmb_solve_batch_i32 "
+                              "with pinned host buffers",
                        "engine": ENGINES.get(engine_used, (str(engine_used), ""))[0]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic_used,
@@ -484,9 +494,11 @@ def main():
                     "h2d_bytes_per_step": int(host.nbytes),
                     "d2h_bytes_per_step": int(count * N * (4 + 8 + 8) + count * 8 + count * 4),
                     "matches_device_run": ok_e2e},
-            # per timed step of the value leg: the engine kernel + k_batch_summary
-            # (the per-instance stats/status fold) — profiles/r01_bench_launches.csv
-            "gpu_launches": 2 * args.steps,
+            # per timed step of the value leg (the stream-ordered call): the
+            # engine kernel — profiles/r01_bench_launches.csv
+            "gpu_launches": args.steps,
+            "sync_call": {"api": "kmb_solve_batch_i32 (status fold + host wait per step)",
+                          "ms_per_step": sync_ms, "value": BATCH / (sync_ms * 1e-3)},
             "clocks": clk.summary(),
             "extras": extras,
         }

@@ -129,6 +129,18 @@ int kmb_solve_batch_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, i
                         int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
                         int64_t* total_cost, kmb_stats* stats);
 
+/* Stream-ordered variant of kmb_solve_batch_i32 for device-resident batches:
+ * enqueues the solve on the context's stream and returns at once (no host
+ * synchronisation, so back-to-back batches pipeline and the call can be
+ * captured in a CUDA graph once a first call has sized the workspace).  All
+ * six buffers must be device memory; status[b] (batch int32) receives instance
+ * b's outcome when the stream reaches it: 0 ok, KMB_ENEGATIVE, KMB_ERANGE, or
+ * another nonzero code for an engine fault.  The return value reports argument
+ * and launch errors only. */
+int kmb_solve_batch_async_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, int32_t n,
+                              int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
+                              int64_t* total_cost, int32_t* status);
+
 /* One process, several GPUs (BASELINE config 3 "instances sharded across
  * GPUs" without one process per GPU): the batch is split into nctx contiguous
  * slices of equal size (+-1) and slice k is solved by kmb_solve_batch_i32 on

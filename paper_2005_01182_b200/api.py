@@ -23,11 +23,13 @@ from . import _build
 
 KMB_SEED_KM = 0
 KMB_SEED_BATCHED = 1
+KMB_OK, KMB_EINVAL, KMB_ENEGATIVE, KMB_ERANGE = 0, 1, 2, 3  # include/kmb.h status codes
 OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_U16, OPT_PIPELINE = 1, 2, 3, 4, 5, 6
 
 # every symbol include/kmb.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
-               "kmb_solve_batch_i32", "kmb_solve_batch_multi_i32", "kmb_nccl_unique_id",
+               "kmb_solve_batch_i32", "kmb_solve_batch_async_i32", "kmb_solve_batch_multi_i32",
+               "kmb_nccl_unique_id",
                "kmb_shard_init_nccl",
                "kmb_shard_init_callbacks", "kmb_solve_sharded_i32", "kmb_bench_scan",
                "kmb_last_instance_stats", "kmb_costs_from_points", "kmb_auction_i32",
@@ -80,6 +82,8 @@ def load_library(path: str | None = None):
                                       vp, vp, vp, vp, C.POINTER(Stats)]
         lib.kmb_solve_batch_i32.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32,
                                             vp, vp, vp, vp, C.POINTER(Stats)]
+        lib.kmb_solve_batch_async_i32.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32,
+                                                  vp, vp, vp, vp, vp]
         lib.kmb_solve_batch_multi_i32.argtypes = [C.POINTER(vp), C.c_int32, vp, C.c_int32, C.c_int32,
                                                   C.c_int32, vp, vp, vp, vp, C.POINTER(Stats)]
         lib.kmb_bench_scan.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32,
@@ -179,6 +183,16 @@ class Solver:
                                            C.byref(st) if st is not None else None)
         self._check(rc)
         return st
+
+    def solve_batch_async(self, costs, batch: int, n: int, seed: int, row_to_col, u, v,
+                          total_cost, status) -> None:
+        """Stream-ordered batch solve (kmb_solve_batch_async_i32): device buffers
+        only; enqueues on the solver's stream and returns without waiting;
+        per-instance statuses land in ``status`` (device int32)."""
+        self._check(self._lib.kmb_solve_batch_async_i32(
+            self._h, C.c_void_p(_ptr(costs)), batch, n, seed, C.c_void_p(_ptr(row_to_col)),
+            C.c_void_p(_ptr(u)), C.c_void_p(_ptr(v)), C.c_void_p(_ptr(total_cost)),
+            C.c_void_p(_ptr(status))))
 
     def last_instance_stats(self, batch: int):
         """Per-instance counters of the last batch solve: (batch, 11) int64."""

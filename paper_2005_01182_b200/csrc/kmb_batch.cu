@@ -690,16 +690,19 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
 int batch_max_n() { return 256; }
 
 // the kernel instance for n: dirty-column epoch starts for n <= 128
+#ifndef KMB_CTA_DIRTY_MAXN
+#define KMB_CTA_DIRTY_MAXN 128
+#endif
 template <bool SMEM_C>
 static void (*cta_kernel(int n))(BatchArgs) {
-  return n <= 128 ? k_cta_batch<SMEM_C, true> : k_cta_batch<SMEM_C, false>;
+  return n <= KMB_CTA_DIRTY_MAXN ? k_cta_batch<SMEM_C, true> : k_cta_batch<SMEM_C, false>;
 }
 
 // Shared-memory carveout (percent) for the L2 variant holding `want` resident
 // CTAs (capped by the register limit); the rest of the unified cache is L1.
 static int cta_carveout(int n, int want) {
   static int regs_cached[2] = {0, 0};  // benign race: every thread computes the same value
-  const int which = n <= 128 ? 1 : 0;
+  const int which = n <= KMB_CTA_DIRTY_MAXN ? 1 : 0;
   if (!regs_cached[which]) {
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, cta_kernel<false>(n)) != cudaSuccess) {

@@ -206,7 +206,7 @@ constexpr int64_t kStopped = 4;
 static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch, int32_t n,
                             int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
                             int64_t* total_cost, kmb_stats* stats, const char* who, int engine,
-                            double time_budget_s = 0.0) {
+                            double time_budget_s = 0.0, int32_t* async_status = nullptr) {
   cudaStream_t st = c->stream;
   const size_t cbytes = static_cast<size_t>(batch) * n * n * sizeof(int32_t);
   // auto: a batch (or pipeline chunk) that fits the CTA engine's residency in
@@ -265,6 +265,8 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   if (!is_device_ptr(total_cost)) { KMB_CUDA(c->btot.ensure(batch * 8)); dtot = c->btot.as<int64_t>(); }
   KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8));
   KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
+  // stream-ordered calls write the statuses straight into the caller's buffer
+  int32_t* const status_base = async_status ? async_status : c->bstatus.as<int32_t>();
   // U16 mode (warp/L2 engine, 4 or 8 columns per lane): a packing pass writes
   // 16-bit offsets from the row minima, halving the bytes every relax streams
   const bool u16 = engine == 4 && c->u16 && (np == 128 || np == 256);
@@ -293,7 +295,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       a.v = dv + ro;
       a.total_cost = dtot + lo;
       a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
-      a.status = c->bstatus.as<int32_t>() + lo;
+      a.status = status_base + lo;
       return kmb::launch_big(a, c->sm_count, s);
     }
     if (eng == 2 || eng == 6) {
@@ -308,7 +310,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       a.v = dv + ro;
       a.total_cost = dtot + lo;
       a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
-      a.status = c->bstatus.as<int32_t>() + lo;
+      a.status = status_base + lo;
       return kmb::launch_batch(a, c->sm_count, eng == 2, static_cast<int>(c->warps_per_sm), s, &grid);
     }
     kmb::WarpArgs a{};
@@ -323,7 +325,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.v = dv + ro;
     a.total_cost = dtot + lo;
     a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
-    a.status = c->bstatus.as<int32_t>() + lo;
+    a.status = status_base + lo;
     if (u16) {
       a.C16 = c->b16.as<uint16_t>() + ro * np;
       a.rmin = c->brmin.as<int32_t>() + ro;
@@ -349,6 +351,15 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     return e;
   };
   int used = engine;
+  if (async_status) {  // stream-ordered: enqueue and return (device buffers only)
+    if (warp_eng && np != n) {
+      KMB_CUDA(c->bpad.ensure(nb * np * 4));
+      KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4, nb, cudaMemcpyDeviceToDevice, st));
+      src = c->bpad.as<int32_t>();
+    }
+    KMB_CUDA(launch(0, batch, engine, st));
+    return KMB_OK;
+  }
   KMB_CUDA(cudaEventRecord(c->ev0, st));
   if (!pipelined) {
     if (host_in) KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
@@ -447,6 +458,30 @@ int kmb_solve_batch_i32(kmb_context* c, const int32_t* costs, int32_t batch, int
   KMB_CUDA(cudaSetDevice(c->device));
   return solve_batch_impl(c, costs, batch, n, seed, row_to_col, u, v, total_cost, stats, who,
                           c->engine);
+}
+
+// Stream-ordered batch solve (graph-capturable once the workspace is sized):
+// device buffers only, no host synchronisation, per-instance statuses to the
+// caller's device buffer.
+int kmb_solve_batch_async_i32(kmb_context* c, const int32_t* costs, int32_t batch, int32_t n,
+                              int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
+                              int64_t* total_cost, int32_t* status) {
+  const char* who = "kmb_solve_batch_async_i32";
+  if (!c) return fail(KMB_EINVAL, std::string(who) + ": NULL context");
+  if (batch <= 0 || n <= 0) return fail(KMB_EINVAL, std::string(who) + ": dimensions must be positive");
+  if (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED) return fail(KMB_EINVAL, std::string(who) + ": bad seed");
+  if (n > kmb::big_max_n())
+    return fail(KMB_EINVAL, std::string(who) + ": n > " + std::to_string(kmb::big_max_n()));
+  if (n > kmb::warp_max_n() && c->engine != 0 && c->engine != 8)
+    return fail(KMB_EINVAL, std::string(who) + ": n > 256 needs the single-CTA engine (8)");
+  KMB_CUDA(cudaSetDevice(c->device));
+  for (const void* p : {static_cast<const void*>(costs), static_cast<const void*>(row_to_col),
+                        static_cast<const void*>(u), static_cast<const void*>(v),
+                        static_cast<const void*>(total_cost), static_cast<const void*>(status)})
+    if (!p || !is_device_ptr(p))
+      return fail(KMB_EINVAL, std::string(who) + ": every buffer must be device memory");
+  return solve_batch_impl(c, costs, batch, n, seed, row_to_col, u, v, total_cost, nullptr, who,
+                          c->engine, 0.0, status);
 }
 
 // Several contexts (normally one per GPU): contiguous slices of the batch, each

@@ -532,3 +532,79 @@ def test_batch_multi_error_names_slice():
     finally:
         for s in solvers:
             s.close()
+
+
+def _dev_batch(c):
+    import torch
+    b, n, _ = c.shape
+    d = torch.from_numpy(np.ascontiguousarray(c)).cuda()
+    out = (torch.empty((b, n), dtype=torch.int32, device="cuda"),
+           torch.empty((b, n), dtype=torch.int64, device="cuda"),
+           torch.empty((b, n), dtype=torch.int64, device="cuda"),
+           torch.empty(b, dtype=torch.int64, device="cuda"),
+           torch.full((b,), -7, dtype=torch.int32, device="cuda"))
+    return d, out
+
+
+@pytest.mark.parametrize("engine,n", [(0, 128), (4, 128), (6, 100), (3, 40), (8, 300)])
+def test_batch_async_matches_sync(solver, engine, n):
+    """kmb_solve_batch_async_i32: stream-ordered, device buffers, statuses to a
+    device buffer; results equal the synchronous call's."""
+    import torch
+    rng = np.random.default_rng(n + engine)
+    c = W.CONFIGS["c3"].make(batch=96) if n == 128 else rng.integers(0, 10**6, (24, n, n)).astype(np.int32)
+    solver.set_option(OPT_ENGINE, engine)
+    try:
+        base = solver.solve_batch(c, KMB_SEED_BATCHED)
+        d, (r2c, u, v, tot, status) = _dev_batch(c)
+        solver.solve_batch_async(d, c.shape[0], n, KMB_SEED_BATCHED, r2c, u, v, tot, status)
+        torch.cuda.synchronize()
+    finally:
+        solver.set_option(OPT_ENGINE, 0)
+    assert int(status.abs().sum()) == 0
+    np.testing.assert_array_equal(tot.cpu().numpy(), base.total_cost)
+    np.testing.assert_array_equal(u.cpu().numpy(), base.u)
+    np.testing.assert_array_equal(v.cpu().numpy(), base.v)
+    np.testing.assert_array_equal(r2c.cpu().numpy(), base.row_to_col)
+
+
+def test_batch_async_statuses_and_errors(solver):
+    import torch
+    from paper_2005_01182_b200.api import KMB_ENEGATIVE, KMB_ERANGE
+    c = W.CONFIGS["c3"].make(batch=6)
+    c[2, 0, 0] = -5
+    c[4, 1, 1] = 1 << 29
+    d, (r2c, u, v, tot, status) = _dev_batch(c)
+    solver.solve_batch_async(d, 6, 128, KMB_SEED_BATCHED, r2c, u, v, tot, status)
+    torch.cuda.synchronize()
+    assert status.cpu().tolist() == [0, 0, KMB_ENEGATIVE, 0, KMB_ERANGE, 0]
+    ref = O.ref_solve_batched_km(c[5])
+    assert int(tot[5]) == ref.total_cost
+    with pytest.raises(KmbError, match="device memory"):
+        solver.solve_batch_async(c, 6, 128, KMB_SEED_BATCHED, r2c, u, v, tot, status)
+
+
+def test_batch_async_cuda_graph():
+    """The stream-ordered call captured in a CUDA graph and replayed on new data."""
+    import torch
+    from paper_2005_01182_b200 import Solver
+    c = W.CONFIGS["c3"].make(batch=64)
+    d, (r2c, u, v, tot, status) = _dev_batch(c)
+    s = Solver(0)
+    stream = torch.cuda.Stream()
+    s.set_stream(stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        s.solve_batch_async(d, 64, 128, KMB_SEED_BATCHED, r2c, u, v, tot, status)  # sizes the workspace
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+        s.solve_batch_async(d, 64, 128, KMB_SEED_BATCHED, r2c, u, v, tot, status)
+    c2 = W.CONFIGS["c3"].make(batch=128)[64:]
+    d.copy_(torch.from_numpy(c2))
+    tot.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    s.close()
+    for t in (0, 31, 63):
+        assert int(tot[t]) == O.ref_solve_batched_km(c2[t]).total_cost
+    assert int(status.abs().sum()) == 0
