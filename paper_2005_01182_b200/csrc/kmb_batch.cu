@@ -798,7 +798,10 @@ cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warp
   // L2 variant: leave the unified cache to L1 beyond the resident CTAs' state
   // (0.442 -> 0.413 ms at 512)
   int occ = 0;
-  const int want = (a.batch + sm_count - 1) / sm_count;  // CTAs per SM this batch needs
+  // CTAs per SM this batch needs; the chunks of one pipelined call share the
+  // largest chunk's value, so the carveout attribute does not flip per chunk
+  const int sized = a.carve_batch > a.batch ? a.carve_batch : a.batch;
+  const int want = (sized + sm_count - 1) / sm_count;
   cudaError_t e = prepare_launch(reinterpret_cast<const void*>(kern), threads, smem,
                                  smem_c ? -1 : cta_carveout(a.n, want), &occ);
   if (e != cudaSuccess) return e;

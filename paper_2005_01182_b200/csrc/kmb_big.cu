@@ -467,7 +467,7 @@ static cudaError_t launch_nt(const BigArgs& a, int sm_count, size_t smem, cudaSt
   // each, one CTA per SM for a single instance); the rest of the unified cache
   // is L1 for the cost rows
   const int64_t want = std::max<int64_t>(1, std::min<int64_t>(227 * 1024 / (smem + 1024),
-                                                              (a.batch + sm_count - 1) / sm_count));
+                                                              (std::max(a.batch, a.carve_batch) + sm_count - 1) / sm_count));
   const int carve = static_cast<int>(std::min<int64_t>(
       100, (want * static_cast<int64_t>(smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
   int occ = 0;

@@ -200,6 +200,10 @@ static int status_message(int status, const char* who) {
                                  std::to_string(status) + ")");
 }
 
+#ifndef KMB_TAPER_MIN  // the tapered schedule halves the last chunk down to this size
+#define KMB_TAPER_MIN 64
+#endif
+
 // instance status of a time budget that expired (single-CTA engine): not an error
 constexpr int64_t kStopped = 4;
 
@@ -240,7 +244,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     for (int k = 0; k < K && lo < batch; ++k) {
       int cnt = std::min(chunk, batch - lo);
       if (taper && lo + cnt >= batch) {  // the last chunk: halve it down
-        while (cnt > 64 && static_cast<int>(sched.size()) < kmb_context::kMaxChunks - 1) {
+        while (cnt > KMB_TAPER_MIN && static_cast<int>(sched.size()) < kmb_context::kMaxChunks - 1) {
           const int h = cnt / 2;
           sched.emplace_back(lo, h);
           lo += h;
@@ -278,6 +282,8 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   }
   const int32_t* src = dcost;  // warp engines: rows padded to the warp width
   int grid = 0;
+  // the chunks of a pipelined call size their carveout for the largest chunk
+  const int carve_batch = sched.empty() ? 0 : sched[0].second;
   // instances [lo, lo + cnt) on engine eng, stream s
   auto launch = [&](int lo, int cnt, int eng, cudaStream_t s) -> cudaError_t {
     const size_t ro = static_cast<size_t>(lo) * n;
@@ -296,6 +302,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       a.total_cost = dtot + lo;
       a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
       a.status = status_base + lo;
+      a.carve_batch = carve_batch;
       return kmb::launch_big(a, c->sm_count, s);
     }
     if (eng == 2 || eng == 6) {
@@ -311,6 +318,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       a.total_cost = dtot + lo;
       a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
       a.status = status_base + lo;
+      a.carve_batch = carve_batch;
       return kmb::launch_batch(a, c->sm_count, eng == 2, static_cast<int>(c->warps_per_sm), s, &grid);
     }
     kmb::WarpArgs a{};

@@ -85,6 +85,7 @@ struct BatchArgs {
   int64_t* total_cost;   // batch
   int64_t* stats;        // batch x KMB_ISTATS (may be null)
   int32_t* status;       // batch (0 ok)
+  int32_t carve_batch;   // launch hint: size the carveout for this many (0: batch)
 };
 
 int batch_max_n();
@@ -138,6 +139,7 @@ struct BigArgs {
   int64_t* stats;       // batch x KMB_ISTATS (may be null)
   int32_t* status;      // batch
   int32_t* converged;   // batch (may be null)
+  int32_t carve_batch;  // launch hint: size the carveout for this many (0: batch)
 };
 size_t big_smem_bytes(int n);
 int big_max_n();
