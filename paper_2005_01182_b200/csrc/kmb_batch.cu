@@ -38,6 +38,9 @@
 #ifndef KMB_CTA_GB  // survivor rows in flight per thread in the dirty recompute
 #define KMB_CTA_GB 2
 #endif
+#ifndef KMB_CTA_ONEBAR  // one CTA barrier per BFS round in cta_solve_dirty (A/B)
+#define KMB_CTA_ONEBAR 1
+#endif
 #ifndef KMB_CTA_STAGE_CLOCKS
 #define KMB_CTA_STAGE_CLOCKS 0
 #endif
@@ -94,6 +97,10 @@ struct CtaShared {
   int32_t nrows, nfound, ns, won, nd, pad_;
   int32_t lo_all, hi_all;
   int32_t red[8];  // per-warp min slack' / partial sums
+#if KMB_CTA_ONEBAR
+  int32_t cnt[3], fcnt[3], cnt2[2], fcnt2[2];  // one-barrier rounds (cta_solve_dirty)
+  int32_t red3[3][8];
+#endif
 };
 
 __device__ __forceinline__ void shared_min(uint32_t* p, uint32_t x) { atomicMin(p, x); }
@@ -135,6 +142,10 @@ __device__ __forceinline__ int cta_solve_dirty(const BatchArgs& a, const int32_t
     sm.nrows = n;
     sm.nfound = 0;
     sm.nd = 0;
+#if KMB_CTA_ONEBAR
+    for (int q = 0; q < 3; ++q) sm.cnt[q] = sm.fcnt[q] = 0;
+    sm.cnt2[0] = sm.cnt2[1] = sm.fcnt2[0] = sm.fcnt2[1] = 0;
+#endif
   }
   K key = KO::INF;
   int32_t v = 0, dc = 0;
@@ -171,6 +182,9 @@ __device__ __forceinline__ int cta_solve_dirty(const BatchArgs& a, const int32_t
   int nrows = n, head = 0, nfree = n;
   int32_t D = 0;
   int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
+#if KMB_CTA_ONEBAR
+  int kb = 0;  // one-barrier rounds: counter slot of this round
+#endif
   int status = 0;
   long long cyc[4] = {0, 0, 0, 0};  // relax, min (incl. B1), absorb (incl. B2), epoch end
   long long tl = clock64();
@@ -203,6 +217,7 @@ __device__ __forceinline__ int cta_solve_dirty(const BatchArgs& a, const int32_t
       K* dkey = reinterpret_cast<K*>(spare);
       for (int k = j; k < nd; k += T) dkey[k] = KO::INF;
       __syncthreads();
+      if (j == 0) sm.nd = 0;  // every thread has read it; the next appends come at an epoch end
       const int groups = nd > 0 ? max(1, T / nd) : 1;
       for (int item = j; nrows > 0 && item < nd * groups; item += T) {
         const int k = item % nd, g = item / nd;
@@ -233,10 +248,85 @@ __device__ __forceinline__ int cta_solve_dirty(const BatchArgs& a, const int32_t
     KMB_CSTAGE(0);
     // ---- min unreached slack' (hungarian.cpp:203-206): REDUX + one exchange ----
     const int32_t s = rch ? 0x7fffffff : KO::val(key) - v;
+#if KMB_CTA_ONEBAR
+    // One barrier per BFS round: absorb speculatively at the current D and
+    // publish the minimum over the columns that did not turn tight.  When
+    // anything turned tight anywhere there is no dual step and the round ends
+    // at B1; otherwise D = that minimum, absorb again, and B2 publishes it.
+    // Per-round counters are triple-buffered (slot kb written before B1, read
+    // after it, cleared two rounds ahead by thread 0 after B1) and the dual
+    // step's counters alternate by dual-step parity, so a fast thread's next
+    // round never races a slow thread's reads.
+    const bool tight = !rch && s == D;
+    const int32_t wm = __reduce_min_sync(FULL, tight ? 0x7fffffff : s);
+    if (tight) {
+      rch = true;
+      dc = D;
+      const int32_t par = KO::row(key);
+      tree_par[j] = par;
+      const int32_t root = root_row[par];
+      const int32_t i2 = match_col[j];
+      if (i2 < 0) {
+        atomicMin(claim + root, cclaim(epochs, j));
+        found[atomicAdd(&sm.fcnt[kb], 1)] = j;
+      } else {
+        const int32_t w2 = u[i2] - D;
+        w[i2] = w2;
+        root_row[i2] = root;
+        rows[nrows + atomicAdd(&sm.cnt[kb], 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
+      }
+    }
+    if (lane == 0) sm.red3[kb][wid] = wm;
+    __syncthreads();  // ------------------------------------------------ B1
+    int added = sm.cnt[kb], nfound = sm.fcnt[kb];
+    if (j == 0) {
+      const int kc = kb == 0 ? 2 : kb - 1;  // == (kb + 2) % 3
+      sm.cnt[kc] = 0;
+      sm.fcnt[kc] = 0;
+    }
+    if (added == 0 && nfound == 0) {
+      int32_t m = sm.red3[kb][0];
+      for (int q = 1; q < nw; ++q) m = min(m, sm.red3[kb][q]);
+      if (m == 0x7fffffff) {
+        status = -2;
+        break;
+      }
+      D = m;  // dual step (hungarian.cpp:207-215), applied lazily
+      ++dual_steps;
+      const int db = dual_steps & 1;
+      if (!rch && s == D) {
+        rch = true;
+        dc = D;
+        const int32_t par = KO::row(key);
+        tree_par[j] = par;
+        const int32_t root = root_row[par];
+        const int32_t i2 = match_col[j];
+        if (i2 < 0) {
+          atomicMin(claim + root, cclaim(epochs, j));
+          found[atomicAdd(&sm.fcnt2[db], 1)] = j;
+        } else {
+          const int32_t w2 = u[i2] - D;
+          w[i2] = w2;
+          root_row[i2] = root;
+          rows[nrows + atomicAdd(&sm.cnt2[db], 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
+        }
+      }
+      __syncthreads();  // ---------------------------------------------- B2 (dual steps)
+      added = sm.cnt2[db];
+      nfound = sm.fcnt2[db];
+      if (j == 0) {  // the other parity's last readers passed B2 of the previous dual step
+        sm.cnt2[db ^ 1] = 0;
+        sm.fcnt2[db ^ 1] = 0;
+      }
+    }
+    nrows += added;
+    kb = kb == 2 ? 0 : kb + 1;
+    KMB_CSTAGE(2);
+    if (nfound == 0) continue;
+#else
     const int32_t wm = __reduce_min_sync(FULL, s);
     if (lane == 0) sm.red[wid] = wm;
     __syncthreads();  // ------------------------------------------------ B1
-    if (j == 0) sm.nd = 0;  // every thread has read it (next appends: after B2)
     int32_t m = sm.red[0];
     for (int q = 1; q < nw; ++q) m = min(m, sm.red[q]);
     if (m > D) {
@@ -271,6 +361,7 @@ __device__ __forceinline__ int cta_solve_dirty(const BatchArgs& a, const int32_t
     const int nfound = sm.nfound;
     KMB_CSTAGE(2);
     if (nfound == 0) continue;
+#endif
 
     // ---- epoch end: augment and dissolve the trees that reached a free column.
     // Dirty-column mode: the rows appended this round are relaxed over all
