@@ -214,12 +214,12 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   cudaStream_t st = c->stream;
   const size_t cbytes = static_cast<size_t>(batch) * n * n * sizeof(int32_t);
   // auto: a batch (or pipeline chunk) that fits the CTA engine's residency in
-  // one wave runs one CTA per instance (shorter rounds: 0.42 vs 0.67 ms for a
+  // one wave runs one CTA per instance (shorter rounds: 0.38 vs 0.47 ms for a
   // 512-instance config-3 shard); larger batches one warp per instance, all
-  // resident (1.12 ms at 4096 vs 1.8 for CTAs)
+  // resident (1.00 ms at 4096 vs 1.7 for CTAs)
   const bool auto_engine = engine == 0 || engine == 1 || engine == 5;
   const int cap6 = auto_engine ? kmb::cta_batch_capacity(n, c->sm_count) : 0;
-  // n > 256: one 1024-thread CTA per instance (single-CTA engine, n <= 4096)
+  // n > 256: one 512-thread CTA per instance (single-CTA engine, n <= 4096)
   auto pick = [&](int cnt) { return n > kmb::warp_max_n() ? 8 : (cnt <= cap6 ? 6 : 4); };
   if (auto_engine) engine = pick(batch);
   const int np = kmb::warp_pitch(n);
@@ -230,7 +230,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   const bool warp_eng = engine == 3 || engine == 4;
   const bool pipelined = host_in && batch >= 256 && (!warp_eng || np == n);
   // chunk schedule [lo, lo + cnt): K equal chunks, and (tapered) the last one
-  // split by halving down to 32 instances, so the solve left after the final
+  // split by halving down to KMB_TAPER_MIN instances, so the solve left after the final
   // copy lands is a short one
   std::vector<std::pair<int, int>> sched;
   if (pipelined) {
