@@ -70,6 +70,12 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
 #ifndef KMB_WARP_CLAMP
 #define KMB_WARP_CLAMP 1
 #endif
+#ifndef KMB_WARP_RB_FAT  // rows per relax batch in the low-occupancy instance
+#define KMB_WARP_RB_FAT 8  // (2048 / 1536 batches: 72-reg build 0.671 / 0.600 ms; RB 5: .664 /
+#endif                     // .598, 8: .639 / .571, 12: .637 / .568; + single-row preload .674 / .610)
+#ifndef KMB_WARP_FAT  // low-occupancy instance for batches of <= 16 warps per SM (A/B)
+#define KMB_WARP_FAT 1
+#endif
 #ifndef KMB_WARP_RB4  // rows per relax batch for <= 4 columns per lane
 #define KMB_WARP_RB4 5  // A/B on c3 (tools/ab_lib.py): 4: 1.09, 5: 1.065, 6-8: 1.12, 12: 1.19 ms
 #endif
@@ -221,7 +227,7 @@ __device__ __forceinline__ uint32_t row_tag(int32_t w, int32_t row, const int32_
   }
 }
 
-template <int CPL, bool SMEM_C, bool NARROW, bool U16 = false>
+template <int CPL, bool SMEM_C, bool NARROW, bool U16 = false, int RB4 = KMB_WARP_RB4>
 __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* Cm, int inst,
                                               const WarpSmem& S, int lane) {
   using KO = Keys<NARROW>;
@@ -284,7 +290,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     // ---- relax rows[head, nrows)  (hungarian.cpp:164-172) ----
     int r = head;
     // RB rows in flight: entries, then all row loads, then the folds
-    constexpr int RB = CPL <= 4 ? KMB_WARP_RB4 : 4;
+    constexpr int RB = CPL <= 4 ? RB4 : 4;
     if constexpr (U16) {
       // offsets arrive pre-shifted: key = min(key, (d << 8) + tag'); the last
       // short batch repeats its last row (idempotent) instead of a serial tail
@@ -555,8 +561,12 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   return status;
 }
 
-template <int CPL, bool SMEM_C>
-__global__ void __launch_bounds__(128, 7) k_warp_batch(WarpArgs a) {
+// MINB: resident CTAs per SM the build targets — 7 (72 registers: a 4096
+// config-3 batch resident in one wave) or 4 (128 registers, deeper relax
+// batches) for batches that need at most 16 warps per SM
+template <int CPL, bool SMEM_C, int MINB = 7>
+__global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
+  constexpr int RBK = MINB >= 7 ? KMB_WARP_RB4 : KMB_WARP_RB_FAT;
   extern __shared__ __align__(16) unsigned char dyn[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;  // warp in block
@@ -671,12 +681,12 @@ __global__ void __launch_bounds__(128, 7) k_warp_batch(WarpArgs a) {
         if (use16 && hi_all < (1 << 21))
           status = solve_instance<CPL, false, true, true>(a, Cm, inst, S, lane);
         else if (hi_all < (1 << 21))
-          status = solve_instance<CPL, SMEM_C, true>(a, Cm, inst, S, lane);
+          status = solve_instance<CPL, SMEM_C, true, false, RBK>(a, Cm, inst, S, lane);
         else
-          status = solve_instance<CPL, SMEM_C, false>(a, Cm, inst, S, lane);
+          status = solve_instance<CPL, SMEM_C, false, false, RBK>(a, Cm, inst, S, lane);
       } else {
-        status = hi_all < (1 << 21) ? solve_instance<CPL, SMEM_C, true>(a, Cm, inst, S, lane)
-                                    : solve_instance<CPL, SMEM_C, false>(a, Cm, inst, S, lane);
+        status = hi_all < (1 << 21) ? solve_instance<CPL, SMEM_C, true, false, RBK>(a, Cm, inst, S, lane)
+                                    : solve_instance<CPL, SMEM_C, false, false, RBK>(a, Cm, inst, S, lane);
       }
     } else {
       for (int k = lane; k < n; k += 32) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
@@ -760,10 +770,17 @@ size_t warp_smem_per_warp(int n, int pitch, bool smem_c, bool u16) {
   return (c + static_cast<size_t>(warp_state_words(n, u16)) * 4 + 16 + 15) & ~static_cast<size_t>(15);
 }
 
-template <int CPL, bool SMEM_C>
+template <int CPL, bool SMEM_C, int MINB = 7>
 static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, int warps_per_sm,
                             cudaStream_t st, int* grid_out) {
-  auto kern = k_warp_batch<CPL, SMEM_C>;
+  if constexpr (KMB_WARP_FAT && MINB == 7 && CPL == 4 && !SMEM_C) {
+    // a batch that needs at most 4 CTAs (16 warps) per SM runs the 128-register
+    // instance (config-3 shards of <= 2,368 instances)
+    if (a.C16 == nullptr && warps_per_sm == 0 &&
+        (a.batch + wpb - 1) / wpb <= 4 * sm_count)
+      return launch_t<CPL, SMEM_C, 4>(a, sm_count, wpb, warps_per_sm, st, grid_out);
+  }
+  auto kern = k_warp_batch<CPL, SMEM_C, MINB>;
   const size_t smem = warp_smem_per_warp(a.n, a.pitch, SMEM_C, a.C16 != nullptr) * wpb;
   // Shared-memory carveout: just the state of the CTAs per SM this launch
   // needs (all instances resident in one wave, at most the register limit),
@@ -772,7 +789,7 @@ static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, int warps_
   // 196 KB carveout instead of the maximum; the longest instance alone 0.61 ->
   // 0.48 ms)
   int occ = 0;
-  static int regs_cached[2][4] = {};  // benign race: every thread computes the same value
+  static int regs_cached[2][4] = {};  // per instantiation; benign race: every thread computes the same value
   int& regs = regs_cached[SMEM_C ? 1 : 0][CPL == 1 ? 0 : CPL == 2 ? 1 : CPL == 4 ? 2 : 3];
   if (!regs) {
     cudaFuncAttributes fa{};
