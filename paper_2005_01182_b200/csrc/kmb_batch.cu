@@ -27,18 +27,19 @@
 #ifndef KMB_CTA_RB  // rows per relax batch
 #define KMB_CTA_RB 4  // A/B (tools/ab_cta.py, 512-shard): 2: .449, 3: .399, 4: .386, 5: .415, 8: .399, 16: .473 ms
 #endif
-// epoch start (cta_solve_dirty, n <= 128): recompute only the reset ("dirty")
-// columns, threads split over (dirty column, survivor-row group) pairs, instead
-// of re-relaxing every survivor row over all columns (~80% of the rows relaxed
-// on config 3; 1024-shard 0.509 -> 0.481 ms, 512 0.386 -> 0.389, c1 n = 256
-// 0.194 -> 0.202: n > 128 keeps the full re-relax, cta_solve_full)
-// (A/B, tools/ab_cta.py, 512-shard / 1024-shard / c1 ms: full re-relax .433 /
-// .581 / .231; dirty GB=1 .403 / .511 / .217, GB=2 .389 / .481 / .203, GB=3
-// .389 / .485 / .204, GB=4 .400 / .511 / .212, GB=8 .403 / .496 / .208)
+// Epoch start: recompute only the reset ("dirty") columns, threads split over
+// (dirty column, survivor-row group) pairs, instead of re-relaxing every
+// survivor row over all columns (~80% of the rows relaxed on config 3).  With
+// one barrier per BFS round (KMB_CTA_ONEBAR) it beats the full re-relax at
+// every n <= 256: 512-shard 0.386 -> 0.373 ms, 1024-shard 0.509 -> 0.468, c1
+// (n = 256) 0.197 -> 0.186.  Rows in flight per thread in the recompute (A/B,
+// tools/ab_cta.py, 512-shard / 1024-shard / c1 ms, two-barrier build): GB=1
+// .403 / .511 / .217, GB=2 .389 / .481 / .203, GB=3 .389 / .485 / .204, GB=4
+// .400 / .511 / .212, GB=8 .403 / .496 / .208.
 #ifndef KMB_CTA_GB  // survivor rows in flight per thread in the dirty recompute
 #define KMB_CTA_GB 2
 #endif
-#ifndef KMB_CTA_ONEBAR  // one CTA barrier per BFS round in cta_solve_dirty (A/B)
+#ifndef KMB_CTA_ONEBAR  // one CTA barrier per BFS round (A/B)
 #define KMB_CTA_ONEBAR 1
 #endif
 #ifndef KMB_CTA_STAGE_CLOCKS
@@ -92,13 +93,13 @@ __device__ __forceinline__ bool cclaimed(uint32_t c, int epoch) {
 
 struct CtaShared {
   uint64_t bar;  // mbarrier of the TMA bulk copy
-  // (pad_: with a 7-word header ptxas gives the full-re-relax instance 48
+  // (pad_: with a 7-word header ptxas gave the former full-re-relax build 48
   // registers and stops keeping a relax batch's loads in flight; 62 with 8)
   int32_t nrows, nfound, ns, won, nd, pad_;
   int32_t lo_all, hi_all;
   int32_t red[8];  // per-warp min slack' / partial sums
 #if KMB_CTA_ONEBAR
-  int32_t cnt[3], fcnt[3], cnt2[2], fcnt2[2];  // one-barrier rounds (cta_solve_dirty)
+  int32_t cnt[3], fcnt[3], cnt2[2], fcnt2[2];  // one-barrier rounds
   int32_t red3[3][8];
 #endif
 };
@@ -124,7 +125,7 @@ __host__ __device__ inline size_t cta_smem_bytes(int n, bool smem_c) {
 }
 
 template <bool SMEM_C, bool NARROW>
-__device__ __forceinline__ int cta_solve_dirty(const BatchArgs& a, const int32_t* Cm, int inst,
+__device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, int inst,
                                          CtaShared& sm, int2* rows, int2* spare, int32_t* u,
                                          int32_t* w, int32_t* root_row, int32_t* match_row,
                                          int32_t* match_col, int32_t* tree_par, int32_t* found,
@@ -458,207 +459,7 @@ __device__ __forceinline__ int cta_solve_dirty(const BatchArgs& a, const int32_t
   return status;
 }
 
-// Full survivor re-relax at epoch starts (the original CTA engine; n > 128).
-template <bool SMEM_C, bool NARROW>
-__device__ __forceinline__ int cta_solve_full(const BatchArgs& a, const int32_t* Cm, int inst,
-                                         CtaShared& sm, int2* rows, int2* spare, int32_t* u,
-                                         int32_t* w, int32_t* root_row, int32_t* match_row,
-                                         int32_t* match_col, int32_t* tree_par, int32_t* found,
-                                         uint32_t* claim) {
-  using KO = CKeys<NARROW>;
-  using K = typename KO::K;
-  constexpr uint32_t FULL = 0xffffffffu;
-  const int n = a.n, T = blockDim.x, nw = T >> 5;
-  const int j = threadIdx.x, lane = j & 31, wid = j >> 5;
-  const bool own = j < n;
-  const int32_t* colp = Cm + (own ? j : 0);  // this thread's column
-
-  for (int k = j; k < n; k += T) rows[k] = make_int2(k, static_cast<int32_t>(KO::tag(w[k], k)));
-  if (j == 0) {
-    sm.nrows = n;
-    sm.nfound = 0;
-  }
-  K key = KO::INF;
-  int32_t v = 0, dc = 0;
-  bool rch = !own;
-  int nrows = n, head = 0, nfree = n;
-  int32_t D = 0;
-  int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
-  int status = 0;
-  long long cyc[4] = {0, 0, 0, 0};  // relax, min (incl. B1), absorb (incl. B2), epoch end
-  long long tl = clock64();
-  const long long t_begin = tl;
-#if KMB_CTA_STAGE_CLOCKS
-#define KMB_CSTAGE(k)               \
-  do {                              \
-    const long long t_ = clock64(); \
-    cyc[k] += t_ - tl;              \
-    tl = t_;                        \
-  } while (0)
-#else
-#define KMB_CSTAGE(k) (void)tl
-#endif
-  __syncthreads();
-
-  while (nfree > 0) {
-    ++rounds;
-    // ---- relax rows[head, nrows) for column j (hungarian.cpp:164-172) ----
-    int r = head;
-    for (; r + KMB_CTA_RB - 1 < nrows; r += KMB_CTA_RB) {
-      int2 e[KMB_CTA_RB];
-      int32_t c[KMB_CTA_RB];
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[r + k];
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
-    }
-    if (nrows - r == 1) {
-      const int2 e = rows[r];
-      key = KO::kmin(key, KO::make(ldc<SMEM_C>(colp + e.x * n), static_cast<uint32_t>(e.y), e.x));
-    } else if (r < nrows) {
-      // 2..KMB_CTA_RB-1 rows: one batch with the last row repeated (the fold is
-      // idempotent), so every load is in flight at once
-      int2 e[KMB_CTA_RB];
-      int32_t c[KMB_CTA_RB];
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[min(r + k, nrows - 1)];
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
-#pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
-    }
-    if (rounds == 1 && a.seed == 1 && own) v = KO::val(key);  // column reduction, :328-333
-    rows_scanned += nrows - head;
-    head = nrows;
-    KMB_CSTAGE(0);
-    // ---- min unreached slack' (hungarian.cpp:203-206): REDUX + one exchange ----
-    const int32_t s = rch ? 0x7fffffff : KO::val(key) - v;
-    const int32_t wm = __reduce_min_sync(FULL, s);
-    if (lane == 0) sm.red[wid] = wm;
-    __syncthreads();  // ------------------------------------------------ B1
-    int32_t m = sm.red[0];
-    for (int q = 1; q < nw; ++q) m = min(m, sm.red[q]);
-    if (m > D) {
-      if (m == 0x7fffffff) {
-        status = -2;
-        break;
-      }
-      D = m;  // dual step (hungarian.cpp:207-215), applied lazily
-      ++dual_steps;
-    }
-    KMB_CSTAGE(1);
-    // ---- absorb (hungarian.cpp:186-199) ----
-    if (!rch && s == D) {
-      rch = true;
-      dc = D;
-      const int32_t par = KO::row(key);
-      tree_par[j] = par;
-      const int32_t root = root_row[par];
-      const int32_t i2 = match_col[j];
-      if (i2 < 0) {
-        atomicMin(claim + root, cclaim(epochs, j));
-        found[atomicAdd(&sm.nfound, 1)] = j;
-      } else {
-        const int32_t w2 = u[i2] - D;
-        w[i2] = w2;
-        root_row[i2] = root;
-        rows[atomicAdd(&sm.nrows, 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
-      }
-    }
-    __syncthreads();  // ------------------------------------------------ B2
-    nrows = sm.nrows;
-    const int nfound = sm.nfound;
-    KMB_CSTAGE(2);
-    if (nfound == 0) continue;
-
-    // ---- epoch end: augment and dissolve the trees that reached a free column
-    if (own) {
-      if (rch) {
-        if (cclaimed(claim[root_row[tree_par[j]]], epochs)) {
-          v -= D - dc;
-          rch = false;
-          key = KO::INF;
-        }
-      } else if (key != KO::INF && cclaimed(claim[root_row[KO::row(key)]], epochs)) {
-        key = KO::INF;
-      }
-    }
-    if (j == 0) {
-      sm.ns = 0;
-      sm.won = 0;
-    }
-    __syncthreads();
-    for (int q = j; q < nrows; q += T) {
-      const int2 e = rows[q];
-      if (cclaimed(claim[root_row[e.x]], epochs)) u[e.x] = w[e.x] + D;
-      else spare[atomicAdd(&sm.ns, 1)] = e;
-    }
-    for (int f = j; f < nfound; f += T) {
-      int32_t jj = found[f];
-      if (claim[root_row[tree_par[jj]]] != cclaim(epochs, jj)) continue;
-      atomicAdd(&sm.won, 1);
-      for (;;) {
-        const int32_t i = tree_par[jj];
-        const int32_t nx = match_row[i];
-        match_row[i] = jj;
-        match_col[jj] = i;
-        if (nx < 0) break;
-        jj = nx;
-      }
-    }
-    __syncthreads();
-    nfree -= sm.won;
-    nrows = sm.ns;
-    int2* t = rows;
-    rows = spare;
-    spare = t;
-    head = 0;  // survivors relax once more for the reset columns
-    ++epochs;
-    __syncthreads();
-    if (j == 0) {
-      sm.nrows = nrows;
-      sm.nfound = 0;
-    }
-    __syncthreads();
-    KMB_CSTAGE(3);
-  }
-#undef KMB_CSTAGE
-  // ---- outputs ----
-  int32_t tot = 0;  // per-thread entry < 2^29; per-warp sum < 2^34 -> reduce in 64 bits
-  int64_t tot64 = 0;
-  if (own) {
-    const int32_t mr = match_row[j];
-    a.row_to_col[static_cast<int64_t>(inst) * n + j] = mr;
-    a.u[static_cast<int64_t>(inst) * n + j] = u[j];
-    a.v[static_cast<int64_t>(inst) * n + j] = v;
-    if (mr >= 0) tot = ldc<SMEM_C>(Cm + j * n + mr);
-  }
-  tot64 = tot;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) tot64 += __shfl_xor_sync(FULL, tot64, o);
-  __syncthreads();
-  if (lane == 0) reinterpret_cast<int64_t*>(spare)[wid] = tot64;  // spare rows are dead now
-  __syncthreads();
-  if (j == 0) {
-    int64_t t = 0;
-    for (int q = 0; q < nw; ++q) t += reinterpret_cast<int64_t*>(spare)[q];
-    a.total_cost[inst] = t;
-    if (a.stats) {
-      int64_t* o = a.stats + KMB_ISTATS * static_cast<int64_t>(inst);
-      o[0] = epochs;
-      o[1] = dual_steps;
-      o[2] = rows_scanned;
-      o[3] = rounds;
-      o[4] = KMB_CTA_STAGE_CLOCKS ? cyc[0] + cyc[1] + cyc[2] + cyc[3] : clock64() - t_begin;
-      for (int k = 0; k < 4; ++k) o[5 + k] = cyc[k];
-    }
-  }
-  return status;
-}
-
-template <bool SMEM_C, bool DIRTY>
+template <bool SMEM_C>
 __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ CtaShared sm;
@@ -763,15 +564,11 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
       for (int k = j; k < n; k += T) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
       if (j == 0) a.total_cost[inst] = 0;
     } else if (hi_all < (1 << 21)) {
-      status = DIRTY ? cta_solve_dirty<SMEM_C, true>(a, Cm, inst, sm, rows, spare, u, w, root_row,
-                                                     match_row, match_col, tree_par, found, claim, dlist)
-                     : cta_solve_full<SMEM_C, true>(a, Cm, inst, sm, rows, spare, u, w, root_row,
-                                                    match_row, match_col, tree_par, found, claim);
+      status = cta_solve<SMEM_C, true>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
+                                       match_col, tree_par, found, claim, dlist);
     } else {
-      status = DIRTY ? cta_solve_dirty<SMEM_C, false>(a, Cm, inst, sm, rows, spare, u, w, root_row,
-                                                      match_row, match_col, tree_par, found, claim, dlist)
-                     : cta_solve_full<SMEM_C, false>(a, Cm, inst, sm, rows, spare, u, w, root_row,
-                                                     match_row, match_col, tree_par, found, claim);
+      status = cta_solve<SMEM_C, false>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
+                                       match_col, tree_par, found, claim, dlist);
     }
     if (j == 0) a.status[inst] = status;
     __syncthreads();
@@ -780,30 +577,20 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
 
 int batch_max_n() { return 256; }
 
-// the kernel instance for n: dirty-column epoch starts for n <= 128
-#ifndef KMB_CTA_DIRTY_MAXN
-#define KMB_CTA_DIRTY_MAXN 128
-#endif
-template <bool SMEM_C>
-static void (*cta_kernel(int n))(BatchArgs) {
-  return n <= KMB_CTA_DIRTY_MAXN ? k_cta_batch<SMEM_C, true> : k_cta_batch<SMEM_C, false>;
-}
-
 // Shared-memory carveout (percent) for the L2 variant holding `want` resident
 // CTAs (capped by the register limit); the rest of the unified cache is L1.
 static int cta_carveout(int n, int want) {
-  static int regs_cached[2] = {0, 0};  // benign race: every thread computes the same value
-  const int which = n <= KMB_CTA_DIRTY_MAXN ? 1 : 0;
-  if (!regs_cached[which]) {
+  static int regs_cached = 0;  // benign race: every thread computes the same value
+  if (!regs_cached) {
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, cta_kernel<false>(n)) != cudaSuccess) {
+    if (cudaFuncGetAttributes(&fa, k_cta_batch<false>) != cudaSuccess) {
       cudaGetLastError();
       return 100;
     }
-    regs_cached[which] = fa.numRegs > 0 ? fa.numRegs : 1;
+    regs_cached = fa.numRegs > 0 ? fa.numRegs : 1;
   }
   const int threads = ((n + 31) / 32) * 32;
-  const int regs = ((regs_cached[which] + 7) / 8) * 8;
+  const int regs = ((regs_cached + 7) / 8) * 8;
   int ctas = 65536 / (threads * regs);
   ctas = ctas < 1 ? 1 : (ctas > 32 ? 32 : ctas);
   if (want > 0 && want < ctas) ctas = want;
@@ -871,7 +658,7 @@ int cta_batch_capacity(int n, int sm_count) {  // instances resident at once (L2
   if (n < 1 || n > 256) return 0;
   const int threads = ((n + 31) / 32) * 32;
   int occ = 0;
-  if (prepare_launch(reinterpret_cast<const void*>(cta_kernel<false>(n)), threads,
+  if (prepare_launch(reinterpret_cast<const void*>(k_cta_batch<false>), threads,
                      cta_smem_bytes(n, false), cta_carveout(n, 0), &occ) != cudaSuccess) {
     cudaGetLastError();
     return 0;
@@ -885,7 +672,7 @@ cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warp
   const int threads = ((a.n + 31) / 32) * 32;
   if (smem_c && cta_smem_bytes(a.n, true) > 200 * 1024) smem_c = false;
   const size_t smem = cta_smem_bytes(a.n, smem_c);
-  auto kern = smem_c ? cta_kernel<true>(a.n) : cta_kernel<false>(a.n);
+  auto kern = smem_c ? k_cta_batch<true> : k_cta_batch<false>;
   // L2 variant: leave the unified cache to L1 beyond the resident CTAs' state
   // (0.442 -> 0.413 ms at 512)
   int occ = 0;
