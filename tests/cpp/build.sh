@@ -10,6 +10,11 @@ mkdir -p "$HERE/build"
 # simulated-shard protocol library (no reference needed)
 g++ -O2 -std=c++17 -fPIC -shared -I"$ROOT/paper_2005_01182_b200/csrc" "$HERE/shard_sim.cpp" \
   -o "$HERE/build/libshardsim.so"
+# C ABI + CUDA runtime host test (stream-ordered call, CUDA graph, multi-context)
+CUDA_HOME=${CUDA_HOME:-/usr/local/cuda}
+g++ -O2 -std=c++17 -I"$ROOT/include" -I"$CUDA_HOME/include" "$HERE/test_stream.cpp" \
+  -L"$ROOT/paper_2005_01182_b200" -lkmb -L"$CUDA_HOME/lib64" -lcudart \
+  -Wl,-rpath,'$ORIGIN/../../../paper_2005_01182_b200' -o "$HERE/build/test_stream"
 if [ ! -f "$REF/include/ot/hungarian.hpp" ]; then
   echo "reference headers absent; keeping prebuilt binary" ; exit 0
 fi

@@ -27,3 +27,15 @@ def test_cpp_reference_harness():
     out = subprocess.run([b], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "harness: 0 failed" in out.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_stream_ordered_and_graph():
+    """C++ host through the C ABI: the stream-ordered call, its CUDA-graph
+    capture/replay, the multi-context split and per-instance statuses."""
+    b = os.path.join(HERE, "cpp", "build", "test_stream")
+    if not os.path.exists(b):
+        pytest.fail(f"{b} missing: run tests/cpp/build.sh")
+    out = subprocess.run([b], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "test_stream: ok" in out.stdout
