@@ -153,6 +153,9 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
   bool rch = !own;
   bool dirty_round = false;
   int dirty_k = -1;  // this column's slot in dlist while it is dirty
+  // this column's matched row and its u: both change only at epoch ends, so
+  // they are kept in registers (one dependent shared load less per absorb)
+  int32_t mi2 = -1, mu2 = 0;
   auto relax = [&](int r, int end) {
     for (; r + KMB_CTA_RB - 1 < end; r += KMB_CTA_RB) {
       int2 e[KMB_CTA_RB];
@@ -266,12 +269,12 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
       const int32_t par = KO::row(key);
       tree_par[j] = par;
       const int32_t root = root_row[par];
-      const int32_t i2 = match_col[j];
+      const int32_t i2 = mi2;
       if (i2 < 0) {
         atomicMin(claim + root, cclaim(epochs, j));
         found[atomicAdd(&sm.fcnt[kb], 1)] = j;
       } else {
-        const int32_t w2 = u[i2] - D;
+        const int32_t w2 = mu2 - D;
         w[i2] = w2;
         root_row[i2] = root;
         rows[nrows + atomicAdd(&sm.cnt[kb], 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
@@ -301,12 +304,12 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
         const int32_t par = KO::row(key);
         tree_par[j] = par;
         const int32_t root = root_row[par];
-        const int32_t i2 = match_col[j];
+        const int32_t i2 = mi2;
         if (i2 < 0) {
           atomicMin(claim + root, cclaim(epochs, j));
           found[atomicAdd(&sm.fcnt2[db], 1)] = j;
         } else {
-          const int32_t w2 = u[i2] - D;
+          const int32_t w2 = mu2 - D;
           w[i2] = w2;
           root_row[i2] = root;
           rows[nrows + atomicAdd(&sm.cnt2[db], 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
@@ -346,12 +349,12 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
       const int32_t par = KO::row(key);
       tree_par[j] = par;
       const int32_t root = root_row[par];
-      const int32_t i2 = match_col[j];
+      const int32_t i2 = mi2;
       if (i2 < 0) {
         atomicMin(claim + root, cclaim(epochs, j));
         found[atomicAdd(&sm.nfound, 1)] = j;
       } else {
-        const int32_t w2 = u[i2] - D;
+        const int32_t w2 = mu2 - D;
         w[i2] = w2;
         root_row[i2] = root;
         rows[atomicAdd(&sm.nrows, 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
@@ -410,6 +413,10 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
     }
     __syncthreads();
     nfree -= sm.won;
+    if (own) {  // flips and dissolves are done (barrier above)
+      mi2 = match_col[j];
+      mu2 = mi2 >= 0 ? u[mi2] : 0;
+    }
     nrows = sm.ns;
     int2* t = rows;
     rows = spare;

@@ -6,7 +6,7 @@ from paper_2005_01182_b200 import Solver, workloads as W
 from paper_2005_01182_b200.api import OPT_ENGINE
 s = Solver(0)
 full = W.CONFIGS["c3"].make()
-for b in (512, 1024, 4096):
+for b in [int(x) for x in os.environ.get("BATCHES", "512,1024,4096").split(",")]:
     c = torch.from_numpy(full[:b].copy()).cuda(); n = 128
     r2c = torch.empty((b, n), dtype=torch.int32, device="cuda"); u = torch.empty((b, n), dtype=torch.int64, device="cuda")
     v = torch.empty_like(u); tot = torch.empty(b, dtype=torch.int64, device="cuda")
