@@ -73,6 +73,13 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
 #ifndef KMB_WARP_RB_FAT  // rows per relax batch in the low-occupancy instance
 #define KMB_WARP_RB_FAT 8  // (2048 / 1536 batches: 72-reg build 0.671 / 0.600 ms; RB 5: .664 /
 #endif                     // .598, 8: .639 / .571, 12: .637 / .568; + single-row preload .674 / .610)
+#ifndef KMB_WARP_CACHE_ALL  // the register cache in the 72-register build too (A/B: spills, c3 0.997 -> 1.166 ms)
+#define KMB_WARP_CACHE_ALL 0
+#endif
+#ifndef KMB_WARP_FAT_CACHE  // matched rows / u in registers in the low-occupancy build
+// (A/B: 2048 0.639 -> 0.625 ms, 1536 0.571 -> 0.559)
+#define KMB_WARP_FAT_CACHE 1
+#endif
 #ifndef KMB_WARP_FAT  // low-occupancy instance for batches of <= 16 warps per SM (A/B)
 #define KMB_WARP_FAT 1
 #endif
@@ -227,7 +234,8 @@ __device__ __forceinline__ uint32_t row_tag(int32_t w, int32_t row, const int32_
   }
 }
 
-template <int CPL, bool SMEM_C, bool NARROW, bool U16 = false, int RB4 = KMB_WARP_RB4>
+template <int CPL, bool SMEM_C, bool NARROW, bool U16 = false, int RB4 = KMB_WARP_RB4,
+          bool CACHE = false>
 __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* Cm, int inst,
                                               const WarpSmem& S, int lane) {
   using KO = Keys<NARROW>;
@@ -266,6 +274,14 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     if (c0 + q >= n) pad |= 1u << q;
   }
   uint32_t rch = pad;  // bit q: column c0+q reached (padding counts as reached)
+  // CACHE (low-occupancy build): each column's matched row and its u in
+  // registers between epoch ends (both change only there)
+  int32_t mi2[CACHE ? CPL : 1], mu2[CACHE ? CPL : 1];
+#pragma unroll
+  for (int q = 0; q < (CACHE ? CPL : 1); ++q) {
+    mi2[q] = -1;
+    mu2[q] = 0;
+  }
   int nrows = n, head = 0, nfree = n;  // rows[0, nrows) reached; [head, nrows) to relax
   int32_t D = 0;
   int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
@@ -443,12 +459,12 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
         const int32_t par = KO::row(key[q]);
         tree_par[col] = par;
         const int32_t root = root_row[par];
-        const int32_t i2 = match_col[col];
+        const int32_t i2 = CACHE ? mi2[CACHE ? q : 0] : match_col[col];
         if (i2 < 0) {
           atomicMin(claim + root, wclaim(epochs, col));
           found[atomicAdd(S.ctr + 1, 1)] = col;
         } else {
-          const int32_t w2 = u[i2] - D;
+          const int32_t w2 = (CACHE ? mu2[CACHE ? q : 0] : u[i2]) - D;
           w[i2] = w2;
           root_row[i2] = root;
           rows[atomicAdd(S.ctr, 1)] =
@@ -522,6 +538,13 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     }
     __syncwarp();
     nfree -= won;
+    if constexpr (CACHE) {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        mi2[q] = (pad >> q) & 1 ? -1 : match_col[c0 + q];
+        mu2[q] = mi2[q] >= 0 ? u[mi2[q]] : 0;
+      }
+    }
     int2* t = rows;
     rows = spare;
     spare = t;
@@ -567,6 +590,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
 template <int CPL, bool SMEM_C, int MINB = 7>
 __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
   constexpr int RBK = MINB >= 7 ? KMB_WARP_RB4 : KMB_WARP_RB_FAT;
+  constexpr bool CK = (MINB < 7 || KMB_WARP_CACHE_ALL) && KMB_WARP_FAT_CACHE;
   extern __shared__ __align__(16) unsigned char dyn[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;  // warp in block
@@ -681,12 +705,12 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
         if (use16 && hi_all < (1 << 21))
           status = solve_instance<CPL, false, true, true>(a, Cm, inst, S, lane);
         else if (hi_all < (1 << 21))
-          status = solve_instance<CPL, SMEM_C, true, false, RBK>(a, Cm, inst, S, lane);
+          status = solve_instance<CPL, SMEM_C, true, false, RBK, CK>(a, Cm, inst, S, lane);
         else
-          status = solve_instance<CPL, SMEM_C, false, false, RBK>(a, Cm, inst, S, lane);
+          status = solve_instance<CPL, SMEM_C, false, false, RBK, CK>(a, Cm, inst, S, lane);
       } else {
-        status = hi_all < (1 << 21) ? solve_instance<CPL, SMEM_C, true, false, RBK>(a, Cm, inst, S, lane)
-                                    : solve_instance<CPL, SMEM_C, false, false, RBK>(a, Cm, inst, S, lane);
+        status = hi_all < (1 << 21) ? solve_instance<CPL, SMEM_C, true, false, RBK, CK>(a, Cm, inst, S, lane)
+                                    : solve_instance<CPL, SMEM_C, false, false, RBK, CK>(a, Cm, inst, S, lane);
       }
     } else {
       for (int k = lane; k < n; k += 32) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
