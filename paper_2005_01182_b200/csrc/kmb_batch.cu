@@ -6,7 +6,8 @@
 // (:223-309), the reductions of :323-333 as seed 1 — laid out so a round's
 // dependency chain is short: each thread folds only its own column, the
 // min-slack reduction is one REDUX per warp plus one shared-memory exchange,
-// and a round costs two CTA barriers.
+// a BFS round costs one CTA barrier (a dual-step round two), and an epoch start
+// recomputes only the columns whose key was reset.
 //
 // Cost source (template SMEM_C): the instance's matrix staged into shared
 // memory by one TMA bulk copy (cp.async.bulk + mbarrier), or streamed from
