@@ -132,7 +132,8 @@ int kmb_solve_batch_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, i
 /* Stream-ordered variant of kmb_solve_batch_i32 for device-resident batches:
  * enqueues the solve on the context's stream and returns at once (no host
  * synchronisation, so back-to-back batches pipeline and the call can be
- * captured in a CUDA graph once a first call has sized the workspace).  All
+ * captured in a CUDA graph once a first call has sized the workspace; capture
+ * in cudaStreamCaptureModeRelaxed, since the call queries pointer attributes).  All
  * six buffers must be device memory; status[b] (batch int32) receives instance
  * b's outcome when the stream reaches it: 0 ok, KMB_ENEGATIVE, KMB_ERANGE, or
  * another nonzero code for an engine fault.  The return value reports argument
