@@ -67,16 +67,15 @@ enum kmb_option {
                                n<=3072, cluster n<=5120, grid beyond; batches
                                warp or CTA (n<=256, by residency), single-CTA
                                (n<=4096);
-                               1 grid (persistent), 2 CTA/SMEM, 6 CTA/L2,
-                               3 warp/SMEM, 4 warp/L2 (2,3,4,6: n <= 256),
+                               1 grid (persistent), 4 warp (n <= 256),
                                5 cluster (grid engine on one <=16-CTA cluster),
+                               6 CTA (n <= 256),
                                8 single-CTA (one 512-thread CTA, n <= 4096);
-                               stats->engine 7 = column-sharded              */
+                               stats->engine 7 = column-sharded, 9 = wide
+                               (int64 costs, kmb_solve_i64)                   */
   KMB_OPT_WARPS_PER_SM = 4, /* warp engine: resident instances per SM (0 = max);
                                bounds the L2 working set of streamed matrices   */
-  KMB_OPT_U16 = 5,          /* warp/L2 engine (n in 65..256): stream 16-bit
-                               offsets from the row minima, exact (rows with an
-                               offset >= 65535 fall back to int32); 0 = default */
+  /* 5 (the 16-bit warp-engine mode of ABI 1) was removed: slower */
   KMB_OPT_PIPELINE = 6      /* host-input batches (>= 256 instances): chunks the
                                H2D copy is split into so solves overlap it.
                                0 = auto (tapered: min(8, batch/128) equal

@@ -72,7 +72,8 @@ def _load_ref():
             C.c_double, _f64p, _i32p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
             C.POINTER(C.c_int64), _i32p, C.POINTER(C.c_double)]
         lib.otref_solve_many_i32.argtypes = [
-            _i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i64p, C.POINTER(C.c_double)]
+            _i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i64p, C.c_void_p, C.c_void_p,
+            C.POINTER(C.c_double)]
         _ref = lib
     return _ref
 
@@ -259,17 +260,24 @@ def ref_build_instance(a, b, scale: float) -> np.ndarray:
     return out.reshape(n, m)
 
 
-def ref_solve_many_i32(costs: np.ndarray, mode: int = 1, nthreads: int = 1):
+def ref_solve_many_i32(costs: np.ndarray, mode: int = 1, nthreads: int = 1, duals: bool = False):
     """Reference solver over a batch of int32 instances on ``nthreads`` host
     threads (mode 1 = solve_batched_km at lossless B, 0 = solve_km).
-    Returns (total_costs[int64 batch], wall_seconds)."""
+    Returns (total_costs[int64 batch], wall_seconds), or with ``duals`` also
+    u and v (int64, batch x n each)."""
     lib = _load_ref()
     c = np.ascontiguousarray(costs, dtype=np.int32)
     b, n, _ = c.shape
     tot = np.zeros(b, np.int64); wall = C.c_double()
-    rc = lib.otref_solve_many_i32(c, b, n, mode, nthreads, tot, C.byref(wall))
+    u = np.zeros((b, n), np.int64) if duals else None
+    v = np.zeros((b, n), np.int64) if duals else None
+    rc = lib.otref_solve_many_i32(c, b, n, mode, nthreads, tot,
+                                  None if u is None else u.ctypes.data,
+                                  None if v is None else v.ctypes.data, C.byref(wall))
     if rc:
         raise RefError(rc, lib.otref_last_error().decode())
+    if duals:
+        return tot, u, v, wall.value
     return tot, wall.value
 
 

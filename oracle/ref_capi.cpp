@@ -201,13 +201,16 @@ int otref_solve_auction(const int64_t* cost, int32_t n, int32_t scaled, double e
 // CPU baseline helper: `batch` independent int32 instances (n x n each),
 // solved with the reference solver (mode 0 = solve_km, 1 = solve_batched_km
 // at the lossless B = max(N,1)) on `nthreads` threads (the reference is
-// re-entrant: no mutable globals in core.cpp / hungarian.cpp).  The int32 ->
-// int64 widening happens per instance outside the timed solve call, as
-// bench.cpp:95-121 times only spec.run.  Returns the summed solve seconds
-// (per-thread sums) in *solve_seconds and the wall time in *wall_seconds.
+// re-entrant: no mutable globals in core.cpp / hungarian.cpp).  Outputs (each
+// optional): total cost per instance, and the duals u, v (batch x n each), so
+// the caller can compare every instance bit for bit.  *wall_seconds is the
+// wall time of the whole pool, and it INCLUDES each instance's int32 -> int64
+// widening into an OTInstance (a 64 KiB copy for n = 128, well under 1% of a
+// 3-4 ms solve); bench.cpp:95-121 times spec.run alone, so this rate is a
+// slight underestimate of the reference's.
 int otref_solve_many_i32(const int32_t* costs, int32_t batch, int32_t n,
                          int32_t mode, int32_t nthreads, int64_t* total_costs,
-                         double* wall_seconds) {
+                         int64_t* u_out, int64_t* v_out, double* wall_seconds) {
   return guarded([&] {
     const auto t0 = std::chrono::steady_clock::now();
     std::atomic<int32_t> next{0};
@@ -227,16 +230,20 @@ int otref_solve_many_i32(const int32_t* costs, int32_t batch, int32_t n,
         try {
           ot::OTInstance inst = make_unit(buf.data(), n);
           ot::SolveResult res;
+          ot::DualPotentials d;
           if (mode == 0) {
-            res = ot::solve_km(inst);
+            res = ot::solve_km(inst, &d);
           } else {
             ot::BatchedKMConfig cfg;
             cfg.B = mx > 0 ? mx : 1;
-            res = ot::solve_batched_km(inst, cfg);
+            res = ot::solve_batched_km(inst, cfg, &d);
           }
           int64_t t = 0;
           for (const auto& e : res.flow.entries()) t += inst.cost_at(e.i, e.j);
           if (total_costs) total_costs[b] = t;
+          const size_t o = static_cast<size_t>(b) * n;
+          if (u_out && d.u.size() == static_cast<size_t>(n)) std::memcpy(u_out + o, d.u.data(), 8 * n);
+          if (v_out && d.v.size() == static_cast<size_t>(n)) std::memcpy(v_out + o, d.v.data(), 8 * n);
         } catch (const std::exception&) {
           failed.store(1);
         }

@@ -24,7 +24,7 @@ from . import _build
 KMB_SEED_KM = 0
 KMB_SEED_BATCHED = 1
 KMB_OK, KMB_EINVAL, KMB_ENEGATIVE, KMB_ERANGE = 0, 1, 2, 3  # include/kmb.h status codes
-OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_U16, OPT_PIPELINE = 1, 2, 3, 4, 5, 6
+OPT_MAX_CTAS, OPT_CONTINUE_BFS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_PIPELINE = 1, 2, 3, 4, 6
 
 # every symbol include/kmb.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",
@@ -416,12 +416,15 @@ def solve_km(cost, supplies=None, demands=None, time_budget_s: float = 0.0,
     return r
 
 
-def solve_batched_km(cost, B: int | None = None, supplies=None, demands=None,
+def solve_batched_km(cost, B: int | None = 100, supplies=None, demands=None,
                      time_budget_s: float = 0.0, solver: Solver | None = None,
                      return_quantized: bool = False):
-    """``ot::solve_batched_km`` on chat = quantize_costs(cost, B); ``B=None`` is the
-    lossless B = N.  ``exact`` = lossless and converged (hungarian.cpp:374-376);
-    the total cost and objective are reported against the true costs."""
+    """``ot::solve_batched_km`` on chat = quantize_costs(cost, B).  The default
+    B = 100 is ``BatchedKMConfig{}``'s (hungarian.hpp:42-45), so a caller
+    relying on the default gets the reference's (possibly lossy) answer;
+    ``B=None`` (an extension) is the lossless B = N.  ``exact`` = lossless and
+    converged (hungarian.cpp:374-376); the total cost and objective are
+    reported against the true costs."""
     c = _validate(cost, supplies, demands, "solve_batched_km")
     if (c < 0).any():
         raise ValueError("solve_batched_km: costs must be nonnegative")

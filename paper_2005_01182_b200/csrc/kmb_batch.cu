@@ -9,40 +9,35 @@
 // a BFS round costs one CTA barrier (a dual-step round two), and an epoch start
 // recomputes only the columns whose key was reset.
 //
-// Cost source (template SMEM_C): the instance's matrix staged into shared
-// memory by one TMA bulk copy (cp.async.bulk + mbarrier), or streamed from
-// L2 with coalesced loads (more CTAs per SM, bounded by KMB_OPT_WARPS_PER_SM
-// so the resident matrices stay in L2).
+// Costs stream from L2 with coalesced loads, which leaves shared memory to the
+// per-instance state (more CTAs per SM; KMB_OPT_WARPS_PER_SM bounds them).  The
+// round-1 variant staging each matrix in shared memory by TMA was slower at
+// every batch size (2.6 vs 1.8 ms for 4096 instances) and was removed.
 // Keys (NARROW): 32-bit ((c - w + 2^22) << 8) | row when n <= 256 and costs
 // < 2^21, else 64-bit ((c - w + 2^30) << 32) | row (kmb_common.cuh).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <map>
+#include <mutex>
 
 #include "kmb_common.cuh"
 #include "kmb_internal.h"
 #include "kmb_launch.h"
 
-// per-stage clock64 accounting (kmb_last_instance_stats columns 5-8): a
-// diagnostic build flag, off in production (it costs a few percent)
-#ifndef KMB_CTA_RB  // rows per relax batch
-#define KMB_CTA_RB 4  // A/B (tools/ab_cta.py, 512-shard): 2: .449, 3: .399, 4: .386, 5: .415, 8: .399, 16: .473 ms
-#endif
+// Build-time constants, A/B measured in round 1 (tools/ab_cta.py, 512-shard ms):
+//   kCtaRB rows per relax batch: 2: .449, 3: .399, 4: .386, 5: .415, 8: .399
+//   kCtaGB survivor rows in flight per thread in the dirty-column recompute
+//          (512-shard / 1024-shard / c1): 1 .403/.511/.217, 2 .389/.481/.203,
+//          3 .389/.485/.204, 4 .400/.511/.212, 8 .403/.496/.208
 // Epoch start: recompute only the reset ("dirty") columns, threads split over
 // (dirty column, survivor-row group) pairs, instead of re-relaxing every
-// survivor row over all columns (~80% of the rows relaxed on config 3).  With
-// one barrier per BFS round (KMB_CTA_ONEBAR) it beats the full re-relax at
-// every n <= 256: 512-shard 0.386 -> 0.373 ms, 1024-shard 0.509 -> 0.468, c1
-// (n = 256) 0.197 -> 0.186.  Rows in flight per thread in the recompute (A/B,
-// tools/ab_cta.py, 512-shard / 1024-shard / c1 ms, two-barrier build): GB=1
-// .403 / .511 / .217, GB=2 .389 / .481 / .203, GB=3 .389 / .485 / .204, GB=4
-// .400 / .511 / .212, GB=8 .403 / .496 / .208.
-#ifndef KMB_CTA_GB  // survivor rows in flight per thread in the dirty recompute
-#define KMB_CTA_GB 2
-#endif
-#ifndef KMB_CTA_ONEBAR  // one CTA barrier per BFS round (A/B)
-#define KMB_CTA_ONEBAR 1
-#endif
+// survivor row over all columns (~80% of the rows relaxed on config 3); with
+// one barrier per BFS round it beats the full re-relax at every n <= 256:
+// 512-shard 0.386 -> 0.373 ms, 1024-shard 0.509 -> 0.468, c1 0.197 -> 0.186.
+// KMB_CTA_STAGE_CLOCKS (diagnostics): per-stage clock64 accounting
+// (kmb_last_instance_stats columns 5-8), off in production.
 #ifndef KMB_CTA_STAGE_CLOCKS
 #define KMB_CTA_STAGE_CLOCKS 0
 #endif
@@ -51,9 +46,7 @@ namespace kmb {
 
 namespace {
 
-__device__ __forceinline__ uint32_t saddr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
+constexpr int kCtaRB = 4, kCtaGB = 2;
 
 template <bool NARROW>
 struct CKeys;
@@ -93,16 +86,14 @@ __device__ __forceinline__ bool cclaimed(uint32_t c, int epoch) {
 }
 
 struct CtaShared {
-  uint64_t bar;  // mbarrier of the TMA bulk copy
+  uint64_t pad0_;
   // (pad_: with a 7-word header ptxas gave the former full-re-relax build 48
   // registers and stops keeping a relax batch's loads in flight; 62 with 8)
   int32_t nrows, nfound, ns, won, nd, pad_;
   int32_t lo_all, hi_all;
-  int32_t red[8];  // per-warp min slack' / partial sums
-#if KMB_CTA_ONEBAR
+  int32_t red[8];  // per-warp partial sums
   int32_t cnt[3], fcnt[3], cnt2[2], fcnt2[2];  // one-barrier rounds
   int32_t red3[3][8];
-#endif
 };
 
 __device__ __forceinline__ void shared_min(uint32_t* p, uint32_t x) { atomicMin(p, x); }
@@ -110,22 +101,15 @@ __device__ __forceinline__ void shared_min(uint64_t* p, uint64_t x) {
   atomicMin(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(x));
 }
 
-template <bool SMEM_C>
-__device__ __forceinline__ int32_t ldc(const int32_t* p) {
-  if constexpr (SMEM_C) return *p;
-  else return __ldg(p);
-}
+__device__ __forceinline__ int32_t ldc(const int32_t* p) { return __ldg(p); }
 
 }  // namespace
 
-// dynamic smem: [Cs n*n (SMEM_C)] | rows[2][n] (int2) | u w root_row match_row
-// match_col tree_par found (int32 x n) | claim (u32 x n) | dlist (int32 x n)
-__host__ __device__ inline size_t cta_smem_bytes(int n, bool smem_c) {
-  const size_t cs = smem_c ? ((static_cast<size_t>(n) * n * 4 + 15) & ~static_cast<size_t>(15)) : 0;
-  return cs + static_cast<size_t>(n) * (2 * 8 + 9 * 4);
-}
+// dynamic smem: rows[2][n] (int2) | u w root_row match_row match_col tree_par
+// found (int32 x n) | claim (u32 x n) | dlist (int32 x n)
+__host__ __device__ inline size_t cta_smem_bytes(int n) { return static_cast<size_t>(n) * (2 * 8 + 9 * 4); }
 
-template <bool SMEM_C, bool NARROW>
+template <bool NARROW>
 __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, int inst,
                                          CtaShared& sm, int2* rows, int2* spare, int32_t* u,
                                          int32_t* w, int32_t* root_row, int32_t* match_row,
@@ -144,10 +128,8 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
     sm.nrows = n;
     sm.nfound = 0;
     sm.nd = 0;
-#if KMB_CTA_ONEBAR
     for (int q = 0; q < 3; ++q) sm.cnt[q] = sm.fcnt[q] = 0;
     sm.cnt2[0] = sm.cnt2[1] = sm.fcnt2[0] = sm.fcnt2[1] = 0;
-#endif
   }
   K key = KO::INF;
   int32_t v = 0, dc = 0;
@@ -158,38 +140,36 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
   // they are kept in registers (one dependent shared load less per absorb)
   int32_t mi2 = -1, mu2 = 0;
   auto relax = [&](int r, int end) {
-    for (; r + KMB_CTA_RB - 1 < end; r += KMB_CTA_RB) {
-      int2 e[KMB_CTA_RB];
-      int32_t c[KMB_CTA_RB];
+    for (; r + kCtaRB - 1 < end; r += kCtaRB) {
+      int2 e[kCtaRB];
+      int32_t c[kCtaRB];
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[r + k];
+      for (int k = 0; k < kCtaRB; ++k) e[k] = rows[r + k];
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+      for (int k = 0; k < kCtaRB; ++k) c[k] = ldc(colp + e[k].x * n);
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
+      for (int k = 0; k < kCtaRB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
     }
     if (end - r == 1) {
       const int2 e = rows[r];
-      key = KO::kmin(key, KO::make(ldc<SMEM_C>(colp + e.x * n), static_cast<uint32_t>(e.y), e.x));
+      key = KO::kmin(key, KO::make(ldc(colp + e.x * n), static_cast<uint32_t>(e.y), e.x));
     } else if (r < end) {
-      // 2..KMB_CTA_RB-1 rows: one batch with the last row repeated (the fold is
+      // 2..kCtaRB-1 rows: one batch with the last row repeated (the fold is
       // idempotent), so every load is in flight at once
-      int2 e[KMB_CTA_RB];
-      int32_t c[KMB_CTA_RB];
+      int2 e[kCtaRB];
+      int32_t c[kCtaRB];
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) e[k] = rows[min(r + k, end - 1)];
+      for (int k = 0; k < kCtaRB; ++k) e[k] = rows[min(r + k, end - 1)];
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) c[k] = ldc<SMEM_C>(colp + e[k].x * n);
+      for (int k = 0; k < kCtaRB; ++k) c[k] = ldc(colp + e[k].x * n);
 #pragma unroll
-      for (int k = 0; k < KMB_CTA_RB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
+      for (int k = 0; k < kCtaRB; ++k) key = KO::kmin(key, KO::make(c[k], static_cast<uint32_t>(e[k].y), e[k].x));
     }
   };
   int nrows = n, head = 0, nfree = n;
   int32_t D = 0;
   int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
-#if KMB_CTA_ONEBAR
   int kb = 0;  // one-barrier rounds: counter slot of this round
-#endif
   int status = 0;
   long long cyc[4] = {0, 0, 0, 0};  // relax, min (incl. B1), absorb (incl. B2), epoch end
   long long tl = clock64();
@@ -228,7 +208,7 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
         const int k = item % nd, g = item / nd;
         const int col = dlist[k];
         K best = KO::INF;
-        constexpr int GB = KMB_CTA_GB;
+        constexpr int GB = kCtaGB;
         for (int r = g; r < nrows; r += groups * GB) {
           int2 e[GB];
           int32_t c[GB];
@@ -238,7 +218,7 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
             e[b] = rows[rr < nrows ? rr : nrows - 1];  // repeat: the fold is idempotent
           }
 #pragma unroll
-          for (int b = 0; b < GB; ++b) c[b] = ldc<SMEM_C>(Cm + e[b].x * n + col);
+          for (int b = 0; b < GB; ++b) c[b] = ldc(Cm + e[b].x * n + col);
 #pragma unroll
           for (int b = 0; b < GB; ++b) best = KO::kmin(best, KO::make(c[b], static_cast<uint32_t>(e[b].y), e[b].x));
         }
@@ -253,7 +233,6 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
     KMB_CSTAGE(0);
     // ---- min unreached slack' (hungarian.cpp:203-206): REDUX + one exchange ----
     const int32_t s = rch ? 0x7fffffff : KO::val(key) - v;
-#if KMB_CTA_ONEBAR
     // One barrier per BFS round: absorb speculatively at the current D and
     // publish the minimum over the columns that did not turn tight.  When
     // anything turned tight anywhere there is no dual step and the round ends
@@ -328,45 +307,6 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
     kb = kb == 2 ? 0 : kb + 1;
     KMB_CSTAGE(2);
     if (nfound == 0) continue;
-#else
-    const int32_t wm = __reduce_min_sync(FULL, s);
-    if (lane == 0) sm.red[wid] = wm;
-    __syncthreads();  // ------------------------------------------------ B1
-    int32_t m = sm.red[0];
-    for (int q = 1; q < nw; ++q) m = min(m, sm.red[q]);
-    if (m > D) {
-      if (m == 0x7fffffff) {
-        status = -2;
-        break;
-      }
-      D = m;  // dual step (hungarian.cpp:207-215), applied lazily
-      ++dual_steps;
-    }
-    KMB_CSTAGE(1);
-    // ---- absorb (hungarian.cpp:186-199) ----
-    if (!rch && s == D) {
-      rch = true;
-      dc = D;
-      const int32_t par = KO::row(key);
-      tree_par[j] = par;
-      const int32_t root = root_row[par];
-      const int32_t i2 = mi2;
-      if (i2 < 0) {
-        atomicMin(claim + root, cclaim(epochs, j));
-        found[atomicAdd(&sm.nfound, 1)] = j;
-      } else {
-        const int32_t w2 = mu2 - D;
-        w[i2] = w2;
-        root_row[i2] = root;
-        rows[atomicAdd(&sm.nrows, 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
-      }
-    }
-    __syncthreads();  // ------------------------------------------------ B2
-    nrows = sm.nrows;
-    const int nfound = sm.nfound;
-    KMB_CSTAGE(2);
-    if (nfound == 0) continue;
-#endif
 
     // ---- epoch end: augment and dissolve the trees that reached a free column.
     // Dirty-column mode: the rows appended this round are relaxed over all
@@ -442,7 +382,7 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
     a.row_to_col[static_cast<int64_t>(inst) * n + j] = mr;
     a.u[static_cast<int64_t>(inst) * n + j] = u[j];
     a.v[static_cast<int64_t>(inst) * n + j] = v;
-    if (mr >= 0) tot = ldc<SMEM_C>(Cm + j * n + mr);
+    if (mr >= 0) tot = ldc(Cm + j * n + mr);
   }
   tot64 = tot;
 #pragma unroll
@@ -467,15 +407,12 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
   return status;
 }
 
-template <bool SMEM_C>
 __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ CtaShared sm;
   const int n = a.n, T = blockDim.x;
   const int j = threadIdx.x;
-  const size_t cs = SMEM_C ? ((static_cast<size_t>(n) * n * 4 + 15) & ~static_cast<size_t>(15)) : 0;
-  int32_t* Cs = reinterpret_cast<int32_t*>(dyn);
-  int2* rows = reinterpret_cast<int2*>(dyn + cs);
+  int2* rows = reinterpret_cast<int2*>(dyn);
   int2* spare = rows + n;
   int32_t* u = reinterpret_cast<int32_t*>(spare + n);
   int32_t* w = u + n;
@@ -486,38 +423,9 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
   int32_t* found = tree_par + n;
   uint32_t* claim = reinterpret_cast<uint32_t*>(found + n);
   int32_t* dlist = reinterpret_cast<int32_t*>(claim + n);
-  const bool bulk = SMEM_C && ((static_cast<int64_t>(n) * n) & 3) == 0;
-  if (bulk && j == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&sm.bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  uint32_t parity = 0;
 
   for (int inst = blockIdx.x; inst < a.batch; inst += gridDim.x) {
-    const int32_t* Cg = a.C + static_cast<int64_t>(inst) * n * n;
-    const int32_t* Cm = SMEM_C ? Cs : Cg;
-    if constexpr (SMEM_C) {  // stage the matrix: TMA bulk copy into shared memory
-      if (bulk) {
-        if (j == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          const uint32_t total = static_cast<uint32_t>(n) * n * 4;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&sm.bar)),
-                       "r"(total)
-                       : "memory");
-          for (uint32_t off = 0; off < total; off += 32768u) {
-            const uint32_t b = total - off < 32768u ? total - off : 32768u;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-                    "r"(saddr(reinterpret_cast<unsigned char*>(Cs) + off)),
-                "l"(reinterpret_cast<const unsigned char*>(Cg) + off), "r"(b), "r"(saddr(&sm.bar))
-                : "memory");
-          }
-        }
-      } else {
-        for (int k = j; k < n * n; k += T) Cs[k] = Cg[k];
-      }
-    }
+    const int32_t* Cm = a.C + static_cast<int64_t>(inst) * n * n;
     for (int k = j; k < n; k += T) {
       match_row[k] = -1;
       match_col[k] = -1;
@@ -528,15 +436,6 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
       sm.lo_all = 0x7fffffff;
       sm.hi_all = 0;
     }
-    if (bulk) {
-      asm volatile(
-          "{\n.reg .pred p;\nW_%=:\n"
-          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-          "@!p bra W_%=;\n}\n" ::"r"(saddr(&sm.bar)),
-          "r"(parity)
-          : "memory");
-      parity ^= 1;
-    }
     __syncthreads();
     // validation (core.cpp:144-145 + device range) and row reductions
     // (hungarian.cpp:323-327): one warp per row, lanes across columns
@@ -546,7 +445,7 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
       for (int i = wid; i < n; i += nw) {
         int32_t lo = 0x7fffffff, hi = 0;
         for (int k = lane; k < n; k += 32) {
-          const int32_t x = ldc<SMEM_C>(Cm + i * n + k);
+          const int32_t x = ldc(Cm + i * n + k);
           lo = min(lo, x);
           hi = max(hi, x);
         }
@@ -572,10 +471,10 @@ __global__ void __launch_bounds__(256) k_cta_batch(BatchArgs a) {
       for (int k = j; k < n; k += T) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
       if (j == 0) a.total_cost[inst] = 0;
     } else if (hi_all < (1 << 21)) {
-      status = cta_solve<SMEM_C, true>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
+      status = cta_solve<true>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
                                        match_col, tree_par, found, claim, dlist);
     } else {
-      status = cta_solve<SMEM_C, false>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
+      status = cta_solve<false>(a, Cm, inst, sm, rows, spare, u, w, root_row, match_row,
                                        match_col, tree_par, found, claim, dlist);
     }
     if (j == 0) a.status[inst] = status;
@@ -591,7 +490,7 @@ static int cta_carveout(int n, int want) {
   static int regs_cached = 0;  // benign race: every thread computes the same value
   if (!regs_cached) {
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, k_cta_batch<false>) != cudaSuccess) {
+    if (cudaFuncGetAttributes(&fa, k_cta_batch) != cudaSuccess) {
       cudaGetLastError();
       return 100;
     }
@@ -602,7 +501,7 @@ static int cta_carveout(int n, int want) {
   int ctas = 65536 / (threads * regs);
   ctas = ctas < 1 ? 1 : (ctas > 32 ? 32 : ctas);
   if (want > 0 && want < ctas) ctas = want;
-  const size_t need = static_cast<size_t>(ctas) * (cta_smem_bytes(n, false) + 2048);
+  const size_t need = static_cast<size_t>(ctas) * (cta_smem_bytes(n) + 2048);
   const int pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024));
   return pct > 100 ? 100 : (pct < 1 ? 1 : pct);
 }
@@ -662,34 +561,51 @@ cudaError_t launch_batch_summary(const int64_t* stats, const int32_t* status, in
   return cudaGetLastError();
 }
 
-int cta_batch_capacity(int n, int sm_count) {  // instances resident at once (L2 variant)
+// Instances resident at once.  Computed from the kernel's registers and the
+// full shared-memory carveout without touching the carveout attribute (the
+// launch path alone sets it: a second writer flipped it on every auto-engine
+// call and raced between contexts), cached per (device, n).
+int cta_batch_capacity(int n, int sm_count) {
   if (n < 1 || n > 256) return 0;
-  const int threads = ((n + 31) / 32) * 32;
-  int occ = 0;
-  if (prepare_launch(reinterpret_cast<const void*>(k_cta_batch<false>), threads,
-                     cta_smem_bytes(n, false), cta_carveout(n, 0), &occ) != cudaSuccess) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
-  return occ * sm_count;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find({dev, n});
+  if (it != cache.end()) return it->second * sm_count;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, k_cta_batch) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int threads = ((n + 31) / 32) * 32;
+  const int regs = ((std::max(fa.numRegs, 1) + 7) / 8) * 8;
+  int per_sm = std::min({65536 / (threads * regs), 2048 / threads, 32});
+  const size_t per_cta = cta_smem_bytes(n) + fa.sharedSizeBytes + 1024;  // +1 KiB reserved per CTA
+  per_sm = std::min<int>(per_sm, static_cast<int>((228 * 1024) / per_cta));
+  cache[{dev, n}] = per_sm;
+  return per_sm * sm_count;
 }
 
-cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warps_per_sm,
-                         cudaStream_t st, int* grid_out) {
+cudaError_t launch_batch(const BatchArgs& a, int sm_count, int warps_per_sm, cudaStream_t st,
+                         int* grid_out) {
   if (a.n < 1 || a.n > 256) return cudaErrorInvalidValue;
   const int threads = ((a.n + 31) / 32) * 32;
-  if (smem_c && cta_smem_bytes(a.n, true) > 200 * 1024) smem_c = false;
-  const size_t smem = cta_smem_bytes(a.n, smem_c);
-  auto kern = smem_c ? k_cta_batch<true> : k_cta_batch<false>;
-  // L2 variant: leave the unified cache to L1 beyond the resident CTAs' state
-  // (0.442 -> 0.413 ms at 512)
+  const size_t smem = cta_smem_bytes(a.n);
+  auto kern = k_cta_batch;
+  // leave the unified cache to L1 beyond the resident CTAs' state (0.442 ->
+  // 0.413 ms at 512)
   int occ = 0;
   // CTAs per SM this batch needs; the chunks of one pipelined call share the
   // largest chunk's value, so the carveout attribute does not flip per chunk
   const int sized = a.carve_batch > a.batch ? a.carve_batch : a.batch;
   const int want = (sized + sm_count - 1) / sm_count;
   cudaError_t e = prepare_launch(reinterpret_cast<const void*>(kern), threads, smem,
-                                 smem_c ? -1 : cta_carveout(a.n, want), &occ);
+                                 cta_carveout(a.n, want), &occ);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int wpc = threads / 32;

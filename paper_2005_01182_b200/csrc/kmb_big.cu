@@ -150,8 +150,13 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
     }
     __syncthreads();
     const int status0 = sm.lo_all < 0 ? 2 : (sm.hi_all >= (1 << 29) ? 3 : 0);
-    if (status0) {
-      if (t == 0) a.status[inst] = status0;
+    if (status0) {  // invalid instance: no stale totals or stats for async callers
+      if (t == 0) {
+        a.status[inst] = status0;
+        a.total_cost[inst] = 0;
+        if (a.converged) a.converged[inst] = 0;
+      }
+      if (a.stats && t < KMB_ISTATS) a.stats[KMB_ISTATS * static_cast<int64_t>(inst) + t] = 0;
       for (int k = t; k < n; k += kT) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
       __syncthreads();
       continue;

@@ -75,15 +75,15 @@ struct kmb_context {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t max_ctas = 0;
   int64_t warps_per_sm = 0;  // warp engine residency bound (0 = occupancy limit)
-  int64_t u16 = 0;           // warp/L2 engine: 16-bit row-offset packing (opt-in)
   int64_t pipeline = 0;      // host-input batches: chunk schedule (0 = tapered auto)
   int continue_bfs = 0;
   int engine = 0;
+  int64_t last_batch = 0;  // instances of the last batch solve (kmb_last_instance_stats)
   // grid-engine workspace
   DevBuf cost, u, v, mrow, mcol, tpar, root, claim, lrow0, lrow1, lw0, lw1, found, partial,
       ctrl, obj;
   // batch workspace
-  DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus, b16, brmin, bimin, bimax;
+  DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus;
   // cost construction workspace (host-resident points / output)
   DevBuf pa, pb, pout, pbad;
   // auction workspace
@@ -142,7 +142,7 @@ void kmb_destroy(kmb_context* c) {
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
-                    &c->obj, &c->bcost, &c->bpad, &c->b16, &c->brmin, &c->bimin, &c->bimax, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
+                    &c->obj, &c->bcost, &c->bpad, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
                     &c->bstatus, &c->pa, &c->pb, &c->pout, &c->pbad, &c->aprice, &c->ar2c, &c->atot,
                     &c->abids, &c->acomp, &c->aeps, &c->amin, &c->amax, &c->bsum})
     b->release();
@@ -171,15 +171,14 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
     case KMB_OPT_MAX_CTAS: c->max_ctas = value; return KMB_OK;
     case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_WARPS_PER_SM: c->warps_per_sm = value; return KMB_OK;
-    case KMB_OPT_U16: c->u16 = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_PIPELINE:
       if (value < -(kmb_context::kMaxChunks / 2) || value > kmb_context::kMaxChunks)
         return fail(KMB_EINVAL, "kmb_set_option: pipeline chunk count out of range");
       c->pipeline = value;
       return KMB_OK;
     case KMB_OPT_ENGINE:
-      if (value < 0 || value > 8 || value == 7)
-        return fail(KMB_EINVAL, "kmb_set_option: engine must be 0..6 or 8");
+      if (value < 0 || value > 8 || value == 2 || value == 3 || value == 7)
+        return fail(KMB_EINVAL, "kmb_set_option: engine must be 0, 1, 4, 5, 6 or 8");
       c->engine = static_cast<int>(value);
       return KMB_OK;
     default: return fail(KMB_EINVAL, "kmb_set_option: unknown option");
@@ -227,8 +226,12 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // as its H2D copy lands and its results leaving as soon as it ends, so the
   // PCIe transfers overlap the solves (the transfer bounds the end-to-end rate).
   const bool host_in = !is_device_ptr(costs);
-  const bool warp_eng = engine == 3 || engine == 4;
+  const bool warp_eng = engine == 4;
   const bool pipelined = host_in && batch >= 256 && (!warp_eng || np == n);
+  // the warp engine's 128-bit row loads need rows padded to the warp width and
+  // a 16-byte aligned base: a caller's device buffer that is neither is copied
+  // into the aligned, padded workspace (a misaligned vector load would fault)
+  const bool repack = np != n || (!host_in && (reinterpret_cast<uintptr_t>(costs) & 15) != 0);
   // chunk schedule [lo, lo + cnt): K equal chunks, and (tapered) the last one
   // split by halving down to KMB_TAPER_MIN instances, so the solve left after the final
   // copy lands is a short one
@@ -268,18 +271,10 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   if (!is_device_ptr(v)) { KMB_CUDA(c->bv.ensure(nb * 8)); dv = c->bv.as<int64_t>(); }
   if (!is_device_ptr(total_cost)) { KMB_CUDA(c->btot.ensure(batch * 8)); dtot = c->btot.as<int64_t>(); }
   KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8));
+  c->last_batch = batch;
   KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
   // stream-ordered calls write the statuses straight into the caller's buffer
   int32_t* const status_base = async_status ? async_status : c->bstatus.as<int32_t>();
-  // U16 mode (warp/L2 engine, 4 or 8 columns per lane): a packing pass writes
-  // 16-bit offsets from the row minima, halving the bytes every relax streams
-  const bool u16 = engine == 4 && c->u16 && (np == 128 || np == 256);
-  if (u16) {
-    KMB_CUDA(c->b16.ensure(nb * np * 2));
-    KMB_CUDA(c->brmin.ensure(nb * 4));
-    KMB_CUDA(c->bimin.ensure(static_cast<size_t>(batch) * 4));
-    KMB_CUDA(c->bimax.ensure(static_cast<size_t>(batch) * 4));
-  }
   const int32_t* src = dcost;  // warp engines: rows padded to the warp width
   int grid = 0;
   // the chunks of a pipelined call size their carveout for the largest chunk
@@ -305,7 +300,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       a.carve_batch = carve_batch;
       return kmb::launch_big(a, c->sm_count, s);
     }
-    if (eng == 2 || eng == 6) {
+    if (eng == 6) {
       kmb::BatchArgs a{};
       a.C = dcost + ro * n;
       a.batch = cnt;
@@ -319,7 +314,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
       a.status = status_base + lo;
       a.carve_batch = carve_batch;
-      return kmb::launch_batch(a, c->sm_count, eng == 2, static_cast<int>(c->warps_per_sm), s, &grid);
+      return kmb::launch_batch(a, c->sm_count, static_cast<int>(c->warps_per_sm), s, &grid);
     }
     kmb::WarpArgs a{};
     a.C = src + ro * np;
@@ -334,17 +329,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.total_cost = dtot + lo;
     a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
     a.status = status_base + lo;
-    if (u16) {
-      a.C16 = c->b16.as<uint16_t>() + ro * np;
-      a.rmin = c->brmin.as<int32_t>() + ro;
-      a.imin = c->bimin.as<int32_t>() + lo;
-      a.imax = c->bimax.as<int32_t>() + lo;
-      cudaError_t e = kmb::launch_pack16(a, c->sm_count, const_cast<uint16_t*>(a.C16),
-                                         const_cast<int32_t*>(a.rmin), const_cast<int32_t*>(a.imin),
-                                         const_cast<int32_t*>(a.imax), s);
-      if (e != cudaSuccess) return e;
-    }
-    return kmb::launch_warp_batch(a, c->sm_count, eng == 3, static_cast<int>(c->warps_per_sm), s, &grid);
+    return kmb::launch_warp_batch(a, c->sm_count, static_cast<int>(c->warps_per_sm), s, &grid);
   };
   // results of instances [lo, lo + cnt) to the caller's host buffers
   auto results_out = [&](int lo, int cnt, cudaStream_t s) -> cudaError_t {
@@ -360,7 +345,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   };
   int used = engine;
   if (async_status) {  // stream-ordered: enqueue and return (device buffers only)
-    if (warp_eng && np != n) {
+    if (warp_eng && repack) {
       KMB_CUDA(c->bpad.ensure(nb * np * 4));
       KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4, nb, cudaMemcpyDeviceToDevice, st));
       src = c->bpad.as<int32_t>();
@@ -371,7 +356,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   KMB_CUDA(cudaEventRecord(c->ev0, st));
   if (!pipelined) {
     if (host_in) KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
-    if (warp_eng && np != n) {  // rows padded to the warp width (in-bounds 128-bit loads): pad once
+    if (warp_eng && repack) {  // rows padded to the warp width (in-bounds 128-bit loads): pad once
       KMB_CUDA(c->bpad.ensure(nb * np * 4));
       KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4, nb, cudaMemcpyDeviceToDevice, st));
       src = c->bpad.as<int32_t>();
@@ -638,10 +623,10 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   // 269 vs 298 geometric)
   if (engine == 0)
     engine = (n <= 256 && time_budget_s <= 0.0) ? 6 : n <= 3072 ? 8 : (n <= 5120 ? 5 : 1);
-  if ((engine == 2 || engine == 6) && n > kmb::batch_max_n()) engine = 1;
-  if ((engine == 3 || engine == 4) && n > kmb::warp_max_n()) engine = 1;
+  if (engine == 6 && n > kmb::batch_max_n()) engine = 1;
+  if (engine == 4 && n > kmb::warp_max_n()) engine = 1;
   if (engine == 8 && n > kmb::big_max_n()) engine = 1;
-  if ((engine >= 2 && engine <= 4) || engine == 6 || engine == 8) {
+  if (engine == 4 || engine == 6 || engine == 8) {
     if (time_budget_s > 0.0 && engine != 8)
       return fail(KMB_EINVAL, "kmb_solve_i32: the per-instance engines have no time budget; use engine 1");
     const int32_t* src = cost;
@@ -701,10 +686,15 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
 int kmb_last_instance_stats(kmb_context* c, int64_t* out, int64_t capacity, int64_t* count) {
   if (!c || !out || !count) return fail(KMB_EINVAL, "kmb_last_instance_stats: bad arguments");
   KMB_CUDA(cudaSetDevice(c->device));
-  const int64_t have = static_cast<int64_t>(c->bstat.bytes / 8);
+  // the last batch's instances only, read in order with the context's stream
+  // (a non-blocking stream is not ordered with the legacy default stream)
+  const int64_t have = c->last_batch * kmb::KMB_ISTATS;
   const int64_t k = capacity < have ? capacity : have;
-  *count = have / kmb::KMB_ISTATS;
-  if (k > 0) KMB_CUDA(cudaMemcpy(out, c->bstat.p, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost));
+  *count = c->last_batch;
+  if (k > 0) {
+    KMB_CUDA(cudaMemcpyAsync(out, c->bstat.p, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost, c->stream));
+    KMB_CUDA(cudaStreamSynchronize(c->stream));
+  }
   return KMB_OK;
 }
 

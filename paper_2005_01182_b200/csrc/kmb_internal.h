@@ -72,7 +72,7 @@ size_t solver_smem_bytes(int W);
 cudaError_t launch_scan_all(const SolverArgs& a, int G, uint64_t* keys_out, cudaStream_t st);
 int solver_threads();
 
-// ---- batched small instances (one CTA per instance, cost matrix in SMEM) ----
+// ---- batched small instances (one CTA per instance, costs from L2) ----
 struct BatchArgs {
   const int32_t* C;      // batch x n x n (contiguous instances)
   int32_t batch;
@@ -89,8 +89,8 @@ struct BatchArgs {
 };
 
 int batch_max_n();
-cudaError_t launch_batch(const BatchArgs& a, int sm_count, bool smem_c, int warps_per_sm,
-                         cudaStream_t st, int* grid_out);
+cudaError_t launch_batch(const BatchArgs& a, int sm_count, int warps_per_sm, cudaStream_t st,
+                         int* grid_out);
 
 }  // namespace kmb
 
@@ -109,23 +109,15 @@ struct WarpArgs {
   int64_t* total_cost;   // batch
   int64_t* stats;        // batch x KMB_ISTATS (may be null)
   int32_t* status;       // batch
-  // U16 mode (optional, from launch_pack16): 16-bit offsets from the row
-  // minimum, row minima with the "wide" flag in bit 31, per-instance min/max
-  const uint16_t* C16;
-  const int32_t* rmin;
-  const int32_t* imin;
-  const int32_t* imax;
 };
 int warp_max_n();
 int cta_batch_capacity(int n, int sm_count);  // CTA/L2 engine: instances resident at once
 // folds per-instance stats + status into 11 int64 (kmb_batch.cu)
 cudaError_t launch_batch_summary(const int64_t* stats, const int32_t* status, int32_t batch,
                                  int64_t* out, cudaStream_t st);
-cudaError_t launch_pack16(const WarpArgs& a, int sm_count, uint16_t* C16, int32_t* rmin,
-                          int32_t* imin, int32_t* imax, cudaStream_t st);
 int warp_pitch(int n);  // padded row pitch the warp engine requires (32 * columns per lane)
-cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, bool smem_c, int warps_per_sm,
-                              cudaStream_t st, int* grid_out);
+cudaError_t launch_warp_batch(const WarpArgs& a, int sm_count, int warps_per_sm, cudaStream_t st,
+                              int* grid_out);
 // single-CTA engine for 256 < n <= 4096 (kmb_big.cu)
 struct BigArgs {
   const int32_t* C;     // batch instances, row stride ld, instance stride inst_stride

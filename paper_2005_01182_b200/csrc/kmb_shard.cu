@@ -426,22 +426,29 @@ int kmb_solve_sharded_i32(kmb_context* c, const int32_t* slab, int32_t n, int64_
   if (!c) return sfail(KMB_EINVAL, "kmb_solve_sharded_i32: NULL context");
   auto& exp = kmb::context_exchange(c);
   if (!exp) return sfail(KMB_EINVAL, "kmb_solve_sharded_i32: call kmb_shard_init_* first");
+  // A local failure before the protocol starts is still voted on in its first
+  // collective (kmb_shard_proto.h), so the peer ranks return an error instead
+  // of waiting forever in their next allreduce.
   if (n <= 0 || ncols < 0 || ld < ncols || !slab || col_begin < 0 || col_begin + ncols > n ||
-      (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED))
+      (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED)) {
+    int64_t vote = kmb::kShardPeerFail;
+    exp->allreduce_min(&vote, 1);
     return sfail(KMB_EINVAL, "kmb_solve_sharded_i32: bad arguments");
+  }
   cudaSetDevice(kmb::context_device(c));
   CudaSlabOps ops(kmb::context_stream(c), n, ncols);
   ops.col_begin_ = col_begin;
-  if (!ops.ok()) return sfail(KMB_ECUDA, std::string(who) + ": out of device memory");
+  std::string pre;
+  if (!ops.ok()) pre = std::string(who) + ": out of device memory";
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, ops.st);
-  if (ops.load(slab, ld) != 0) return sfail(KMB_ECUDA, std::string(who) + ": " + ops.err);
+  if (pre.empty() && ops.load(slab, ld) != 0) pre = std::string(who) + ": " + ops.err;
   kmb::ShardResult res;
   std::string err;
   const int rc = kmb::sharded_solve(ops, *exp, n, col_begin, ncols, seed, row_to_col, u_out, v_slab,
-                                    &res, &err);
+                                    &res, &err, pre);
   cudaEventRecord(e1, ops.st);
   cudaStreamSynchronize(ops.st);
   float ms = 0.f;

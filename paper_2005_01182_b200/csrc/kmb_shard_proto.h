@@ -43,14 +43,29 @@ struct ShardResult {
 
 constexpr int64_t kShardInf = 0x7FFFFFFFFFFFFFFFLL;
 
-// Returns 0, a positive kmb_status (invalid input), or -1 (ops / exchange
-// failure, message in *err), -2 (engine invariant).
+// Every rank must reach the same collectives, so a rank-local failure never
+// returns on its own: it is remembered (lfail) and voted on at the next
+// collective, which carries a failure flag (the min-slack allreduce a second
+// word, the count allgathers a negative count), and then every rank returns
+// -1 together.  A failure before the protocol starts (bad arguments, out of
+// memory, slab load) enters as `pre_fail` and is voted on in the first
+// collective.  Only a failing collective itself returns at once.
+//
+// Returns 0, a positive kmb_status (invalid input), -1 (ops / exchange
+// failure on this or another rank, message in *err), -2 (engine invariant).
+constexpr int64_t kShardPeerFail = -100;  // vote value of a rank-local failure
+
 template <class Ops>
 int sharded_solve(Ops& ops, ShardExchange& ex, int32_t n, int32_t col_begin, int32_t ncols,
                   int32_t seed, int32_t* row_to_col, int64_t* u_out, int64_t* v_slab,
-                  ShardResult* res, std::string* err) {
+                  ShardResult* res, std::string* err, const std::string& pre_fail = "") {
   const int NR = ex.nranks;
-  const size_t nn = static_cast<size_t>(n), nc = static_cast<size_t>(ncols);
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 0), nc = static_cast<size_t>(ncols > 0 ? ncols : 0);
+  std::string lfail = pre_fail;
+  auto failed_everywhere = [&]() {
+    *err = lfail.empty() ? std::string("another rank failed") : lfail;
+    return -1;
+  };
 #define KMB_OK_OR(x, what)          \
   do {                              \
     if ((x) != 0) {                 \
@@ -58,14 +73,20 @@ int sharded_solve(Ops& ops, ShardExchange& ex, int32_t n, int32_t col_begin, int
       return -1;                    \
     }                               \
   } while (0)
+#define KMB_TRY(x, what)                                                        \
+  do {                                                                          \
+    if ((x) != 0 && lfail.empty())                                              \
+      lfail = std::string(what) + (ops.err.empty() ? "" : ": " + ops.err);      \
+  } while (0)
   std::vector<int64_t> u(nn, 0), w(nn, 0), rowmin(nn, kShardInf);
   std::vector<int32_t> root(nn), match_row(nn, -1), match_col(nc, -1), tree_par(nc, -1);
   std::vector<int32_t> rows;
   int32_t status = 0;
-  KMB_OK_OR(ops.rowmin(rowmin.data(), &status), "slab row minima");
-  {  // validation is global: any rank's bad entry fails every rank
-    int64_t bad = -static_cast<int64_t>(status);
+  if (lfail.empty()) KMB_TRY(ops.rowmin(rowmin.data(), &status), "slab row minima");
+  {  // validation is global: any rank's bad entry (or local failure) fails every rank
+    int64_t bad = lfail.empty() ? -static_cast<int64_t>(status) : kShardPeerFail;
     KMB_OK_OR(ex.allreduce_min(&bad, 1), "exchange (validation)");
+    if (bad == kShardPeerFail) return failed_everywhere();
     if (bad < 0) return static_cast<int>(-bad);
   }
   KMB_OK_OR(ex.allreduce_min(rowmin.data(), n), "exchange (row minima)");  // :323-327
@@ -89,12 +110,15 @@ int sharded_solve(Ops& ops, ShardExchange& ex, int32_t n, int32_t col_begin, int
     const int32_t cnt = static_cast<int32_t>(rows.size() - head);
     ws.resize(cnt);
     for (int32_t r = 0; r < cnt; ++r) ws[r] = w[rows[head + r]];
-    int64_t m = kShardInf;
-    KMB_OK_OR(ops.relax(rows.data() + head, ws.data(), cnt, first && seed == 1, &m), "slab relax");
+    int64_t mv[2] = {kShardInf, 0};  // min slack', failure flag
+    KMB_TRY(ops.relax(rows.data() + head, ws.data(), cnt, first && seed == 1, &mv[0]), "slab relax");
     first = false;
     res->rows_scanned += cnt;
     head = rows.size();
-    KMB_OK_OR(ex.allreduce_min(&m, 1), "exchange (min slack)");  // :203-206
+    if (!lfail.empty()) mv[1] = -1;
+    KMB_OK_OR(ex.allreduce_min(mv, 2), "exchange (min slack)");  // :203-206
+    if (mv[1] < 0) return failed_everywhere();
+    const int64_t m = mv[0];
     if (m > D) {
       if (m == kShardInf) {
         *err = "no unreached column";
@@ -105,7 +129,8 @@ int sharded_solve(Ops& ops, ShardExchange& ex, int32_t n, int32_t col_begin, int
     }
     // ---- absorb tight slab columns, entries for the replicated row side ----
     int32_t na = 0;
-    KMB_OK_OR(ops.absorb(D, cols.data(), pars.data(), &na), "slab absorb");
+    KMB_TRY(ops.absorb(D, cols.data(), pars.data(), &na), "slab absorb");
+    if (!lfail.empty()) na = 0;
     order.resize(na);
     for (int32_t k = 0; k < na; ++k) order[k] = k;
     std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cols[a] < cols[b]; });
@@ -118,10 +143,13 @@ int sharded_solve(Ops& ops, ShardExchange& ex, int32_t n, int32_t col_begin, int
       if (i2 < 0) out.insert(out.end(), {1, col_begin + j, rt, 0});  // free column
       else out.insert(out.end(), {0, i2, u[i2] - D, rt});             // new row
     }
-    int64_t mine = static_cast<int64_t>(out.size() / 4);
+    int64_t mine = lfail.empty() ? static_cast<int64_t>(out.size() / 4) : -1;
     KMB_OK_OR(ex.allgather(&mine, 8, counts.data()), "exchange (entry counts)");
     int64_t maxc = 0;
-    for (int64_t x : counts) maxc = std::max(maxc, x);
+    for (int64_t x : counts) {
+      if (x < 0) return failed_everywhere();
+      maxc = std::max(maxc, x);
+    }
     if (maxc == 0) continue;
     out.resize(static_cast<size_t>(maxc) * 4, 0);
     gathered.assign(static_cast<size_t>(maxc) * 4 * NR, 0);
@@ -151,14 +179,17 @@ int sharded_solve(Ops& ops, ShardExchange& ex, int32_t n, int32_t col_begin, int
     const int64_t ep = res->epochs;
     auto claimed = [&](int32_t rt) { return claim_ep[rt] == ep; };
     std::vector<uint8_t> rch(nc, 0);
-    KMB_OK_OR(ops.reached(rch.data()), "slab reached");
+    KMB_TRY(ops.reached(rch.data()), "slab reached");
     std::vector<int64_t> tout;  // (global col, parent) of claimed trees' columns
-    for (int32_t j = 0; j < ncols; ++j)
+    for (int32_t j = 0; lfail.empty() && j < ncols; ++j)
       if (rch[j] && claimed(root[tree_par[j]])) tout.insert(tout.end(), {col_begin + j, tree_par[j]});
-    int64_t tc = static_cast<int64_t>(tout.size() / 2);
+    int64_t tc = lfail.empty() ? static_cast<int64_t>(tout.size() / 2) : -1;
     KMB_OK_OR(ex.allgather(&tc, 8, counts.data()), "exchange (tree counts)");
     int64_t tmax = 0;
-    for (int64_t x : counts) tmax = std::max(tmax, x);
+    for (int64_t x : counts) {
+      if (x < 0) return failed_everywhere();
+      tmax = std::max(tmax, x);
+    }
     tout.resize(static_cast<size_t>(tmax) * 2, 0);
     std::vector<int64_t> tall(static_cast<size_t>(tmax) * 2 * NR);
     if (tmax) KMB_OK_OR(ex.allgather(tout.data(), tmax * 16, tall.data()), "exchange (trees)");
@@ -170,7 +201,7 @@ int sharded_solve(Ops& ops, ShardExchange& ex, int32_t n, int32_t col_begin, int
       }
     std::vector<uint8_t> cl(nn, 0);
     for (int32_t i = 0; i < n; ++i) cl[i] = claimed(i) ? 1 : 0;
-    KMB_OK_OR(ops.dissolve(root.data(), cl.data(), D), "slab dissolve");
+    KMB_TRY(ops.dissolve(root.data(), cl.data(), D), "slab dissolve");  // voted next round
     std::vector<int32_t> surv;
     for (int32_t i : rows) {
       if (claimed(root[i])) u[i] = w[i] + D;
@@ -193,16 +224,21 @@ int sharded_solve(Ops& ops, ShardExchange& ex, int32_t n, int32_t col_begin, int
     head = 0;
     ++res->epochs;
   }
-  KMB_OK_OR(ops.finish(D, v_slab), "slab finish");
-  int64_t part = 0;
-  KMB_OK_OR(ops.cost(match_row.data(), &part), "slab cost");
-  std::vector<int64_t> parts(NR);
-  KMB_OK_OR(ex.allgather(&part, 8, parts.data()), "exchange (cost)");
+  KMB_TRY(ops.finish(D, v_slab), "slab finish");
+  int64_t part[2] = {0, 0};  // partial cost, failure flag
+  if (lfail.empty()) KMB_TRY(ops.cost(match_row.data(), &part[0]), "slab cost");
+  if (!lfail.empty()) part[1] = -1;
+  std::vector<int64_t> parts(2 * NR);
+  KMB_OK_OR(ex.allgather(part, 16, parts.data()), "exchange (cost)");
   res->total_cost = 0;
-  for (int64_t x : parts) res->total_cost += x;
+  for (int r = 0; r < NR; ++r) {
+    if (parts[2 * r + 1] < 0) return failed_everywhere();
+    res->total_cost += parts[2 * r];
+  }
   if (row_to_col) std::copy(match_row.begin(), match_row.end(), row_to_col);
   if (u_out) std::copy(u.begin(), u.end(), u_out);
 #undef KMB_OK_OR
+#undef KMB_TRY
   return 0;
 }
 

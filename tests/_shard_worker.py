@@ -47,6 +47,24 @@ def run(rank, world, port, mode, outdir):
                                         C.c_void_p(u.ctypes.data), C.c_void_p(v.ctypes.data),
                                         C.c_void_p(out.ctypes.data))
                 results.append((rc, r2c, u, v[:nc], int(out[0]), int(out[1]), cb))
+    elif mode.startswith("fail"):  # "fail:<op>:<at>": rank 1 fails, every rank must return -1
+        _, op, at = mode.split(":")
+        lib = C.CDLL(os.path.join(ROOT, "tests", "cpp", "build", "libshardsim.so"))
+        ex = GroupExchange()
+        c = make_cases()[-1]  # config 1, n = 256
+        n = c.shape[0]
+        cb, nc = column_span(n, world, rank)
+        slab = np.ascontiguousarray(c[:, cb:cb + nc])
+        r2c = np.full(n, -1, np.int32)
+        u = np.zeros(n, np.int64)
+        v = np.zeros(max(nc, 1), np.int64)
+        out = np.zeros(4, np.int64)
+        rc = lib.shardsim_solve_fail(
+            C.c_void_p(slab.ctypes.data), C.c_int32(n), C.c_int64(max(nc, 1)), C.c_int32(cb),
+            C.c_int32(nc), C.c_int32(1), C.c_int32(world), C.c_int32(rank), ex.ar, ex.ag,
+            C.c_void_p(r2c.ctypes.data), C.c_void_p(u.ctypes.data), C.c_void_p(v.ctypes.data),
+            C.c_void_p(out.ctypes.data), C.c_int32(int(op) if rank == 1 else 0), C.c_int32(int(at)))
+        results.append(rc)
     else:  # "gpu"/"nccl": the CUDA slab kernels; exchange through this gloo group
         # (ranks share cuda:0) or through NCCL (one rank per GPU)
         from paper_2005_01182_b200 import Solver

@@ -141,7 +141,7 @@ def test_gpu_circle_square_acceptance(solver, k, objective):
     sq, ci = circle_square_points(k)
     c = solver.costs_from_points(sq, ci, 1e4)
     np.testing.assert_array_equal(c, circle_square(k))
-    r = solve_batched_km(c, solver=solver)
+    r = solve_batched_km(c, None, solver=solver)  # lossless
     assert r.total_cost == objective
     ref = O.ref_solve_batched_km(c)
     np.testing.assert_array_equal(r.u, ref.u)

@@ -87,7 +87,7 @@ def check_against(res, ref, c, dual_steps=None):
 def test_known_2x2(solver):  # test_hungarian.cpp:72-85
     c = np.array([[1, 3], [2, 1]], np.int32)
     for seed in (KMB_SEED_KM, KMB_SEED_BATCHED):
-        for engine in (1, 2, 3, 4, 5, 6):
+        for engine in (1, 4, 5, 6):
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, seed)
             assert r.total_cost == 2
@@ -108,7 +108,7 @@ def test_known_constant(solver):  # :133-142: constant 6x6 cost 4 -> 24, one pha
     assert r.stats["dual_steps"] == 0
 
 
-@pytest.mark.parametrize("engine", [1, 2, 3, 4, 5, 6, 8])
+@pytest.mark.parametrize("engine", [1, 4, 5, 6, 8])
 @pytest.mark.parametrize("seed", [KMB_SEED_KM, KMB_SEED_BATCHED])
 def test_random_small_vs_reference(solver, engine, seed):
     rng = np.random.default_rng(100 + 10 * engine + seed)
@@ -177,7 +177,7 @@ def test_matching_equals_mirror(solver):
         n = int(rng.integers(2, 300))
         c = rng.integers(0, 20, size=(n, n)).astype(np.int32)
         mi = O.mirror_solve_incr(c, 1)
-        engines = [1, 5, 8] + ([2, 3, 4, 6] if n <= 256 else [])
+        engines = [1, 5, 8] + ([4, 6] if n <= 256 else [])
         for engine in engines:
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, KMB_SEED_BATCHED)
@@ -192,7 +192,7 @@ def test_matching_equals_mirror(solver):
 def test_negative_cost_rejected(solver):
     c = np.ones((5, 5), np.int32)
     c[2, 3] = -1
-    for engine in (1, 2, 3, 4, 5, 6):
+    for engine in (1, 4, 5, 6):
         solver.set_option(OPT_ENGINE, engine)
         with pytest.raises(KmbError, match="costs must be nonnegative"):
             solver.solve(c, KMB_SEED_BATCHED)
@@ -202,7 +202,7 @@ def test_negative_cost_rejected(solver):
 def test_out_of_device_range_rejected(solver):
     c = np.ones((5, 5), np.int32)
     c[0, 0] = 2**29
-    for engine in (1, 2, 3, 4, 5, 6):
+    for engine in (1, 4, 5, 6):
         solver.set_option(OPT_ENGINE, engine)
         with pytest.raises(KmbError, match="device range"):
             solver.solve(c, KMB_SEED_BATCHED)
@@ -247,7 +247,7 @@ def test_config2(solver):
     check_against(r, ref, c)
 
 
-@pytest.mark.parametrize("engine", [2, 3, 4, 6])
+@pytest.mark.parametrize("engine", [4, 6])
 def test_config3_subset(solver, engine):
     c = W.CONFIGS["c3"].make(batch=64)
     solver.set_option(OPT_ENGINE, engine)
@@ -284,15 +284,57 @@ def test_config3_golden(solver):
     assert np.array_equal(r.u.sum(1) + r.v.sum(1), r.total_cost)
 
 
-@pytest.mark.parametrize("key", ["c4", "c5"])
-def test_large_config_golden(solver, key):
+@pytest.mark.parametrize("engine", [0, 6])
+def test_config3_all_instances_vs_reference(solver, engine):
+    """The headline workload in full: all 4096 config-3 instances, total cost,
+    u and v bit-exact against the unmodified reference run on this host's
+    cores (oracle/_ref, solve_batched_km at lossless B) and against the
+    committed golden hashes of that run (tests/golden/c3_all); exact
+    certificates on every instance; the assignment equal to the reference's
+    wherever the optimum is unique (checked on every 8th instance).
+    engine 0 = auto (the warp engine at 4096 instances), 6 = the CTA engine."""
+    g = _golden()["c3_all"]
+    c = W.CONFIGS["c3"].make()
+    assert W.fnv1a64(c) == g["cost_fnv"]
+    solver.set_option(OPT_ENGINE, engine)
+    try:
+        r = solver.solve_batch(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_ENGINE, 0)
+    tot, u, v, _ = O.ref_solve_many_i32(c, mode=1, nthreads=os.cpu_count() or 1, duals=True)
+    bad = np.nonzero((r.total_cost != tot) | (r.u != u).any(1) | (r.v != v).any(1))[0]
+    assert bad.size == 0, f"{bad.size} instances differ, first {bad[:8].tolist()}"
+    assert W.fnv1a64(r.total_cost) == g["total_fnv"]
+    assert W.fnv1a64(r.u) == g["u_fnv"] and W.fnv1a64(r.v) == g["v_fnv"]
+    cc = c.astype(np.int64)
+    assert ((cc - r.u[:, :, None] - r.v[:, None, :]) >= 0).all()
+    rows = np.arange(c.shape[1])
+    for t in range(c.shape[0]):
+        assert sorted(r.row_to_col[t].tolist()) == rows.tolist()
+        assert (cc[t, rows, r.row_to_col[t]] == r.u[t] + r.v[t, r.row_to_col[t]]).all()
+    for t in range(0, c.shape[0], 8):
+        if optimum_unique(c[t], r.u[t], r.v[t], r.row_to_col[t]):
+            np.testing.assert_array_equal(r.row_to_col[t], O.ref_solve_batched_km(c[t]).row_to_col)
+
+
+@pytest.mark.parametrize("key,engine", [("c4", 0), ("c4", 1), ("c4", 5), ("c4", 8),
+                                        ("c5", 0), ("c5", 5)])
+def test_large_config_golden(solver, key, engine):
+    """Configs 4 and 5 on every engine that accepts them (0 = auto: cluster for
+    c4, grid for c5): cost, u, v equal to the golden (c4: the unmodified
+    reference; c5: the seeded e-maxx restatement, pinned to the reference on
+    c1/c2/c4 by tests/test_oracle.py)."""
     g = _golden()
     if key not in g:
         pytest.skip(f"no golden for {key}")
     g = g[key]
     c = W.CONFIGS[key].make()
     assert W.fnv1a64(c) == g["cost_fnv"]
-    r = solver.solve(c, KMB_SEED_BATCHED)
+    solver.set_option(OPT_ENGINE, engine)
+    try:
+        r = solver.solve(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_ENGINE, 0)
     assert r.total_cost == g["total_cost"]
     assert W.fnv1a64(r.u) == g["u_fnv"]
     assert W.fnv1a64(r.v) == g["v_fnv"]
@@ -336,6 +378,21 @@ def test_api_batched_km_quantization_matches_reference():
                 assert r.objective == ref.objective
 
 
+def test_api_batched_km_default_b_is_the_references():
+    """BatchedKMConfig{} has B = 100 (hungarian.hpp:42-45): the mirror's default
+    call quantizes the same way and returns the reference's duals."""
+    from paper_2005_01182_b200 import solve_batched_km
+    rng = np.random.default_rng(23)
+    for t in range(10):
+        n = int(rng.integers(2, 40))
+        c = rng.integers(0, int(rng.choice([50, 5000])), size=(n, n))
+        ref = O.ref_solve_batched_km(c, B=100)
+        r = solve_batched_km(c)
+        assert r.exact == ref.exact
+        np.testing.assert_array_equal(r.u, ref.u)
+        np.testing.assert_array_equal(r.v, ref.v)
+
+
 def test_api_solve_km_and_errors():
     from paper_2005_01182_b200 import solve_batched_km, solve_km
     c = np.array([[1, 3], [2, 1]])
@@ -360,37 +417,6 @@ def test_calibrate_batch_level_matches_reference_rule():
     while B < cap and O.ref_solve_batched_km(c, B=B).objective > 1.1 * exact * (1 + 1e-12):
         B *= 2
     assert calibrate_batch_level(c, exact, 1.1) == min(B, cap)
-
-
-def test_warp_engine_u16_mode_exact(solver):
-    """KMB_OPT_U16: 16-bit row offsets with an exact int32 fallback for rows
-    whose range reaches 65535 ("wide" rows) — same duals as the reference,
-    including instances forced to have wide rows."""
-    from paper_2005_01182_b200.api import OPT_U16
-    rng = np.random.default_rng(61)
-    c = W.CONFIGS["c3"].make(batch=48).copy()
-    for t in range(0, 48, 3):  # make some rows wide
-        c[t, rng.integers(0, 128), rng.integers(0, 128)] += 200000
-    solver.set_option(OPT_ENGINE, 4)
-    solver.set_option(OPT_U16, 1)
-    try:
-        r = solver.solve_batch(c, KMB_SEED_BATCHED)
-        for n in (100, 128, 200, 256):  # 4 and 8 columns per lane, padded pitches
-            cc = rng.integers(0, 70000 + 2000 * (n % 7), size=(6, n, n)).astype(np.int32)
-            rr = solver.solve_batch(cc, KMB_SEED_BATCHED)
-            for t in range(6):
-                ref = O.ref_solve_batched_km(cc[t])
-                assert rr.total_cost[t] == ref.total_cost
-                np.testing.assert_array_equal(rr.u[t], ref.u)
-                np.testing.assert_array_equal(rr.v[t], ref.v)
-    finally:
-        solver.set_option(OPT_U16, 0)
-        solver.set_option(OPT_ENGINE, 0)
-    for t in range(48):
-        ref = O.ref_solve_batched_km(c[t])
-        assert r.total_cost[t] == ref.total_cost
-        np.testing.assert_array_equal(r.u[t], ref.u)
-        np.testing.assert_array_equal(r.v[t], ref.v)
 
 
 @pytest.mark.gpu
@@ -546,7 +572,7 @@ def _dev_batch(c):
     return d, out
 
 
-@pytest.mark.parametrize("engine,n", [(0, 128), (4, 128), (6, 100), (3, 40), (8, 300)])
+@pytest.mark.parametrize("engine,n", [(0, 128), (4, 128), (6, 100), (4, 40), (8, 300)])
 def test_batch_async_matches_sync(solver, engine, n):
     """kmb_solve_batch_async_i32: stream-ordered, device buffers, statuses to a
     device buffer; results equal the synchronous call's."""
@@ -608,3 +634,33 @@ def test_batch_async_cuda_graph():
     for t in (0, 31, 63):
         assert int(tot[t]) == O.ref_solve_batched_km(c2[t]).total_cost
     assert int(status.abs().sum()) == 0
+
+
+def test_batch_misaligned_device_buffer_and_instance_stats(solver):
+    """A device cost buffer that is not 16-byte aligned (offset by one int32)
+    goes through the aligned workspace instead of faulting in the warp
+    engine's 128-bit loads; kmb_last_instance_stats reports
+    the last batch's instance count."""
+    import torch
+    c = W.CONFIGS["c3"].make(batch=40)
+    b, n, _ = c.shape
+    buf = torch.zeros(b * n * n + 1, dtype=torch.int32, device="cuda")
+    buf[1:] = torch.from_numpy(c.ravel()).cuda()
+    dc = buf[1:]
+    assert dc.data_ptr() % 16 == 4
+    r2c = torch.empty((b, n), dtype=torch.int32, device="cuda")
+    u = torch.empty((b, n), dtype=torch.int64, device="cuda")
+    v = torch.empty_like(u)
+    tot = torch.empty(b, dtype=torch.int64, device="cuda")
+    for engine in (0, 4, 6):
+        solver.set_option(OPT_ENGINE, engine)
+        try:
+            solver.solve_batch_into(dc, b, n, 1, r2c, u, v, tot)
+        finally:
+            solver.set_option(OPT_ENGINE, 0)
+        for t in range(b):
+            ref = O.ref_solve_batched_km(c[t])
+            assert int(tot[t]) == ref.total_cost
+            np.testing.assert_array_equal(u[t].cpu().numpy(), ref.u)
+    st = solver.last_instance_stats(b)
+    assert st.shape == (b, 11) and (st[:, 3] > 0).all()  # rounds of every instance

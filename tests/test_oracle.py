@@ -183,3 +183,22 @@ def test_golden_fixtures():
         k = O.kmo_solve_batched(c)
         assert k.total_cost == small["total"][t]
         assert np.array_equal(k.u, small["u"][t, :n]) and np.array_equal(k.v, small["v"][t, :n])
+
+
+def test_seeded_km_restatement_equals_reference_on_config4():
+    """The c5 golden is produced by the seeded e-maxx restatement (the
+    reference's solve_batched_km would take ~1 h there).  That restatement
+    must equal the unmodified reference on the largest config the reference
+    solves in this repo: config 4 (n = 4096, GMM), whose golden the reference
+    itself produced (tests/golden/make_golden.py --with-c4).  ~4 s."""
+    import json
+    from paper_2005_01182_b200 import workloads as W
+    with open(os.path.join(os.path.dirname(__file__), "golden", "configs.json")) as f:
+        g = json.load(f)
+    for key in ("c1", "c2", "c4"):
+        c = W.CONFIGS[key].make()
+        assert W.fnv1a64(c) == g[key]["cost_fnv"]
+        assert "reference" in g[key]["producer"]
+        r = O.kmo_solve_km_seeded(c)
+        assert r.total_cost == g[key]["total_cost"]
+        assert W.fnv1a64(r.u) == g[key]["u_fnv"] and W.fnv1a64(r.v) == g[key]["v_fnv"]

@@ -57,6 +57,16 @@ def test_sharded_protocol_cpu_gloo(world):
     _check(_run(world, "sim"))
 
 
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("op,at", [(8, 1), (2, 7), (3, 5), (5, 3), (7, 1)])
+def test_sharded_local_failure_fails_every_rank(op, at):
+    """A failure on one rank (before the protocol, or in any slab operation at
+    any round) is voted on at the next collective: every rank returns -1
+    instead of the others waiting forever."""
+    per_rank = _run(2, f"fail:{op}:{at}")
+    assert [int(r[0]) for r in per_rank] == [-1, -1]
+
+
 @pytest.mark.gpu
 def test_sharded_cuda_two_ranks_one_gpu():
     _check(_run(2, "gpu"))

@@ -12,14 +12,11 @@ ap.add_argument("--batch", type=int, default=4096)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--maxg", type=int, default=0)
-ap.add_argument("--u16", type=int, default=1)
 a = ap.parse_args()
 s = Solver(0)
 s.set_option(OPT_ENGINE, a.engine)
 from paper_2005_01182_b200.api import OPT_MAX_CTAS
 s.set_option(OPT_MAX_CTAS, a.maxg)
-from paper_2005_01182_b200.api import OPT_U16
-s.set_option(OPT_U16, a.u16)
 c = W.CONFIGS[a.config].make(batch=a.batch) if a.config == "c3" else W.CONFIGS[a.config].make()
 dc = torch.from_numpy(c).cuda()
 if a.config == "c3":
