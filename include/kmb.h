@@ -54,7 +54,9 @@ enum kmb_status {
   KMB_OK = 0,
   KMB_EINVAL = 1,        /* bad argument (n <= 0, null pointer, ld < n) */
   KMB_ENEGATIVE = 2,     /* "costs must be nonnegative" (core.cpp:144-145) */
-  KMB_ERANGE = 3,        /* a cost >= 2^29 (device range)                  */
+  KMB_ERANGE = 3,        /* _i32 calls: a cost >= 2^29 (32-bit engines' range);
+                            _i64 calls: validate_instance's headroom
+                            (core.cpp:47-53) exceeded                        */
   KMB_ECUDA = -1,        /* CUDA runtime error                             */
   KMB_EINTERNAL = -2,    /* engine invariant violated                      */
   KMB_ENODEVICE = -3     /* no sm_100 device                               */
@@ -140,6 +142,42 @@ int kmb_solve_batch_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, i
 int kmb_solve_batch_async_i32(kmb_context* ctx, const int32_t* costs, int32_t batch, int32_t n,
                               int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
                               int64_t* total_cost, int32_t* status);
+
+/* ---- 64-bit costs: the reference's own cost type (OTInstance::cost) --------
+ * kmb_solve_i64 / kmb_solve_batch_i64: kmb_solve_i32 / kmb_solve_batch_i32 on
+ * int64 costs over the reference's whole admissible range — any nonnegative
+ * cost within validate_instance's headroom n * maxC * (2n + 2) <= 2^62
+ * (core.cpp:47-53; KMB_ERANGE "supply * cost magnitude too large for 64-bit
+ * arithmetic" beyond it).  Validation runs on the device; costs < 2^29 are
+ * narrowed on the device and solved by the 32-bit engines, larger costs by the
+ * wide engine (64-bit keys and duals, stats->engine 9).  Same duals as the
+ * reference. */
+int kmb_solve_i64(kmb_context* ctx, const int64_t* cost, int32_t n, int64_t ld, int32_t seed,
+                  double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
+                  int64_t* total_cost, kmb_stats* stats);
+int kmb_solve_batch_i64(kmb_context* ctx, const int64_t* costs, int32_t batch, int32_t n,
+                        int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
+                        int64_t* total_cost, kmb_stats* stats);
+
+/* quantize_costs (hungarian.cpp:33-53) on the device: N = max cost (1 when
+ * every cost is 0), chat[k] = floor(cost[k] * B / N), lossless = every product
+ * divisible.  chat (count entries) may be NULL; host or device pointers.
+ * KMB_EINVAL with the reference's messages "quantize_costs: B must be
+ * positive" / "quantize_costs: B * max cost overflows". */
+int kmb_quantize_i64(kmb_context* ctx, const int64_t* cost, int64_t count, int64_t B, int64_t* chat,
+                     int64_t* N, int32_t* lossless);
+
+/* ot::solve_batched_km (hungarian.cpp:313-381) end to end on the device:
+ * validation, quantization to chat = floor(C * B / N), the reductions and the
+ * search on chat.  u, v: the duals of chat (DualPotentials); row_to_col; total_cost
+ * = the objective on the caller's costs C; chat (n*n, optional) / N / lossless:
+ * QuantizedCosts.  B = N * n reproduces solve_km's optimum (lossless).  Error
+ * messages are the reference's ("solve_batched_km: costs must be nonnegative",
+ * "quantize_costs: ..."). */
+int kmb_solve_batched_km_i64(kmb_context* ctx, const int64_t* cost, int32_t n, int64_t B,
+                             double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
+                             int64_t* total_cost, int64_t* chat, int64_t* N, int32_t* lossless,
+                             kmb_stats* stats);
 
 /* One process, several GPUs (BASELINE config 3 "instances sharded across
  * GPUs" without one process per GPU): the batch is split into nctx contiguous

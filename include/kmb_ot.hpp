@@ -14,9 +14,11 @@
 // Same inputs (OTInstance), same outputs (SolveResult built with the
 // reference's own make_result, optional DualPotentials / Matching /
 // QuantizedCosts overwritten wholesale), same exceptions and messages
-// (hungarian.cpp:15-21, :34, :44-45, :353-354).  Beyond the reference, costs
-// must fit the device range [0, 2^29) after quantization; a larger entry
-// throws std::invalid_argument("<who>: cost exceeds the device range [0, 2^29)").
+// (hungarian.cpp:15-21, :34, :44-45, :353-354).  The KM solvers take the
+// reference's int64 costs over its whole admissible range (kmb_solve_i64,
+// kmb_solve_batched_km_i64: validation and quantization run on the device; the
+// one deviation is a quantized cost above 2^60, i.e. B > 2^60, which throws
+// std::invalid_argument rather than risk the reference's own int64 overflow).
 // A CUDA failure throws std::runtime_error (there is no CPU fallback).
 //
 // Registering them as bench plugins (bench.cpp:391-464) is one line each,
@@ -56,20 +58,18 @@ inline void require_unit_square(const OTInstance& inst, const char* who) {
     throw std::invalid_argument(std::string(who) + ": requires a unit-capacity square instance");
 }
 
-inline std::vector<int32_t> narrow(const std::vector<int64_t>& c, const char* who) {
-  std::vector<int32_t> out(c.size());
-  for (size_t k = 0; k < c.size(); ++k) {
-    if (c[k] >= (int64_t{1} << 29))
-      throw std::invalid_argument(std::string(who) + ": cost exceeds the device range [0, 2^29)");
-    out[k] = static_cast<int32_t>(c[k]);
-  }
-  return out;
-}
-
 inline void check(int rc, const char* who) {
   if (rc == KMB_OK) return;
   if (rc > 0) throw std::invalid_argument(std::string(who) + ": " + kmb_last_error());
   throw std::runtime_error(std::string(who) + ": " + kmb_last_error());
+}
+
+// the C ABI's message as is: kmb_solve_batched_km_i64 words its errors like
+// the reference ("solve_batched_km: ...", "quantize_costs: ...")
+inline void check_verbatim(int rc) {
+  if (rc == KMB_OK) return;
+  if (rc > 0) throw std::invalid_argument(kmb_last_error());
+  throw std::runtime_error(kmb_last_error());
 }
 
 inline Flow matching_flow(int32_t n, const std::vector<int32_t>& row_to_col) {
@@ -87,12 +87,11 @@ inline SolveResult solve_km_b200(const OTInstance& inst, DualPotentials* duals =
   kmb_detail::require_unit_square(inst, "solve_km");
   const auto t0 = std::chrono::steady_clock::now();
   const int32_t n = inst.n;
-  const std::vector<int32_t> c = kmb_detail::narrow(inst.cost, "solve_km");
   std::vector<int32_t> r2c(n, -1);
   std::vector<int64_t> u(n), v(n);
   int64_t total = 0;
   kmb_stats st{};
-  kmb_detail::check(kmb_solve_i32(kmb_detail::context(), c.data(), n, n, KMB_SEED_KM,
+  kmb_detail::check(kmb_solve_i64(kmb_detail::context(), inst.cost.data(), n, n, KMB_SEED_KM,
                                   time_budget_s, r2c.data(), u.data(), v.data(), &total, &st),
                     "solve_km");
   const bool done = st.converged != 0;
@@ -105,7 +104,9 @@ inline SolveResult solve_km_b200(const OTInstance& inst, DualPotentials* duals =
   }
   int32_t matched = 0;
   for (int32_t j : r2c) matched += j >= 0;
-  // iterations: rows inserted (hungarian.cpp:113, :130)
+  // iterations: rows inserted (hungarian.cpp:113, :130).  On budget expiry the
+  // reference reports the i + 1 rows it processed, each of which it matched;
+  // the parallel engine's counterpart is the number of matched rows.
   SolveResult res = make_result(inst, kmb_detail::matching_flow(n, r2c), done ? n : matched,
                                 /*exact=*/done, /*converged=*/done);
   res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -118,35 +119,25 @@ inline SolveResult solve_batched_km_b200(const OTInstance& inst, const BatchedKM
   kmb_detail::require_unit_square(inst, "solve_batched_km");
   const auto t0 = std::chrono::steady_clock::now();
   const int32_t n = inst.n;
-  QuantizedCosts q = quantize_costs(inst.cost, config.B);  // the reference's own, :33-53
-  // B a multiple of N (e.g. the lossless B = N*n): chat = k*C exactly and the
-  // search is scale-equivariant, so solve C and scale the duals by k when chat
-  // itself would leave the device range.
-  int64_t k = 1;
-  if (q.N > 0 && config.B % q.N == 0) {
-    int64_t mx = 0;
-    for (int64_t x : q.chat) mx = x > mx ? x : mx;
-    if (mx >= (int64_t{1} << 29)) k = config.B / q.N;
-  }
-  const std::vector<int32_t> c = kmb_detail::narrow(k > 1 ? inst.cost : q.chat, "solve_batched_km");
   std::vector<int32_t> r2c(n, -1);
   std::vector<int64_t> u(n), v(n);
   int64_t total = 0;
   kmb_stats st{};
-  kmb_detail::check(kmb_solve_i32(kmb_detail::context(), c.data(), n, n, KMB_SEED_BATCHED,
-                                  config.time_budget_s, r2c.data(), u.data(), v.data(), &total,
-                                  &st),
-                    "solve_batched_km");
+  QuantizedCosts q;
+  q.B = config.B;
+  if (quantized) q.chat.resize(inst.cost.size());
+  int32_t lossless = 0;
+  // validation, quantize_costs (:33-53, K11), reductions and search on the device
+  kmb_detail::check_verbatim(kmb_solve_batched_km_i64(
+      kmb_detail::context(), inst.cost.data(), n, config.B, config.time_budget_s, r2c.data(), u.data(),
+      v.data(), &total, quantized ? q.chat.data() : nullptr, &q.N, &lossless, &st));
+  q.lossless = lossless != 0;
   const bool budget_ok = st.converged != 0;
   if (duals) {
     duals->u = u;
     duals->v = v;
-    if (k > 1) {
-      for (int64_t& x : duals->u) x *= k;
-      for (int64_t& x : duals->v) x *= k;
-    }
   }
-  if (quantized) *quantized = q;
+  if (quantized) *quantized = std::move(q);
   // iterations = phases + dual adjustments (hungarian.cpp:375); the dual-step
   // count equals the reference's, the phase count is the engine's own.
   SolveResult res = make_result(inst, kmb_detail::matching_flow(n, r2c), st.phases + st.dual_steps,

@@ -33,7 +33,8 @@ ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", 
                "kmb_shard_init_nccl",
                "kmb_shard_init_callbacks", "kmb_solve_sharded_i32", "kmb_bench_scan",
                "kmb_last_instance_stats", "kmb_costs_from_points", "kmb_auction_i32",
-               "kmb_last_error", "kmb_abi_version")
+               "kmb_solve_i64", "kmb_solve_batch_i64", "kmb_quantize_i64",
+               "kmb_solve_batched_km_i64", "kmb_last_error", "kmb_abi_version")
 
 
 class KmbUnavailable(RuntimeError):
@@ -92,6 +93,13 @@ def load_library(path: str | None = None):
                                               C.c_int32, C.c_int32, C.c_double, C.c_int32, vp]
         lib.kmb_auction_i32.argtypes = [vp, vp, C.c_int32, C.c_int32, C.POINTER(AuctionConfig),
                                         vp, vp, vp, vp, vp, vp, C.POINTER(C.c_double)]
+        lib.kmb_solve_i64.argtypes = lib.kmb_solve_i32.argtypes
+        lib.kmb_solve_batch_i64.argtypes = lib.kmb_solve_batch_i32.argtypes
+        lib.kmb_quantize_i64.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int32)]
+        lib.kmb_solve_batched_km_i64.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_double, vp, vp, vp,
+                                                 vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                                 C.POINTER(Stats)]
         lib.kmb_last_error.restype = C.c_char_p
         lib.kmb_abi_version.restype = C.c_int
         _lib = lib
@@ -183,6 +191,50 @@ class Solver:
                                            C.byref(st) if st is not None else None)
         self._check(rc)
         return st
+
+    def solve_i64_into(self, cost, n: int, ld: int, seed: int, row_to_col, u, v, total_cost,
+                       time_budget_s: float = 0.0, stats: bool = True) -> Stats | None:
+        """``kmb_solve_i64``: int64 costs over the reference's whole range."""
+        st = Stats() if stats else None
+        rc = self._lib.kmb_solve_i64(self._h, C.c_void_p(_ptr(cost)), n, ld, seed, time_budget_s,
+                                     C.c_void_p(_ptr(row_to_col)), C.c_void_p(_ptr(u)),
+                                     C.c_void_p(_ptr(v)), C.c_void_p(_ptr(total_cost)),
+                                     C.byref(st) if st is not None else None)
+        self._check(rc)
+        return st
+
+    def solve_batch_i64_into(self, costs, batch: int, n: int, seed: int, row_to_col, u, v,
+                             total_cost, stats: bool = True) -> Stats | None:
+        st = Stats() if stats else None
+        rc = self._lib.kmb_solve_batch_i64(self._h, C.c_void_p(_ptr(costs)), batch, n, seed,
+                                           C.c_void_p(_ptr(row_to_col)), C.c_void_p(_ptr(u)),
+                                           C.c_void_p(_ptr(v)), C.c_void_p(_ptr(total_cost)),
+                                           C.byref(st) if st is not None else None)
+        self._check(rc)
+        return st
+
+    def quantize(self, cost, B: int, chat=None) -> tuple[int, bool]:
+        """``kmb_quantize_i64`` (K11 on the device): fills ``chat`` (optional,
+        same size as ``cost``) and returns (N, lossless)."""
+        N = C.c_int64()
+        ll = C.c_int32()
+        count = int(np.prod(cost.shape)) if len(cost.shape) else 1
+        self._check(self._lib.kmb_quantize_i64(self._h, C.c_void_p(_ptr(cost)), count, int(B),
+                                               C.c_void_p(_ptr(chat)), C.byref(N), C.byref(ll)))
+        return int(N.value), bool(ll.value)
+
+    def solve_batched_km_into(self, cost, n: int, B: int, row_to_col, u, v, total_cost,
+                              chat=None, time_budget_s: float = 0.0) -> tuple[Stats, int, bool]:
+        """``kmb_solve_batched_km_i64``: the reference's solve_batched_km on the
+        device (quantization included); returns (stats, N, lossless)."""
+        st = Stats()
+        N = C.c_int64()
+        ll = C.c_int32()
+        self._check(self._lib.kmb_solve_batched_km_i64(
+            self._h, C.c_void_p(_ptr(cost)), n, int(B), time_budget_s, C.c_void_p(_ptr(row_to_col)),
+            C.c_void_p(_ptr(u)), C.c_void_p(_ptr(v)), C.c_void_p(_ptr(total_cost)),
+            C.c_void_p(_ptr(chat)), C.byref(N), C.byref(ll), C.byref(st)))
+        return st, int(N.value), bool(ll.value)
 
     def solve_batch_async(self, costs, batch: int, n: int, seed: int, row_to_col, u, v,
                           total_cost, status) -> None:
@@ -285,7 +337,10 @@ class Solver:
     # -- numpy convenience -------------------------------------------------------
     def solve(self, cost: np.ndarray, seed: int = KMB_SEED_BATCHED,
               time_budget_s: float = 0.0) -> Result:
-        c = np.ascontiguousarray(cost, dtype=np.int32)
+        """int64 input goes through kmb_solve_i64 (the reference's cost type and
+        range), anything else through kmb_solve_i32."""
+        wide = np.asarray(cost).dtype == np.int64
+        c = np.ascontiguousarray(cost, dtype=np.int64 if wide else np.int32)
         if c.ndim != 2 or c.shape[0] != c.shape[1]:
             raise ValueError("square cost matrix required")
         n = c.shape[0]
@@ -294,14 +349,16 @@ class Solver:
         v = np.zeros(n, np.int64)
         tot = np.zeros(1, np.int64)
         t0 = time.perf_counter()
-        st = self.solve_into(c, n, n, seed, r2c, u, v, tot, time_budget_s)
+        call = self.solve_i64_into if wide else self.solve_into
+        st = call(c, n, n, seed, r2c, u, v, tot, time_budget_s)
         wall = time.perf_counter() - t0
         return Result(r2c, u, v, int(tot[0]), iterations=int(st.phases + st.dual_steps),
                       exact=bool(st.converged), converged=bool(st.converged), wall_seconds=wall,
                       stats=_stats_dict(st))
 
     def solve_batch(self, costs: np.ndarray, seed: int = KMB_SEED_BATCHED) -> Result:
-        c = np.ascontiguousarray(costs, dtype=np.int32)
+        wide = np.asarray(costs).dtype == np.int64
+        c = np.ascontiguousarray(costs, dtype=np.int64 if wide else np.int32)
         b, n, n2 = c.shape
         if n != n2:
             raise ValueError("square cost matrices required")
@@ -310,7 +367,8 @@ class Solver:
         v = np.zeros((b, n), np.int64)
         tot = np.zeros(b, np.int64)
         t0 = time.perf_counter()
-        st = self.solve_batch_into(c, b, n, seed, r2c, u, v, tot)
+        call = self.solve_batch_i64_into if wide else self.solve_batch_into
+        st = call(c, b, n, seed, r2c, u, v, tot)
         wall = time.perf_counter() - t0
         return Result(r2c, u, v, tot, iterations=int(st.phases + st.dual_steps),
                       wall_seconds=wall, stats=_stats_dict(st))
@@ -387,31 +445,32 @@ def _validate(cost, supplies, demands, who: str) -> np.ndarray:
     return c
 
 
-def quantize_costs(cost, B: int):
-    """``ot::quantize_costs`` (hungarian.cpp:33-53): chat = floor(C*B/N)."""
+def quantize_costs(cost, B: int, solver: Solver | None = None):
+    """``ot::quantize_costs`` (hungarian.cpp:33-53) on the device
+    (``kmb_quantize_i64``): returns (chat = floor(C*B/N), N, lossless)."""
     if B <= 0:
         raise ValueError("quantize_costs: B must be positive")
-    c = np.asarray(cost, dtype=np.int64)
-    N = int(c.max()) if c.size else 0
-    if N <= 0:
-        return c.copy(), 1, True
-    if B > (2**63 - 1) // N:
-        raise ValueError("quantize_costs: B * max cost overflows")
-    scaled = c * np.int64(B)
-    chat = scaled // np.int64(N)
-    return chat, N, bool(np.array_equal(chat * N, scaled))
+    c = np.ascontiguousarray(cost, dtype=np.int64)
+    chat = np.empty_like(c)
+    try:
+        N, lossless = (solver or default_solver()).quantize(c, int(B), chat)
+    except KmbError as e:
+        raise ValueError(str(e)) from None
+    return chat, N, lossless
 
 
 def solve_km(cost, supplies=None, demands=None, time_budget_s: float = 0.0,
              solver: Solver | None = None) -> Result:
-    """Exact KM from u = v = 0; duals identical to ``ot::solve_km``."""
+    """Exact KM from u = v = 0; duals identical to ``ot::solve_km``.  int64
+    costs over the reference's whole admissible range (kmb_solve_i64)."""
     c = _validate(cost, supplies, demands, "solve_km")
-    if (c < 0).any():
-        raise ValueError("solve_km: costs must be nonnegative")
-    if c.max() >= 2**29:
-        _range_error("solve_km")
     s = solver or default_solver()
-    r = s.solve(c.astype(np.int32, copy=False), KMB_SEED_KM, time_budget_s)
+    try:
+        r = s.solve(np.asarray(c, dtype=np.int64), KMB_SEED_KM, time_budget_s)
+    except KmbError as e:
+        if e.code > 0:
+            raise ValueError("solve_km: " + str(e).split(": ", 1)[-1]) from None
+        raise
     r.iterations = c.shape[0]  # hungarian.cpp:130: iterations = n
     return r
 
@@ -419,36 +478,35 @@ def solve_km(cost, supplies=None, demands=None, time_budget_s: float = 0.0,
 def solve_batched_km(cost, B: int | None = 100, supplies=None, demands=None,
                      time_budget_s: float = 0.0, solver: Solver | None = None,
                      return_quantized: bool = False):
-    """``ot::solve_batched_km`` on chat = quantize_costs(cost, B).  The default
-    B = 100 is ``BatchedKMConfig{}``'s (hungarian.hpp:42-45), so a caller
-    relying on the default gets the reference's (possibly lossy) answer;
-    ``B=None`` (an extension) is the lossless B = N.  ``exact`` = lossless and
-    converged (hungarian.cpp:374-376); the total cost and objective are
-    reported against the true costs."""
+    """``ot::solve_batched_km`` end to end on the device
+    (``kmb_solve_batched_km_i64``: validation, quantization to chat, search).
+    The default B = 100 is ``BatchedKMConfig{}``'s (hungarian.hpp:42-45), so a
+    caller relying on the default gets the reference's (possibly lossy) answer;
+    ``B=None`` (an extension) is the lossless B = N.  u, v are the duals of
+    chat; ``exact`` = lossless and converged (hungarian.cpp:374-376); the total
+    cost and objective are reported against the true costs."""
     c = _validate(cost, supplies, demands, "solve_batched_km")
-    if (c < 0).any():
-        raise ValueError("solve_batched_km: costs must be nonnegative")
-    c64 = np.asarray(c, dtype=np.int64)
+    c64 = np.ascontiguousarray(c, dtype=np.int64)
     if B is None:
         B = max(int(c64.max()), 1)
-    chat, N, lossless = quantize_costs(c64, int(B))
+    n = c64.shape[0]
     s = solver or default_solver()
-    scale = int(B) // N if int(B) % N == 0 and N > 0 else 0
-    if scale > 1 and chat.size and chat.max() >= 2**29 and c64.max() < 2**29:
-        # B a multiple of N (e.g. the lossless B = N*n): chat = k*C exactly.  The
-        # search is scale-equivariant (every slack, delta and comparison scales by
-        # k > 0), so the reference's duals on chat are k times the duals on C.
-        r = s.solve(c64.astype(np.int32), KMB_SEED_BATCHED, time_budget_s)
-        r.u = r.u * scale
-        r.v = r.v * scale
-    else:
-        if chat.size and chat.max() >= 2**29:
-            _range_error("solve_batched_km")
-        r = s.solve(chat.astype(np.int32), KMB_SEED_BATCHED, time_budget_s)
-    r.exact = bool(lossless and r.converged)
-    rows = np.arange(c64.shape[0])
-    ok = r.row_to_col >= 0
-    r.total_cost = int(c64[rows[ok], r.row_to_col[ok]].sum())
+    r2c = np.full(n, -1, np.int32)
+    u = np.zeros(n, np.int64)
+    v = np.zeros(n, np.int64)
+    tot = np.zeros(1, np.int64)
+    chat = np.empty_like(c64) if return_quantized else None
+    t0 = time.perf_counter()
+    try:
+        st, N, lossless = s.solve_batched_km_into(c64, n, int(B), r2c, u, v, tot, chat, time_budget_s)
+    except KmbError as e:
+        if e.code > 0:
+            raise ValueError(str(e)) from None
+        raise
+    wall = time.perf_counter() - t0
+    r = Result(r2c, u, v, int(tot[0]), iterations=int(st.phases + st.dual_steps),
+               exact=bool(lossless and st.converged), converged=bool(st.converged),
+               wall_seconds=wall, stats=_stats_dict(st))
     if return_quantized:
         return r, (chat, int(B), N, lossless)
     return r
@@ -536,6 +594,3 @@ def calibrate_auction_eps(cost, exact_int: int, solver: Solver | None = None) ->
         raise RuntimeError("auction calibration failed at epsilon = 1/(n+1)")
     return best
 
-
-def _range_error(who: str):
-    raise ValueError(f"{who}: cost exceeds the device range [0, 2^29)")

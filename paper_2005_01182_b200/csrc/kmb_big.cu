@@ -14,8 +14,11 @@
 // they are recomputed cooperatively (threads split the survivor rows of each
 // dirty column) instead of streaming every survivor row through one SM.
 //
-// Layout: thread t owns columns t, t + T, ..., t + (CPT-1)·T (coalesced row
-// loads); per-column key / v / Dc in registers; per-row state, the row lists,
+// Layout: thread t owns CPT columns in groups of V contiguous ones, group g at
+// columns V·(t + g·T) .. V·(t + g·T) + V - 1, so a row is read with one V-wide
+// vector load per group (LDG.64 / LDG.128: a lone SM is issue-bound, and
+// scalar loads issued V times more load instructions); per-column key / v / Dc
+// in registers; per-row state, the row lists,
 // parents, matching, 32-bit tree claims and the dirty-column list in shared
 // memory (14n words: 224 KB at n = 4096).
 #include <cuda_runtime.h>
@@ -23,7 +26,6 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
-#include <cstdlib>
 #include <type_traits>
 
 #include "kmb_common.cuh"
@@ -84,12 +86,29 @@ struct BigShared {
   unsigned long long tot;
 };
 
-template <int CPT, int kT>
+// V contiguous int32 of a row (16·V-bit vector load of immutable costs)
+template <int V>
+__device__ __forceinline__ void load_vec(const int32_t* p, int32_t* out) {
+  if constexpr (V == 4) {
+    const int4 x = __ldg(reinterpret_cast<const int4*>(p));
+    out[0] = x.x; out[1] = x.y; out[2] = x.z; out[3] = x.w;
+  } else if constexpr (V == 2) {
+    const int2 x = __ldg(reinterpret_cast<const int2*>(p));
+    out[0] = x.x; out[1] = x.y;
+  } else {
+    out[0] = __ldg(p);
+  }
+}
+
+template <int CPT, int kT, int V>
 __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
+  static_assert(CPT % V == 0, "columns per thread must be whole vector groups");
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BigShared sm;
   const int n = a.n;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  // column of this thread's q-th slot
+  auto colof = [&](int q) { return V * (t + (q / V) * kT) + (q % V); };
   int2* rows = reinterpret_cast<int2*>(dyn);
   int2* spare = rows + n;  // also the dirty-column keys in the round after an epoch end
   int32_t* u = reinterpret_cast<int32_t*>(spare + n);
@@ -171,7 +190,7 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
       key[q] = ~0ull;
       v[q] = 0;
       dc[q] = 0;
-      if (t + q * kT >= n) rch |= 1u << q;
+      if (colof(q) >= n) rch |= 1u << q;
     }
     int nrows = n, head = 0, nfree = n, nfound = 0;
     int32_t D = 0;
@@ -195,9 +214,12 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
 #pragma unroll
       for (int k = 0; k < K; ++k)
 #pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-          const int col = t + q * kT;
-          c[k][q] = col < n ? __ldg(Cm + (e[k].x * ld32 + col)) : 0;
+        for (int g = 0; g < CPT / V; ++g) {
+          const int col = V * (t + g * kT);  // the pitch is padded to V: a group is in or out
+          if (col < n) load_vec<V>(Cm + (e[k].x * ld32 + col), &c[k][g * V]);
+          else
+#pragma unroll
+            for (int h = 0; h < V; ++h) c[k][g * V + h] = 0;
         }
 #pragma unroll
       for (int k = 0; k < K; ++k)
@@ -265,7 +287,7 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
-          const int col = t + q * kT;
+          const int col = colof(q);
           if (col < n && !((rch >> q) & 1) && key[q] == ~0ull)
             key[q] = reinterpret_cast<const uint64_t*>(spare)[dpos[col]];
         }
@@ -303,7 +325,7 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
         if (((rch >> q) & 1) || s[q] != D) continue;
-        const int col = t + q * kT;
+        const int col = colof(q);
         rch |= 1u << q;
         dc[q] = D;
         const int32_t par = BK::row(key[q]);
@@ -340,7 +362,7 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
-        const int col = t + q * kT;
+        const int col = colof(q);
         if (col >= n) continue;
         if ((rch >> q) & 1) {
           if (bclaimed(claim[root_row[tree_par[col]]], epochs)) {
@@ -416,7 +438,7 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
       }
 #pragma unroll
       for (int q = 0; q < CPT; ++q)
-        if (((rch >> q) & 1) && t + q * kT < n) v[q] -= D - dc[q];
+        if (((rch >> q) & 1) && colof(q) < n) v[q] -= D - dc[q];
     }
     __syncthreads();
     // ---- outputs ----
@@ -429,7 +451,7 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
     }
 #pragma unroll
     for (int q = 0; q < CPT; ++q)
-      if (t + q * kT < n) a.v[static_cast<int64_t>(inst) * n + t + q * kT] = v[q];
+      if (colof(q) < n) a.v[static_cast<int64_t>(inst) * n + colof(q)] = v[q];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
     if (lane == 0) atomicAdd(&sm.tot, static_cast<unsigned long long>(tot));
@@ -465,9 +487,9 @@ int big_max_n() { return 4096; }
 #define KMB_BIG_CARVE 1
 #endif
 
-template <int CPT, int NT>
+template <int CPT, int NT, int V = (CPT >= 4 ? 4 : CPT)>
 static cudaError_t launch_nt(const BigArgs& a, int sm_count, size_t smem, cudaStream_t st) {
-  const void* k = reinterpret_cast<const void*>(k_big<CPT, NT>);
+  const void* k = reinterpret_cast<const void*>(k_big<CPT, NT, V>);
   // carveout: the shared memory of the CTAs per SM this batch needs (+1 KiB
   // each, one CTA per SM for a single instance); the rest of the unified cache
   // is L1 for the cost rows
@@ -480,37 +502,22 @@ static cudaError_t launch_nt(const BigArgs& a, int sm_count, size_t smem, cudaSt
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int grid = static_cast<int>(std::min<int64_t>(a.batch, static_cast<int64_t>(occ) * sm_count));
-  k_big<CPT, NT><<<grid, NT, smem, st>>>(a);
+  k_big<CPT, NT, V><<<grid, NT, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_big(const BigArgs& a, int sm_count, cudaStream_t st) {
   if (a.n < 1 || a.n > big_max_n()) return cudaErrorInvalidValue;
   const size_t smem = big_smem_bytes(a.n);
-  // threads per CTA: a lone SM is issue-bound, so columns per thread trade
-  // per-warp overhead against per-thread work.  Measured (c2 / c4 / uniform
-  // n=2048 / geometric n=3072, ms): 1024 threads 8.88 / 158 / 16.2 / 107,
-  // 512: 8.85 / 157 / 14.1 / 103, 256: 10.9 / 214 / 17.2 / 135.
-  // KMB_BIG_THREADS (256 / 512 / 1024) overrides for A/B runs.
-  static const int nt_env = getenv("KMB_BIG_THREADS") ? atoi(getenv("KMB_BIG_THREADS")) : 0;
-  int nt = nt_env ? nt_env : 512;
-  const int cpt = (a.n + nt - 1) / nt;
-  if (nt == 256) {
-    if (cpt <= 1) return launch_nt<1, 256>(a, sm_count, smem, st);
-    if (cpt <= 2) return launch_nt<2, 256>(a, sm_count, smem, st);
-    if (cpt <= 4) return launch_nt<4, 256>(a, sm_count, smem, st);
-    if (cpt <= 8) return launch_nt<8, 256>(a, sm_count, smem, st);
-    return launch_nt<16, 256>(a, sm_count, smem, st);
-  }
-  if (nt == 512) {
-    if (cpt <= 1) return launch_nt<1, 512>(a, sm_count, smem, st);
-    if (cpt <= 2) return launch_nt<2, 512>(a, sm_count, smem, st);
-    if (cpt <= 4) return launch_nt<4, 512>(a, sm_count, smem, st);
-    return launch_nt<8, 512>(a, sm_count, smem, st);
-  }
-  if (cpt <= 1) return launch_nt<1, 1024>(a, sm_count, smem, st);
-  if (cpt <= 2) return launch_nt<2, 1024>(a, sm_count, smem, st);
-  return launch_nt<4, 1024>(a, sm_count, smem, st);
+  // 512 threads per CTA: a lone SM is issue-bound, so columns per thread trade
+  // per-warp overhead against per-thread work.  Measured in round 1 (c2 / c4 /
+  // uniform n=2048 / geometric n=3072, ms): 1024 threads 8.88 / 158 / 16.2 /
+  // 107, 512: 8.85 / 157 / 14.1 / 103, 256: 10.9 / 214 / 17.2 / 135.
+  const int cpt = (a.n + 511) / 512;
+  if (cpt <= 1) return launch_nt<1, 512>(a, sm_count, smem, st);
+  if (cpt <= 2) return launch_nt<2, 512>(a, sm_count, smem, st);
+  if (cpt <= 4) return launch_nt<4, 512>(a, sm_count, smem, st);
+  return launch_nt<8, 512>(a, sm_count, smem, st);
 }
 
 }  // namespace kmb

@@ -3,6 +3,7 @@
 // engine) and kmb_batch.cu (SMEM engine).
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <algorithm>
@@ -88,6 +89,9 @@ struct kmb_context {
   DevBuf pa, pb, pout, pbad;
   // auction workspace
   DevBuf aprice, ar2c, atot, abids, acomp, aeps, amin, amax;
+  // 64-bit cost path: staged costs, chat, narrowed costs, min/max + lossy flag,
+  // device-side results, wide-engine slots
+  DevBuf w64in, wchat, wnar, wmm, wr2c, wu, wv, wtot, wws64, wws32;
   // batch summary (device fold + pinned host copy)
   DevBuf bsum;
   int64_t* hsum = nullptr;
@@ -144,7 +148,8 @@ void kmb_destroy(kmb_context* c) {
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
                     &c->obj, &c->bcost, &c->bpad, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
                     &c->bstatus, &c->pa, &c->pb, &c->pout, &c->pbad, &c->aprice, &c->ar2c, &c->atot,
-                    &c->abids, &c->acomp, &c->aeps, &c->amin, &c->amax, &c->bsum})
+                    &c->abids, &c->acomp, &c->aeps, &c->amin, &c->amax, &c->bsum, &c->w64in, &c->wchat,
+                    &c->wnar, &c->wmm, &c->wr2c, &c->wu, &c->wv, &c->wtot, &c->wws64, &c->wws32})
     b->release();
   if (c->hsum) cudaFreeHost(c->hsum);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -221,17 +226,20 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // n > 256: one 512-thread CTA per instance (single-CTA engine, n <= 4096)
   auto pick = [&](int cnt) { return n > kmb::warp_max_n() ? 8 : (cnt <= cap6 ? 6 : 4); };
   if (auto_engine) engine = pick(batch);
-  const int np = kmb::warp_pitch(n);
   // Host input: stream the batch in chunks, each chunk's kernel starting as soon
   // as its H2D copy lands and its results leaving as soon as it ends, so the
   // PCIe transfers overlap the solves (the transfer bounds the end-to-end rate).
   const bool host_in = !is_device_ptr(costs);
   const bool warp_eng = engine == 4;
-  const bool pipelined = host_in && batch >= 256 && (!warp_eng || np == n);
-  // the warp engine's 128-bit row loads need rows padded to the warp width and
-  // a 16-byte aligned base: a caller's device buffer that is neither is copied
-  // into the aligned, padded workspace (a misaligned vector load would fault)
-  const bool repack = np != n || (!host_in && (reinterpret_cast<uintptr_t>(costs) & 15) != 0);
+  // row pitch of the vector-load engines: the warp engine's 128-bit loads need
+  // rows padded to the warp width, the single-CTA engine's (up to 128-bit)
+  // loads a pitch that is a multiple of 4; both a 16-byte aligned base.  A
+  // buffer that is neither is copied into the aligned, padded workspace (a
+  // misaligned vector load would fault).
+  const bool vec_eng = warp_eng || engine == 8;
+  const int np = warp_eng ? kmb::warp_pitch(n) : engine == 8 ? (n + 3) & ~3 : n;
+  const bool repack = vec_eng && (np != n || (!host_in && (reinterpret_cast<uintptr_t>(costs) & 15) != 0));
+  const bool pipelined = host_in && batch >= 256 && np == n;
   // chunk schedule [lo, lo + cnt): K equal chunks, and (tapered) the last one
   // split by halving down to KMB_TAPER_MIN instances, so the solve left after the final
   // copy lands is a short one
@@ -275,7 +283,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
   // stream-ordered calls write the statuses straight into the caller's buffer
   int32_t* const status_base = async_status ? async_status : c->bstatus.as<int32_t>();
-  const int32_t* src = dcost;  // warp engines: rows padded to the warp width
+  const int32_t* src = dcost;  // vector-load engines: rows padded to np
   int grid = 0;
   // the chunks of a pipelined call size their carveout for the largest chunk
   const int carve_batch = sched.empty() ? 0 : sched[0].second;
@@ -284,9 +292,9 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     const size_t ro = static_cast<size_t>(lo) * n;
     if (eng == 8) {
       kmb::BigArgs a{};
-      a.C = dcost + ro * n;
-      a.ld = n;
-      a.inst_stride = static_cast<int64_t>(n) * n;
+      a.C = src + ro * np;
+      a.ld = np;
+      a.inst_stride = static_cast<int64_t>(n) * np;
       a.batch = cnt;
       a.n = n;
       a.seed = seed;
@@ -345,7 +353,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   };
   int used = engine;
   if (async_status) {  // stream-ordered: enqueue and return (device buffers only)
-    if (warp_eng && repack) {
+    if (repack) {
       KMB_CUDA(c->bpad.ensure(nb * np * 4));
       KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4, nb, cudaMemcpyDeviceToDevice, st));
       src = c->bpad.as<int32_t>();
@@ -356,7 +364,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   KMB_CUDA(cudaEventRecord(c->ev0, st));
   if (!pipelined) {
     if (host_in) KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
-    if (warp_eng && repack) {  // rows padded to the warp width (in-bounds 128-bit loads): pad once
+    if (repack) {  // rows padded to np (in-bounds, aligned vector loads): pad once
       KMB_CUDA(c->bpad.ensure(nb * np * 4));
       KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4, nb, cudaMemcpyDeviceToDevice, st));
       src = c->bpad.as<int32_t>();
@@ -680,6 +688,347 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
     stats->rounds = h.rounds;
     for (int k = 0; k < 6; ++k) stats->stage_ns[k] = h.stage_ns[k];
   }
+  return KMB_OK;
+}
+
+}  // extern "C"
+
+// ---- 64-bit costs (the reference's own cost type) ------------------------------
+
+namespace {
+
+constexpr int64_t kNarrowMax = (int64_t{1} << 29) - 1;  // the 32-bit engines' range
+constexpr int64_t kWideMax = int64_t{1} << 60;          // |reduced costs| <= 4 * max < 2^63
+
+// validate_instance's headroom (core.cpp:47-53) for a unit square instance:
+// S * N * (n + m + 2) <= 2^62 with S = n, m = n
+int64_t headroom_max(int32_t n) {
+  const int64_t h = ((int64_t{1} << 62) / n) / (2 * static_cast<int64_t>(n) + 2);
+  return h < kWideMax ? h : kWideMax;
+}
+
+// the caller's costs as one contiguous device block (rows x cols)
+int stage_i64(kmb_context* c, const int64_t* cost, int64_t rows, int32_t cols, int64_t ld,
+              const int64_t** out) {
+  if (is_device_ptr(cost) && ld == cols) {
+    *out = cost;
+    return KMB_OK;
+  }
+  KMB_CUDA(c->w64in.ensure(static_cast<size_t>(rows) * cols * 8));
+  if (ld == cols) {
+    KMB_CUDA(cudaMemcpyAsync(c->w64in.p, cost, static_cast<size_t>(rows) * cols * 8, cudaMemcpyDefault,
+                             c->stream));
+    *out = c->w64in.as<int64_t>();
+    return KMB_OK;
+  }
+  KMB_CUDA(cudaMemcpy2DAsync(c->w64in.p, static_cast<size_t>(cols) * 8, cost, static_cast<size_t>(ld) * 8,
+                             static_cast<size_t>(cols) * 8, rows, cudaMemcpyDefault, c->stream));
+  *out = c->w64in.as<int64_t>();
+  return KMB_OK;
+}
+
+int minmax_i64(kmb_context* c, const int64_t* d, int64_t rows, int32_t cols, long long* lo, long long* hi) {
+  KMB_CUDA(c->wmm.ensure(32));
+  const long long init[2] = {LLONG_MAX, LLONG_MIN};
+  KMB_CUDA(cudaMemcpyAsync(c->wmm.p, init, 16, cudaMemcpyHostToDevice, c->stream));
+  KMB_CUDA(kmb::launch_minmax_i64(d, cols, rows, cols, c->wmm.as<long long>(), c->sm_count, c->stream));
+  long long h[2];
+  KMB_CUDA(cudaMemcpyAsync(h, c->wmm.p, 16, cudaMemcpyDeviceToHost, c->stream));
+  KMB_CUDA(cudaStreamSynchronize(c->stream));
+  *lo = h[0];
+  *hi = h[1];
+  return KMB_OK;
+}
+
+template <class T>
+int dev_or_ws(T* user, DevBuf& ws, size_t count, T** out) {
+  if (user && is_device_ptr(user)) {
+    *out = user;
+    return KMB_OK;
+  }
+  KMB_CUDA(ws.ensure(count * sizeof(T) > 0 ? count * sizeof(T) : 8));
+  *out = ws.as<T>();
+  return KMB_OK;
+}
+
+// Wide engine on contiguous device costs, device outputs; stats summed.
+int solve_wide(kmb_context* c, const int64_t* dC, int32_t batch, int32_t n, int32_t seed,
+               double time_budget_s, int32_t* dr2c, int64_t* du, int64_t* dv, int64_t* dtot,
+               kmb_stats* stats, const char* who) {
+  cudaStream_t st = c->stream;
+  const int slots = kmb::wide_slots(batch, c->sm_count);
+  KMB_CUDA(c->wws64.ensure(kmb::wide_ws64_bytes(n, slots)));
+  KMB_CUDA(c->wws32.ensure(kmb::wide_ws32_bytes(n, slots)));
+  KMB_CUDA(c->bstat.ensure(static_cast<size_t>(batch) * kmb::KMB_ISTATS * 8));
+  KMB_CUDA(c->bstatus.ensure(static_cast<size_t>(batch) * 4));
+  c->last_batch = batch;
+  kmb::WideArgs a{};
+  a.C = dC;
+  a.ld = n;
+  a.inst_stride = static_cast<int64_t>(n) * n;
+  a.batch = batch;
+  a.n = n;
+  a.seed = seed;
+  a.deadline_ns = time_budget_s > 0.0 ? static_cast<int64_t>(time_budget_s * 1e9) : 0;
+  a.row_to_col = dr2c;
+  a.u = du;
+  a.v = dv;
+  a.total_cost = dtot;
+  a.stats = c->bstat.as<int64_t>();
+  a.status = c->bstatus.as<int32_t>();
+  a.ws64 = c->wws64.as<int64_t>();
+  a.ws32 = c->wws32.as<int32_t>();
+  a.max_cost = kWideMax;
+  KMB_CUDA(cudaEventRecord(c->ev0, st));
+  KMB_CUDA(kmb::launch_wide(a, slots, st));
+  KMB_CUDA(cudaEventRecord(c->ev1, st));
+  KMB_CUDA(c->bsum.ensure(16 * 8));
+  if (!c->hsum) KMB_CUDA(cudaMallocHost(&c->hsum, 16 * 8));
+  KMB_CUDA(kmb::launch_batch_summary(c->bstat.as<int64_t>(), c->bstatus.as<int32_t>(), batch,
+                                     c->bsum.as<int64_t>(), st));
+  KMB_CUDA(cudaMemcpyAsync(c->hsum, c->bsum.p, 11 * 8, cudaMemcpyDeviceToHost, st));
+  {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, who);
+  }
+  const int64_t* h = c->hsum;
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->phases = h[1];
+    stats->dual_steps = h[2];
+    stats->rows_scanned = h[3];
+    stats->rounds = h[4];
+    stats->sum_instance_cycles = h[5];
+    stats->max_instance_cycles = h[6];
+    stats->cost_bytes_read = 8 * static_cast<int64_t>(n) * (h[3] + static_cast<int64_t>(batch) * n);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    stats->seconds = ms * 1e-3;
+    stats->converged = h[0] == kStopped ? 0 : 1;
+    stats->engine = 9;
+  }
+  if (h[0] == KMB_ERANGE)
+    return fail(KMB_ERANGE, std::string(who) + ": supply * cost magnitude too large for 64-bit arithmetic");
+  if (h[0] && h[0] != kStopped) return status_message(static_cast<int>(h[0]), who);
+  return KMB_OK;
+}
+
+// Solve `batch` contiguous device instances whose costs lie in [0, hi]: the
+// 32-bit engines on a narrowed copy when hi < 2^29, the wide engine otherwise.
+// Outputs are device buffers.
+// the narrowed copy in c->wnar on the 32-bit engines
+int solve_narrow_dev(kmb_context* c, int32_t batch, int32_t n, int32_t seed, double time_budget_s,
+                     int32_t* dr2c, int64_t* du, int64_t* dv, int64_t* dtot, kmb_stats* stats,
+                     const char* who) {
+  if (batch == 1)
+    return kmb_solve_i32(c, c->wnar.as<int32_t>(), n, n, seed, time_budget_s, dr2c, du, dv, dtot, stats);
+  return solve_batch_impl(c, c->wnar.as<int32_t>(), batch, n, seed, dr2c, du, dv, dtot, stats, who,
+                          c->engine, time_budget_s);
+}
+
+int solve_dev_i64(kmb_context* c, const int64_t* dC, int32_t batch, int32_t n, int32_t seed,
+                  double time_budget_s, long long hi, int32_t* dr2c, int64_t* du, int64_t* dv,
+                  int64_t* dtot, kmb_stats* stats, const char* who) {
+  if (hi <= kNarrowMax) {
+    const size_t cnt = static_cast<size_t>(batch) * n * n;
+    KMB_CUDA(c->wnar.ensure(cnt * 4));
+    KMB_CUDA(kmb::launch_convert_i64(dC, n, static_cast<int64_t>(batch) * n, n, false, 1, 1, nullptr,
+                                     c->wnar.as<int32_t>(), nullptr, c->sm_count, c->stream));
+    return solve_narrow_dev(c, batch, n, seed, time_budget_s, dr2c, du, dv, dtot, stats, who);
+  }
+  return solve_wide(c, dC, batch, n, seed, time_budget_s, dr2c, du, dv, dtot, stats, who);
+}
+
+int copy_results(kmb_context* c, int32_t batch, int32_t n, int32_t* r2c, int64_t* u, int64_t* v,
+                 int64_t* tot, const int32_t* dr2c, const int64_t* du, const int64_t* dv,
+                 const int64_t* dtot) {
+  const size_t nb = static_cast<size_t>(batch) * n;
+  int r;
+  if (r2c != dr2c && (r = copy_out(r2c, dr2c, nb * 4, c->stream))) return r;
+  if (u != du && (r = copy_out(u, du, nb * 8, c->stream))) return r;
+  if (v != dv && (r = copy_out(v, dv, nb * 8, c->stream))) return r;
+  if (tot != dtot && (r = copy_out(tot, dtot, static_cast<size_t>(batch) * 8, c->stream))) return r;
+  KMB_CUDA(cudaStreamSynchronize(c->stream));
+  return KMB_OK;
+}
+
+int solve_i64_common(kmb_context* c, const int64_t* costs, int32_t batch, int32_t n, int64_t ld,
+                     int32_t seed, double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
+                     int64_t* total_cost, kmb_stats* stats, const char* who) {
+  if (!c) return fail(KMB_EINVAL, std::string(who) + ": NULL context");
+  if (batch <= 0 || n <= 0) return fail(KMB_EINVAL, std::string(who) + ": dimensions must be positive");
+  if (!costs) return fail(KMB_EINVAL, std::string(who) + ": cost is NULL");
+  if (ld < n) return fail(KMB_EINVAL, std::string(who) + ": ld < n");
+  if (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED) return fail(KMB_EINVAL, std::string(who) + ": bad seed");
+  KMB_CUDA(cudaSetDevice(c->device));
+  const int64_t* dC = nullptr;
+  int r;
+  if ((r = stage_i64(c, costs, static_cast<int64_t>(batch) * n, n, ld, &dC))) return r;
+  long long lo = 0, hi = 0;
+  if ((r = minmax_i64(c, dC, static_cast<int64_t>(batch) * n, n, &lo, &hi))) return r;
+  if (lo < 0) return fail(KMB_ENEGATIVE, std::string(who) + ": costs must be nonnegative");
+  if (hi > headroom_max(n))
+    return fail(KMB_ERANGE, std::string(who) + ": supply * cost magnitude too large for 64-bit arithmetic");
+  if (batch > 1 && hi <= kNarrowMax && n > kmb::big_max_n())
+    return fail(KMB_EINVAL, std::string(who) + ": n > " + std::to_string(kmb::big_max_n()) +
+                                " (use kmb_solve_i64 per instance)");
+  const size_t nb = static_cast<size_t>(batch) * n;
+  int32_t* dr2c;
+  int64_t *du, *dv, *dtot;
+  if ((r = dev_or_ws(row_to_col, c->wr2c, nb, &dr2c)) || (r = dev_or_ws(u, c->wu, nb, &du)) ||
+      (r = dev_or_ws(v, c->wv, nb, &dv)) || (r = dev_or_ws(total_cost, c->wtot, batch, &dtot)))
+    return r;
+  if ((r = solve_dev_i64(c, dC, batch, n, seed, time_budget_s, hi, dr2c, du, dv, dtot, stats, who)))
+    return r;
+  return copy_results(c, batch, n, row_to_col, u, v, total_cost, dr2c, du, dv, dtot);
+}
+
+// K11 on the device (quantize_costs, hungarian.cpp:33-53): N = max cost (hi),
+// chat = floor(C * B / N) into `chat` (device, optional) and, when B < 2^29 so
+// every chat fits the 32-bit engines, also narrowed into c->wnar; lossless
+// flag.  All-zero costs: N = 1, chat = C, lossless.
+int quantize_dev(kmb_context* c, const int64_t* dC, int64_t rows, int32_t cols, long long hi, int64_t B,
+                 int64_t* chat, bool want_narrow, int64_t* N_out, int32_t* lossless_out) {
+  if (B <= 0) return fail(KMB_EINVAL, "quantize_costs: B must be positive");
+  const size_t cnt = static_cast<size_t>(rows) * cols;
+  int64_t N = hi;
+  if (N <= 0) {
+    *N_out = 1;
+    *lossless_out = 1;
+    if (chat) KMB_CUDA(cudaMemcpyAsync(chat, dC, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
+    if (want_narrow) {
+      KMB_CUDA(c->wnar.ensure(cnt * 4));
+      KMB_CUDA(kmb::launch_convert_i64(dC, cols, rows, cols, false, 1, 1, nullptr, c->wnar.as<int32_t>(),
+                                       nullptr, c->sm_count, c->stream));
+    }
+    return KMB_OK;
+  }
+  if (B > INT64_MAX / N) return fail(KMB_EINVAL, "quantize_costs: B * max cost overflows");
+  KMB_CUDA(c->wmm.ensure(32));
+  int32_t* lossy = reinterpret_cast<int32_t*>(c->wmm.as<char>() + 16);
+  KMB_CUDA(cudaMemsetAsync(lossy, 0, 4, c->stream));
+  int32_t* nar = nullptr;
+  if (want_narrow) {
+    KMB_CUDA(c->wnar.ensure(cnt * 4));
+    nar = c->wnar.as<int32_t>();
+  }
+  KMB_CUDA(kmb::launch_convert_i64(dC, cols, rows, cols, true, B, N, chat, nar, lossy, c->sm_count, c->stream));
+  int32_t h = 0;
+  KMB_CUDA(cudaMemcpyAsync(&h, lossy, 4, cudaMemcpyDeviceToHost, c->stream));
+  KMB_CUDA(cudaStreamSynchronize(c->stream));
+  *N_out = N;
+  *lossless_out = h ? 0 : 1;
+  return KMB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kmb_solve_i64(kmb_context* c, const int64_t* cost, int32_t n, int64_t ld, int32_t seed,
+                  double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
+                  int64_t* total_cost, kmb_stats* stats) {
+  return solve_i64_common(c, cost, 1, n, ld, seed, time_budget_s, row_to_col, u, v, total_cost, stats,
+                          "kmb_solve_i64");
+}
+
+int kmb_solve_batch_i64(kmb_context* c, const int64_t* costs, int32_t batch, int32_t n, int32_t seed,
+                        int32_t* row_to_col, int64_t* u, int64_t* v, int64_t* total_cost,
+                        kmb_stats* stats) {
+  return solve_i64_common(c, costs, batch, n, n, seed, 0.0, row_to_col, u, v, total_cost, stats,
+                          "kmb_solve_batch_i64");
+}
+
+int kmb_quantize_i64(kmb_context* c, const int64_t* cost, int64_t count, int64_t B, int64_t* chat,
+                     int64_t* N, int32_t* lossless) {
+  if (!c) return fail(KMB_EINVAL, "kmb_quantize_i64: NULL context");
+  if (count < 0 || (count > 0 && !cost)) return fail(KMB_EINVAL, "kmb_quantize_i64: bad arguments");
+  if (B <= 0) return fail(KMB_EINVAL, "quantize_costs: B must be positive");
+  if (count == 0) {
+    if (N) *N = 1;
+    if (lossless) *lossless = 1;
+    return KMB_OK;
+  }
+  KMB_CUDA(cudaSetDevice(c->device));
+  const int64_t* dC = nullptr;
+  int r;
+  if ((r = stage_i64(c, cost, count, 1, 1, &dC))) return r;
+  long long lo = 0, hi = 0;
+  if ((r = minmax_i64(c, dC, count, 1, &lo, &hi))) return r;
+  int64_t* dchat = nullptr;
+  if ((r = dev_or_ws(chat, c->wchat, static_cast<size_t>(count), &dchat))) return r;
+  int64_t n_out = 1;
+  int32_t ll = 1;
+  if ((r = quantize_dev(c, dC, count, 1, hi, B, dchat, false, &n_out, &ll))) return r;
+  if (chat && chat != dchat) {
+    KMB_CUDA(cudaMemcpyAsync(chat, dchat, static_cast<size_t>(count) * 8, cudaMemcpyDeviceToHost, c->stream));
+    KMB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  if (N) *N = n_out;
+  if (lossless) *lossless = ll;
+  return KMB_OK;
+}
+
+int kmb_solve_batched_km_i64(kmb_context* c, const int64_t* cost, int32_t n, int64_t B,
+                             double time_budget_s, int32_t* row_to_col, int64_t* u, int64_t* v,
+                             int64_t* total_cost, int64_t* chat, int64_t* N, int32_t* lossless,
+                             kmb_stats* stats) {
+  const char* who = "solve_batched_km";
+  if (!c) return fail(KMB_EINVAL, "kmb_solve_batched_km_i64: NULL context");
+  if (n <= 0) return fail(KMB_EINVAL, std::string(who) + ": dimensions must be positive");
+  if (!cost) return fail(KMB_EINVAL, "kmb_solve_batched_km_i64: cost is NULL");
+  KMB_CUDA(cudaSetDevice(c->device));
+  const int64_t* dC = nullptr;
+  int r;
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  if ((r = stage_i64(c, cost, n, n, n, &dC))) return r;
+  long long lo = 0, hi = 0;
+  if ((r = minmax_i64(c, dC, n, n, &lo, &hi))) return r;
+  // require_unit_square (hungarian.cpp:15-21) before quantize_costs (:318)
+  if (lo < 0) return fail(KMB_ENEGATIVE, std::string(who) + ": costs must be nonnegative");
+  if (hi > headroom_max(n))
+    return fail(KMB_ERANGE, std::string(who) + ": supply * cost magnitude too large for 64-bit arithmetic");
+  const size_t nb = static_cast<size_t>(n);
+  int32_t* dr2c;
+  int64_t *du, *dv, *dtot;
+  if ((r = dev_or_ws(row_to_col, c->wr2c, nb, &dr2c)) || (r = dev_or_ws(u, c->wu, nb, &du)) ||
+      (r = dev_or_ws(v, c->wv, nb, &dv)) || (r = dev_or_ws(total_cost, c->wtot, 1, &dtot)))
+    return r;
+  // B a multiple of N (the lossless B = N * n among them): chat = k * C exactly
+  // and the search is scale-equivariant (every reduced cost, slack and dual
+  // step scales by k, ties stay ties), so C is solved and the duals scaled.
+  const int64_t k = (hi > 0 && B > 0 && B % hi == 0) ? B / hi : 0;
+  int64_t n_q = 1;
+  int32_t ll = 1;
+  int64_t* dchat = nullptr;
+  const bool need_chat = chat != nullptr || (k == 0 && hi > 0 && B > kNarrowMax);
+  if (need_chat && (r = dev_or_ws(chat, c->wchat, static_cast<size_t>(nn), &dchat))) return r;
+  if (k > 0 || hi <= 0) {
+    if ((r = quantize_dev(c, dC, n, n, hi, B, dchat, false, &n_q, &ll))) return r;
+    if ((r = solve_dev_i64(c, dC, 1, n, KMB_SEED_BATCHED, time_budget_s, hi, dr2c, du, dv, dtot, stats, who)))
+      return r;
+    if (k > 1) {
+      KMB_CUDA(kmb::launch_scale_i64(du, n, k, c->sm_count, c->stream));
+      KMB_CUDA(kmb::launch_scale_i64(dv, n, k, c->sm_count, c->stream));
+    }
+  } else {
+    // every chat <= B: the 32-bit engines take it when B < 2^29
+    const bool narrow = B <= kNarrowMax;
+    if (!narrow && B > kWideMax)
+      return fail(KMB_ERANGE, std::string(who) + ": quantized cost exceeds the device range [0, 2^60]");
+    if ((r = quantize_dev(c, dC, n, n, hi, B, dchat, narrow, &n_q, &ll))) return r;
+    if (narrow)
+      r = solve_narrow_dev(c, 1, n, KMB_SEED_BATCHED, time_budget_s, dr2c, du, dv, dtot, stats, who);
+    else
+      r = solve_wide(c, dchat, 1, n, KMB_SEED_BATCHED, time_budget_s, dr2c, du, dv, dtot, stats, who);
+    if (r) return r;
+  }
+  // the objective on the caller's costs (make_result, core.cpp:76-90)
+  KMB_CUDA(kmb::launch_total_i64(dC, n, nn, 1, n, dr2c, dtot, c->sm_count, c->stream));
+  if (chat && chat != dchat) KMB_CUDA(cudaMemcpyAsync(chat, dchat, nn * 8, cudaMemcpyDeviceToHost, c->stream));
+  if ((r = copy_results(c, 1, n, row_to_col, u, v, total_cost, dr2c, du, dv, dtot))) return r;
+  if (N) *N = n_q;
+  if (lossless) *lossless = ll;
   return KMB_OK;
 }
 

@@ -179,3 +179,35 @@ cudaStream_t context_stream(kmb_context* c);
 int context_device(kmb_context* c);
 void set_last_error(const std::string& msg);
 }  // namespace kmb
+
+namespace kmb {
+// ---- 64-bit cost path (kmb_wide.cu) ------------------------------------------
+struct WideArgs {
+  const int64_t* C;     // batch instances, row stride ld, instance stride inst_stride
+  int64_t ld, inst_stride;
+  int32_t batch, n, seed;
+  int64_t deadline_ns;  // per-instance time budget (0: none)
+  int32_t* row_to_col;  // batch x n
+  int64_t* u;           // batch x n
+  int64_t* v;           // batch x n
+  int64_t* total_cost;  // batch
+  int64_t* stats;       // batch x KMB_ISTATS (may be null)
+  int32_t* status;      // batch
+  int32_t* converged;   // batch (may be null)
+  int64_t* ws64;        // wide_ws64_bytes(n, slots)
+  int32_t* ws32;        // wide_ws32_bytes(n, slots)
+  int64_t max_cost;     // an instance with a larger cost fails with status 3
+};
+int wide_slots(int batch, int sm_count);
+size_t wide_ws64_bytes(int n, int slots);
+size_t wide_ws32_bytes(int n, int slots);
+cudaError_t launch_wide(const WideArgs& a, int slots, cudaStream_t st);
+cudaError_t launch_minmax_i64(const int64_t* C, int64_t ld, int64_t rows, int32_t cols, long long* out,
+                              int sm_count, cudaStream_t st);
+cudaError_t launch_convert_i64(const int64_t* C, int64_t ld, int64_t rows, int32_t cols, bool quantize,
+                               int64_t B, int64_t N, int64_t* chat, int32_t* narrow, int32_t* lossy,
+                               int sm_count, cudaStream_t st);
+cudaError_t launch_scale_i64(int64_t* x, int64_t count, int64_t k, int sm_count, cudaStream_t st);
+cudaError_t launch_total_i64(const int64_t* C, int64_t ld, int64_t inst_stride, int32_t batch, int32_t n,
+                             const int32_t* r2c, int64_t* total, int sm_count, cudaStream_t st);
+}  // namespace kmb

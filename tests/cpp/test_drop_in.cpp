@@ -193,6 +193,46 @@ int main() {
     CHECK(a.objective == b.objective);
     CHECK(d1.u == d2.u && d1.v == d2.v);
   }
+  {  // the reference's whole int64 range: costs up to validate_instance's headroom
+     // (core.cpp:47-53) through the wide engine; duals and objective identical
+    std::mt19937_64 rng(97);
+    for (int32_t n : {2, 17, 64}) {
+      const int64_t head = ((int64_t{1} << 62) / n) / (2 * static_cast<int64_t>(n) + 2);
+      OTInstance inst;
+      inst.n = inst.m = n;
+      inst.supplies.assign(n, 1);
+      inst.demands.assign(n, 1);
+      inst.cost.resize(static_cast<size_t>(n) * n);
+      for (int64_t& x : inst.cost) x = static_cast<int64_t>(rng() % static_cast<uint64_t>(head));
+      inst.cost[0] = head;
+      DualPotentials d1, d2;
+      const SolveResult a = solve_km_b200(inst, &d1);
+      const SolveResult b = solve_km(inst, &d2);
+      CHECK(a.objective == b.objective && d1.u == d2.u && d1.v == d2.v);
+      // lossless B = N through the device quantization: the wide engine's duals
+      DualPotentials e0, f0;
+      BatchedKMConfig c0;
+      c0.B = head;
+      const SolveResult g = solve_batched_km_b200(inst, c0, &e0);
+      const SolveResult h = solve_batched_km(inst, c0, &f0);
+      CHECK(g.exact && h.exact && g.objective == h.objective && e0.u == f0.u && e0.v == f0.v);
+      for (int64_t& x : inst.cost) x = static_cast<int64_t>(rng() % 1000000);
+      DualPotentials e1, e2;
+      QuantizedCosts q1, q2;
+      BatchedKMConfig cfg;
+      cfg.B = 3000000007;  // lossy, chat beyond the 32-bit engines' range
+      const SolveResult c = solve_batched_km_b200(inst, cfg, &e1, &q1);
+      const SolveResult d = solve_batched_km(inst, cfg, &e2, &q2);
+      CHECK(e1.u == e2.u && e1.v == e2.v && q1.chat == q2.chat && q1.N == q2.N);
+      CHECK(q1.lossless == q2.lossless && c.exact == d.exact);
+    }
+    OTInstance big = unit_2x2();
+    big.cost[0] = int64_t{1} << 61;  // beyond the headroom: the reference's message
+    std::string a, b;
+    try { solve_km_b200(big); } catch (const std::invalid_argument& e) { a = e.what(); }
+    try { solve_km(big); } catch (const std::invalid_argument& e) { b = e.what(); }
+    CHECK(!a.empty() && a == b);
+  }
   // ---- auction (test_auction.cpp cases; bit-identical prices vs the reference)
   auto same_bits = [](const std::vector<double>& a, const std::vector<double>& b) {
     if (a.size() != b.size()) return false;
