@@ -361,7 +361,23 @@ def extras_c5(solver, hbm_peak: float) -> dict:
             "note": "bytes the scans read (4n per relaxed row, 16 B per dirty row-segment, "
                     "2 reduction passes) / solve time; 15.5k dependent rounds bound it "
                     "(profiles/r02_ncu_solvers.json)"}
+    # the column-sharded engine with the exchange on the device (k_solve_sharded),
+    # its ranks as CTA groups of one launch on this GPU: what sharding costs in
+    # replicated stores and system-scope barriers at the same CTA count
+    sharded = {}
+    for R in (1, 2, 4):
+        try:
+            rs = [solver.solve_sharded_local(dc, R) for _ in range(2)]
+            rr = rs[-1]
+            sharded[f"ranks_{R}"] = {
+                "solve_ms": 1e3 * min(x.stats["seconds"] for x in rs),
+                "rounds": rr.stats["rounds"],
+                "matches_golden": (rr.total_cost == g.get("total_cost") and Wk.fnv1a64(rr.u) == g.get("u_fnv")
+                                   and Wk.fnv1a64(rr.v) == g.get("v_fnv")) if g else None}
+        except Exception as e:  # reported, never silently dropped
+            sharded[f"ranks_{R}"] = {"error": repr(e)}
     return {"workload": "c5: n=16384 U{0..1e6}, 1 GiB int32, single GPU", "engine": "grid",
+            "sharded_device_exchange": sharded,
             "solve_ms": 1e3 * t, "solves_per_s": 1.0 / t, "phases": st.phases,
             "dual_steps": st.dual_steps, "rows_scanned": st.rows_scanned, "rounds": st.rounds,
             "segment_rows": st.segment_rows, "matches_golden": ok,

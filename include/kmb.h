@@ -73,8 +73,10 @@ enum kmb_option {
                                5 cluster (grid engine on one <=16-CTA cluster),
                                6 CTA (n <= 256),
                                8 single-CTA (one 512-thread CTA, n <= 4096);
-                               stats->engine 7 = column-sharded, 9 = wide
-                               (int64 costs, kmb_solve_i64)                   */
+                               stats->engine 7 = column-sharded (host
+                               exchange), 9 = wide (int64 costs,
+                               kmb_solve_i64), 10 = column-sharded (device
+                               exchange)                                       */
   KMB_OPT_WARPS_PER_SM = 4, /* warp engine: resident instances per SM (0 = max);
                                bounds the L2 working set of streamed matrices   */
   /* 5 (the 16-bit warp-engine mode of ABI 1) was removed: slower */
@@ -208,6 +210,32 @@ int kmb_shard_init_callbacks(kmb_context* ctx, int32_t nranks, int32_t rank,
 int kmb_solve_sharded_i32(kmb_context* ctx, const int32_t* slab, int32_t n, int64_t ld,
                           int32_t col_begin, int32_t ncols, int32_t seed, int32_t* row_to_col,
                           int64_t* u, int64_t* v_slab, int64_t* total_cost, kmb_stats* stats);
+
+/* ---- column-sharded single instance, exchange on the device ---------------
+ * The same column sharding with no host round trip per round: one persistent
+ * kernel per rank (the grid engine with its row-side state replicated on every
+ * rank); per round each rank stores its min-slack partial and its appended
+ * rows / free columns into every rank's replica (peer stores over NVLink) and
+ * the ranks meet at a system-scope counting barrier in rank 0's memory.
+ * Collective setup: every rank calls kmb_shard_dev_open (allocates its window
+ * and returns its 64-byte CUDA IPC handle and the slab width: rank r holds
+ * columns [r * slab_cols, min(n, (r + 1) * slab_cols))), the caller allgathers
+ * the handles, every rank calls kmb_shard_dev_connect, then
+ * kmb_solve_sharded_dev_i32 collectively (kmb_shard_init_* must be set up too:
+ * two host barriers per solve order rank 0's reset of its control block).
+ * Outputs as kmb_solve_sharded_i32; stats->engine 10.
+ * kmb_solve_sharded_local_i32 runs the same kernel with `nranks` ranks as CTA
+ * groups of one launch on this context's GPU (replicas side by side; checked
+ * equal after the solve): the protocol on a one-GPU box, whole matrix in. */
+int kmb_shard_dev_open(kmb_context* ctx, int32_t n, int32_t nranks, int32_t rank, int32_t* slab_cols,
+                       uint8_t* handle64);
+int kmb_shard_dev_connect(kmb_context* ctx, const uint8_t* handles64);
+int kmb_solve_sharded_dev_i32(kmb_context* ctx, const int32_t* slab, int32_t n, int64_t ld,
+                              int32_t col_begin, int32_t ncols, int32_t seed, int32_t* row_to_col,
+                              int64_t* u, int64_t* v_slab, int64_t* total_cost, kmb_stats* stats);
+int kmb_solve_sharded_local_i32(kmb_context* ctx, const int32_t* cost, int32_t n, int64_t ld,
+                                int32_t nranks, int32_t seed, int32_t* row_to_col, int64_t* u,
+                                int64_t* v, int64_t* total_cost, kmb_stats* stats);
 
 /* ---- auction (the reference's other unit-capacity solver, auction.hpp) ---
  * Gauss-Seidel auction, bit-identical to ot::solve_auction (scaled = 0,

@@ -34,7 +34,9 @@ ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", 
                "kmb_shard_init_callbacks", "kmb_solve_sharded_i32", "kmb_bench_scan",
                "kmb_last_instance_stats", "kmb_costs_from_points", "kmb_auction_i32",
                "kmb_solve_i64", "kmb_solve_batch_i64", "kmb_quantize_i64",
-               "kmb_solve_batched_km_i64", "kmb_last_error", "kmb_abi_version")
+               "kmb_solve_batched_km_i64", "kmb_shard_dev_open", "kmb_shard_dev_connect",
+               "kmb_solve_sharded_dev_i32", "kmb_solve_sharded_local_i32",
+               "kmb_last_error", "kmb_abi_version")
 
 
 class KmbUnavailable(RuntimeError):
@@ -100,6 +102,12 @@ def load_library(path: str | None = None):
         lib.kmb_solve_batched_km_i64.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_double, vp, vp, vp,
                                                  vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
                                                  C.POINTER(Stats)]
+        lib.kmb_shard_dev_open.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), vp]
+        lib.kmb_shard_dev_connect.argtypes = [vp, vp]
+        lib.kmb_solve_sharded_dev_i32.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                                  C.c_int32, vp, vp, vp, vp, C.POINTER(Stats)]
+        lib.kmb_solve_sharded_local_i32.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                                    vp, vp, vp, vp, C.POINTER(Stats)]
         lib.kmb_last_error.restype = C.c_char_p
         lib.kmb_abi_version.restype = C.c_int
         _lib = lib
@@ -235,6 +243,25 @@ class Solver:
             C.c_void_p(_ptr(u)), C.c_void_p(_ptr(v)), C.c_void_p(_ptr(total_cost)),
             C.c_void_p(_ptr(chat)), C.byref(N), C.byref(ll), C.byref(st)))
         return st, int(N.value), bool(ll.value)
+
+    def solve_sharded_local(self, cost, nranks: int, seed: int = KMB_SEED_BATCHED):
+        """``kmb_solve_sharded_local_i32``: the device-exchange column-sharded
+        engine with ``nranks`` ranks as CTA groups of one launch on this GPU
+        (replicas checked equal after the solve).  numpy or torch input."""
+        n = cost.shape[0]
+        r2c = np.full(n, -1, np.int32)
+        u = np.zeros(n, np.int64)
+        v = np.zeros(n, np.int64)
+        tot = np.zeros(1, np.int64)
+        st = Stats()
+        if not hasattr(cost, "data_ptr"):
+            cost = np.ascontiguousarray(cost, dtype=np.int32)
+        self._check(self._lib.kmb_solve_sharded_local_i32(
+            self._h, C.c_void_p(_ptr(cost)), n, n, nranks, seed, C.c_void_p(r2c.ctypes.data),
+            C.c_void_p(u.ctypes.data), C.c_void_p(v.ctypes.data), C.c_void_p(tot.ctypes.data),
+            C.byref(st)))
+        return Result(r2c, u, v, int(tot[0]), iterations=int(st.phases + st.dual_steps),
+                      stats=_stats_dict(st))
 
     def solve_batch_async(self, costs, batch: int, n: int, seed: int, row_to_col, u, v,
                           total_cost, status) -> None:

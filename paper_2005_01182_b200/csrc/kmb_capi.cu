@@ -97,6 +97,8 @@ struct kmb_context {
   int64_t* hsum = nullptr;
   // column-sharded solve: the collective (NCCL or caller callbacks)
   std::unique_ptr<kmb::Exchange> exchange;
+  // device-resident column-sharded solve (replicas, IPC mappings)
+  kmb::ShardDevPtr shard_dev;
   // chunked host-input pipeline of the batch engines
   static constexpr int kAux = 4, kMaxChunks = 64;
   cudaStream_t aux[kAux] = {};
@@ -107,6 +109,8 @@ struct kmb_context {
 
 namespace kmb {
 std::unique_ptr<Exchange>& context_exchange(kmb_context* c) { return c->exchange; }
+ShardDevPtr& context_shard_dev(kmb_context* c) { return c->shard_dev; }
+int context_sm_count(kmb_context* c) { return c->sm_count; }
 cudaStream_t context_stream(kmb_context* c) { return c->stream; }
 int context_device(kmb_context* c) { return c->device; }
 void set_last_error(const std::string& msg) { g_err = msg; }
@@ -144,6 +148,7 @@ int kmb_create(int device, kmb_context** out) {
 void kmb_destroy(kmb_context* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  c->shard_dev.reset();
   for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
                     &c->obj, &c->bcost, &c->bpad, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,

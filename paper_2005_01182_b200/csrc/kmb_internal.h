@@ -39,6 +39,23 @@ struct Ctrl {
   // counting grid barrier (grid engine): per barrier k % 3, arrivals in bits
   // 0-15, row appends in 16-39, free-column appends in 40-63
   unsigned long long cbar[3];
+  unsigned long long obj;  // column-sharded engine: the objective, summed over the slabs
+};
+
+// ---- column-sharded engine with device-side exchange (k_solve_sharded) --------
+// R ranks (GPUs, or CTA groups of one launch when emulated on one GPU), Gr
+// CTAs each; rank r holds the columns [r*Gr*W, (r+1)*Gr*W) as an n x Gr*W slab
+// and a replica of the row-side state; claims, counters, the barrier word and
+// the cross-rank row minima live in rank 0's home block.  Lives in device
+// memory (the kernel reads it through a pointer).
+constexpr int KMB_MAX_RANKS = 8;
+struct ShardDevArgs {
+  int32_t R, rank_base, Gr, pad_;
+  int64_t slab_pitch;
+  const int32_t* slab[KMB_MAX_RANKS];  // rank r's cost slab (its own HBM)
+  unsigned char* rep[KMB_MAX_RANKS];   // replica bases (peer-mapped for other GPUs)
+  int64_t* vout[KMB_MAX_RANKS];        // rank r's v, slab-local columns
+  int32_t* rowmin;                     // home: R x n slab row minima
 };
 
 struct SolverArgs {
@@ -71,6 +88,8 @@ cudaError_t launch_objective(const int32_t* C, int64_t pitch, int n, const int32
 size_t solver_smem_bytes(int W);
 cudaError_t launch_scan_all(const SolverArgs& a, int G, uint64_t* keys_out, cudaStream_t st);
 int solver_threads();
+size_t shard_rep_bytes(int n, int G);  // one replica of the row side (G = CTAs over all ranks)
+cudaError_t launch_solver_sharded(const SolverArgs& a, const ShardDevArgs* sh_dev, int grid, cudaStream_t st);
 
 // ---- batched small instances (one CTA per instance, costs from L2) ----
 struct BatchArgs {
@@ -173,8 +192,17 @@ struct CallbackExchange : Exchange {
   int allreduce_min(int64_t* p, int32_t count) override { return ar(p, count, user); }
   int allgather(const void* s, int64_t bytes, void* r) override { return ag(s, bytes, r, user); }
 };
+// device-resident column-sharded solve (kmb_shard_dev.cu): per-context state
+struct ShardDevState;
+void destroy_shard_dev(ShardDevState* p);
+struct ShardDevDeleter {
+  void operator()(ShardDevState* p) const { destroy_shard_dev(p); }
+};
+using ShardDevPtr = std::unique_ptr<ShardDevState, ShardDevDeleter>;
 // context accessors (the context struct lives in kmb_capi.cu)
 std::unique_ptr<Exchange>& context_exchange(kmb_context* c);
+ShardDevPtr& context_shard_dev(kmb_context* c);
+int context_sm_count(kmb_context* c);
 cudaStream_t context_stream(kmb_context* c);
 int context_device(kmb_context* c);
 void set_last_error(const std::string& msg);

@@ -148,6 +148,66 @@ struct DMem {
   __device__ static T ld(const T* p) { return *reinterpret_cast<const volatile T*>(p); }
 };
 
+// RMem: the column-sharded engine's replicated row side (k_solve_sharded,
+// DESIGN.md §5).  Rank r's CTAs own a slab of the columns and read rank r's
+// replica of the row-side state; every write goes to every replica (P2P
+// stores over NVLink when the ranks are GPUs, plain stores when they are CTA
+// groups of one launch), so the barrier after it publishes it everywhere.
+// Tree claims and the append counters live in the home block (rank 0) and are
+// updated with atomics there.  Replica layout (shard_rep_bytes): int64 u[n],
+// list_w[2][n], partial[G]; then int32 root_row, match_row, match_col,
+// tree_par, list_row[2], found (n each).
+template <class T>
+struct RRef {
+  unsigned char* const* bases;  // the R replica bases (shared memory)
+  const unsigned char* mine;
+  size_t off;
+  int R;
+  __device__ const RRef& operator*() const { return *this; }
+  __device__ void operator=(T v) const {
+    for (int r = 0; r < R; ++r) *reinterpret_cast<T*>(bases[r] + off) = v;
+  }
+  __device__ T load() const { return ldcg(reinterpret_cast<const T*>(mine + off)); }
+  __device__ T* local() const { return reinterpret_cast<T*>(const_cast<unsigned char*>(mine) + off); }
+};
+
+__host__ __device__ inline size_t shard_rep_o32(int n, int G) {
+  return (8ull * (3ull * n + G) + 15) & ~static_cast<size_t>(15);
+}
+
+struct RMem {
+  unsigned char* const* bases;
+  const unsigned char* mine;
+  int R, n;
+  size_t o32;
+  Ctrl* ctrl;          // home
+  uint64_t* claim_h;   // home
+  template <class T>
+  __device__ RRef<T> ref(size_t off) const { return RRef<T>{bases, mine, off, R}; }
+  __device__ RRef<int64_t> u(int i) const { return ref<int64_t>(8ull * i); }
+  __device__ RRef<int64_t> list_w(int p, int i) const { return ref<int64_t>(8ull * ((1ull + p) * n + i)); }
+  __device__ RRef<int64_t> partial(int b) const { return ref<int64_t>(8ull * (3ull * n + b)); }
+  __device__ RRef<int32_t> a32(int k, int i) const { return ref<int32_t>(o32 + 4ull * (static_cast<size_t>(k) * n + i)); }
+  __device__ RRef<int32_t> root_row(int i) const { return a32(0, i); }
+  __device__ RRef<int32_t> match_row(int i) const { return a32(1, i); }
+  __device__ RRef<int32_t> match_col(int i) const { return a32(2, i); }
+  __device__ RRef<int32_t> tree_par(int i) const { return a32(3, i); }
+  __device__ RRef<int32_t> list_row(int p, int i) const { return a32(4 + p, i); }
+  __device__ RRef<int32_t> found(int i) const { return a32(6, i); }
+  __device__ uint64_t* claim(int i) const { return claim_h + i; }
+  __device__ int* rcnt(int k) const { return &ctrl->rcnt[k]; }
+  __device__ int* fcnt(int k) const { return &ctrl->fcnt[k]; }
+  template <class T>
+  __device__ static T ld(const RRef<T>& r) { return r.load(); }
+  template <class T>
+  __device__ static T ld(const T* p) { return ldcg(p); }
+  __device__ static uint64_t ckey(int ep, int col) { return claim_key(ep, col); }
+  __device__ static bool claimed(uint64_t c, int ep) { return claimed_in(c, ep); }
+  __device__ void claim_min(int root, uint64_t k) const {
+    atomicMin(reinterpret_cast<unsigned long long*>(claim_h + root), static_cast<unsigned long long>(k));
+  }
+};
+
 // dynamic shared memory of the slab state (keys, v, Dc, reached, dirty segments)
 __host__ __device__ inline size_t solver_smem_bytes_dev(int W) {
   return (static_cast<size_t>(W) * (8 + 8 + 8 + 1 + 1) + 16 + 15) & ~static_cast<size_t>(15);
@@ -208,8 +268,8 @@ __global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
 // is a power of two, lanes sharing a segment differ only in their high lane
 // bits (S < 32) and a xor-shuffle tree merges them before the shared atomics.
 template <class Mem, int kRelaxBatch = kSolveBatch>
-__device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, int p, int head,
-                                           int tail, int c0, int W, uint64_t* skey) {
+__device__ __forceinline__ void relax_slab(const int32_t* C, int64_t pitch, const Mem& M, int p,
+                                           int head, int tail, int c0, int W, uint64_t* skey) {
   const int S = W >> 2;
   const int R = kThreads / S > 0 ? kThreads / S : 1;
   const int tid = threadIdx.x;
@@ -220,7 +280,7 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, in
     const int g = tid / Sreal;
     uint64_t best0 = KMB_KEY_INF, best1 = KMB_KEY_INF, best2 = KMB_KEY_INF, best3 = KMB_KEY_INF;
     if (g < R) {
-      const int32_t* base = a.C + c0 + 4 * s;
+      const int32_t* base = C + c0 + 4 * s;
       int r = head + g;
       // kRelaxBatch rows in flight per thread: all list/tag loads, then all
       // 128-bit cost loads, then the folds
@@ -236,7 +296,7 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, in
         }
 #pragma unroll
         for (int k = 0; k < kRelaxBatch; ++k) {
-          c[k] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[k]) * a.pitch));
+          c[k] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[k]) * pitch));
           b[k] = row_bias(M.ld(M.u(i[k])) - dr[k]);  // w = u - D at reach
         }
 #pragma unroll
@@ -250,7 +310,7 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, in
       for (; r < tail; r += R) {
         const int i = M.ld(M.list_row(p, r));
         const int64_t drr = M.ld(M.list_w(p, r));
-        const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * a.pitch));
+        const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * pitch));
         const uint32_t b = row_bias(M.ld(M.u(i)) - drr);
         best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
         best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
@@ -292,8 +352,8 @@ __device__ __forceinline__ void relax_slab(const SolverArgs& a, const Mem& M, in
 // group g, with k in [0, np2), np2 = nd rounded up to a power of two (lanes of
 // the same k differ only in high lane bits, so a xor tree merges them).
 template <class Mem>
-__device__ __forceinline__ void relax_sel(const SolverArgs& a, const Mem& M, int p, int head,
-                                          int tail, int c0, const int32_t* segs, int nd,
+__device__ __forceinline__ void relax_sel(const int32_t* C, int64_t pitch, const Mem& M, int p,
+                                          int head, int tail, int c0, const int32_t* segs, int nd,
                                           uint64_t* skey) {
   int np2 = 1;
   while (np2 < nd) np2 <<= 1;
@@ -303,7 +363,7 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const Mem& M, int
   uint64_t best0 = KMB_KEY_INF, best1 = KMB_KEY_INF, best2 = KMB_KEY_INF, best3 = KMB_KEY_INF;
   const int sg = k < nd ? segs[k] : 0;
   if (k < nd) {
-    const int32_t* base = a.C + c0 + 4 * sg;
+    const int32_t* base = C + c0 + 4 * sg;
     int r = head + g;
     for (; r + (kRelaxBatch - 1) * R < tail; r += kRelaxBatch * R) {
       int i[kRelaxBatch];
@@ -317,7 +377,7 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const Mem& M, int
       }
 #pragma unroll
       for (int q = 0; q < kRelaxBatch; ++q) {
-        c[q] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[q]) * a.pitch));
+        c[q] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[q]) * pitch));
         b[q] = row_bias(M.ld(M.u(i[q])) - dr[q]);
       }
 #pragma unroll
@@ -331,7 +391,7 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const Mem& M, int
     for (; r < tail; r += R) {
       const int i = M.ld(M.list_row(p, r));
       const int64_t drr = M.ld(M.list_w(p, r));
-      const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * a.pitch));
+      const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * pitch));
       const uint32_t b = row_bias(M.ld(M.u(i)) - drr);
       best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
       best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
@@ -365,8 +425,9 @@ __device__ __forceinline__ void relax_sel(const SolverArgs& a, const Mem& M, int
 // the reset ("dirty") columns only — the rows appended in the epoch's last round
 // having been relaxed over the whole slab first — and the search goes on at the
 // same D.
-template <class Barrier, bool DSM>
-__global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
+template <class Barrier, int MK>  // MK: 0 GMem, 1 DMem, 2 RMem (column-sharded ranks)
+__device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevArgs* sh) {
+  constexpr bool DSM = MK == 1, RS = MK == 2;
   extern __shared__ __align__(16) unsigned char dyn[];
   const int W = a.W;
   uint64_t* skey = reinterpret_cast<uint64_t*>(dyn);
@@ -377,15 +438,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   __shared__ SlabSmem sm;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int G = gridDim.x;
-  const int c0 = blockIdx.x * W;
-  const bool leader = (blockIdx.x == 0 && tid == 0);
+  // column-sharded ranks (RS): this launch holds ranks rank_base, ... (gridDim.x /
+  // Gr of them); gb is the CTA's index over all ranks' CTAs, G their count
+  const int Gr = RS ? sh->Gr : 1;
+  const int grank = RS ? sh->rank_base + static_cast<int>(blockIdx.x) / Gr : 0;
+  const int lbr = RS ? static_cast<int>(blockIdx.x) % Gr : 0;
+  const int gb = RS ? grank * Gr + lbr : static_cast<int>(blockIdx.x);
+  const int G = RS ? sh->R * Gr : static_cast<int>(gridDim.x);
+  const int c0 = gb * W;                     // the slab's first column
+  const int cl0 = RS ? lbr * W : c0;         // ... in the cost block this rank holds
+  const int32_t* const Cb = RS ? sh->slab[grank] : a.C;
+  const int64_t pitch = RS ? sh->slab_pitch : a.pitch;
+  const bool leader = (gb == 0 && tid == 0);
   Barrier bar = Barrier::make(&a.ctrl->bar_counter, static_cast<unsigned>(G));
   Ctrl* ctrl = a.ctrl;
-  const int gtid = blockIdx.x * kThreads + tid;
+  const int gtid = gb * kThreads + tid;
   const int gthreads = G * kThreads;
 
-  using Mem = std::conditional_t<DSM, DMem, GMem>;
+  using Mem = std::conditional_t<DSM, DMem, std::conditional_t<RS, RMem, GMem>>;
   Mem M;
   if constexpr (DSM) {  // carve the distributed arrays, copy k_init_rows' state in
     const int L = (a.n + G - 1) / G;
@@ -423,10 +493,109 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     }
     if (tid < 6) M.cnt[tid] = 0;
     bar.sync();  // every CTA's copy in place before any remote access
+  } else if constexpr (RS) {
+    __shared__ unsigned char* rbases[KMB_MAX_RANKS];
+    if (tid < sh->R) rbases[tid] = sh->rep[tid];
+    __syncthreads();
+    M.bases = rbases;
+    M.mine = rbases[grank];
+    M.R = sh->R;
+    M.n = a.n;
+    M.o32 = shard_rep_o32(a.n, G);
+    M.ctrl = ctrl;
+    M.claim_h = a.claim;
   } else {
     M.a = &a;
   }
 
+  if constexpr (RS) {
+    // K1 over the rank's slab (k_init_rows for one rank): validation and the
+    // row minima of this rank's columns, combined over the ranks through the
+    // home block; each rank initialises its own replica
+    const int wl = lbr * (kThreads / 32) + wid, nwl = Gr * (kThreads / 32);
+    const int ncl = min(Gr * W, a.n - grank * Gr * W);  // this rank's real columns
+    for (int i = wl; i < a.n; i += nwl) {
+      int32_t lo = 0x7fffffff, hi = 0;
+      const int32_t* row = Cb + static_cast<int64_t>(i) * pitch;
+      for (int j = lane; j < ncl; j += 32) {
+        const int32_t x = __ldg(row + j);
+        lo = min(lo, x);
+        hi = max(hi, x);
+      }
+      lo = __reduce_min_sync(0xffffffffu, lo);
+      hi = __reduce_max_sync(0xffffffffu, hi);
+      if (lane == 0) {
+        if (lo < 0) atomicMax(&ctrl->status, 2);               // KMB_ENEGATIVE
+        else if (hi >= (1 << 29)) atomicMax(&ctrl->status, 3);  // KMB_ERANGE
+        sh->rowmin[static_cast<int64_t>(grank) * a.n + i] = lo;
+        *M.list_row(0, i).local() = i;
+        *M.list_w(0, i).local() = 0;
+        *M.root_row(i).local() = i;
+        *M.match_row(i).local() = -1;
+        *M.match_col(i).local() = -1;
+        if (grank == 0) a.claim[i] = KMB_KEY_INF;
+      }
+    }
+  }
+  if (tid == 0) {
+    sm.my_rows = sm.my_frees = 0;
+    sm.tot_rows = sm.tot_frees = 0;
+  }
+  // Shared append counters are triple-buffered by barrier index: appends made
+  // between barriers k-1 and k go to cnt[k % 3], every CTA reads it right after
+  // barrier k, and the leader clears cnt[(k+2) % 3] after barrier k (last read
+  // after barrier k-1, next used after barrier k+1), so a fast CTA's appends
+  // never race a slow CTA's read.
+  int kb = 0;
+  // Grid engine: the barrier word also carries the append totals (each CTA
+  // adds 1 | rows << 16 | frees << 40), so nobody re-reads the counters after
+  // it — one L2 round trip less per barrier.  Other engines read the counters.
+  // The sharded engine's ranks may be GPUs: system-scope release / acquire.
+  constexpr bool kCounted = std::is_same_v<Barrier, GridBarrier> && !DSM;
+  auto gsync = [&]() {
+    if constexpr (kCounted) {
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long* w = &ctrl->cbar[(kb + 1) % 3];
+        const unsigned long long add = 1ull | (static_cast<unsigned long long>(sm.my_rows) << 16) |
+                                       (static_cast<unsigned long long>(sm.my_frees) << 40);
+        unsigned long long v;
+        if constexpr (RS) {
+          asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(w), "l"(add) : "memory");
+          do {
+            v = ld_acquire_sys_u64(w);
+          } while ((v & 0xFFFFull) < static_cast<unsigned long long>(G));
+        } else {
+          asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(w), "l"(add) : "memory");
+          do {
+            v = ld_acquire_u64(w);
+          } while ((v & 0xFFFFull) < static_cast<unsigned long long>(G));
+        }
+        sm.tot_rows = static_cast<int32_t>((v >> 16) & 0xFFFFFFull);
+        sm.tot_frees = static_cast<int32_t>(v >> 40);
+        sm.my_rows = sm.my_frees = 0;
+      }
+      __syncthreads();
+    } else {
+      bar.sync();
+    }
+    ++kb;
+    if (leader) {
+      *M.rcnt((kb + 2) % 3) = 0;
+      *M.fcnt((kb + 2) % 3) = 0;
+      if constexpr (kCounted) ctrl->cbar[(kb + 2) % 3] = 0;
+    }
+  };
+  if constexpr (RS) {
+    gsync();  // every rank's row minima and replica in place
+    const int lt = lbr * kThreads + tid, nlt = Gr * kThreads;
+    for (int i = lt; i < a.n; i += nlt) {
+      int32_t lo = 0x7fffffff;
+      for (int r = 0; r < sh->R; ++r) lo = min(lo, ldcg(sh->rowmin + static_cast<int64_t>(r) * a.n + i));
+      *M.u(i).local() = a.seed == 1 ? lo : 0;  // hungarian.cpp:323-327
+    }
+    gsync();
+  }
   if (ldcg(&ctrl->status) != 0) return;  // invalid input (k_init_rows), all CTAs agree
   for (int c = tid; c < W; c += kThreads) {
     vloc[c] = 0;  // seed 0: v = 0
@@ -451,47 +620,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   unsigned long long deadline = a.deadline_ns;
   if (deadline >> 63) deadline = globaltimer_ns() + (deadline & ~(1ull << 63));  // relative budget
 
-  // Shared append counters are triple-buffered by barrier index: appends made
-  // between barriers k-1 and k go to cnt[k % 3], every CTA reads it right after
-  // barrier k, and the leader clears cnt[(k+2) % 3] after barrier k (last read
-  // after barrier k-1, next used after barrier k+1), so a fast CTA's appends
-  // never race a slow CTA's read.
-  int kb = 0;
-  // Grid engine: the barrier word also carries the append totals (each CTA
-  // adds 1 | rows << 16 | frees << 40), so nobody re-reads the counters after
-  // it — one L2 round trip less per barrier.  Other engines read the counters.
-  constexpr bool kCounted = std::is_same_v<Barrier, GridBarrier> && !DSM;
-  if (tid == 0) {
-    sm.my_rows = sm.my_frees = 0;
-    sm.tot_rows = sm.tot_frees = 0;
-  }
-  auto gsync = [&]() {
-    if constexpr (kCounted) {
-      __syncthreads();
-      if (tid == 0) {
-        unsigned long long* w = &ctrl->cbar[(kb + 1) % 3];
-        const unsigned long long add = 1ull | (static_cast<unsigned long long>(sm.my_rows) << 16) |
-                                       (static_cast<unsigned long long>(sm.my_frees) << 40);
-        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(w), "l"(add) : "memory");
-        unsigned long long v;
-        do {
-          v = ld_acquire_u64(w);
-        } while ((v & 0xFFFFull) < static_cast<unsigned long long>(G));
-        sm.tot_rows = static_cast<int32_t>((v >> 16) & 0xFFFFFFull);
-        sm.tot_frees = static_cast<int32_t>(v >> 40);
-        sm.my_rows = sm.my_frees = 0;
-      }
-      __syncthreads();
-    } else {
-      bar.sync();
-    }
-    ++kb;
-    if (leader) {
-      *M.rcnt((kb + 2) % 3) = 0;
-      *M.fcnt((kb + 2) % 3) = 0;
-      if constexpr (kCounted) ctrl->cbar[(kb + 2) % 3] = 0;
-    }
-  };
   auto got_rows = [&]() { return kCounted ? sm.tot_rows : M.ld(M.rcnt(kb % 3)); };
   auto got_frees = [&]() { return kCounted ? sm.tot_frees : M.ld(M.fcnt(kb % 3)); };
   int64_t D = 0;
@@ -518,10 +646,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     KMB_FINE(3);
     if (dirty_round) {
       dirty_round = false;
-      if (sm.ndseg > 0) relax_sel(a, M, p, head, tail, c0, dsegs, sm.ndseg, skey);
+      if (sm.ndseg > 0) relax_sel(Cb, pitch, M, p, head, tail, cl0, dsegs, sm.ndseg, skey);
       seg_rows += static_cast<int64_t>(tail - head) * sm.ndseg;
     } else {
-      relax_slab(a, M, p, head, tail, c0, W, skey);
+      relax_slab(Cb, pitch, M, p, head, tail, cl0, W, skey);
       rows_scanned += tail - head;
     }
     KMB_FINE(0);
@@ -606,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     if (wid == 0) {
       int64_t x = lane < kThreads / 32 ? sm.part[lane] : KMB_I64_INF;
       x = warp_min_i64(x);
-      if (lane == 0) *M.partial(blockIdx.x) = x;
+      if (lane == 0) *M.partial(gb) = x;
     }
     KMB_STAGE(0);
     gsync();  // ---------------------------------------------------- B1
@@ -650,7 +778,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     // round re-relaxes survivors over dirty segments only, so every survivor
     // must already be in the keys); a key whose argmin is one of them that gets
     // dissolved is reset below like any other.
-    relax_slab(a, M, p, head, tail, c0, W, skey);
+    relax_slab(Cb, pitch, M, p, head, tail, cl0, W, skey);
     rows_scanned += tail - head;
     __syncthreads();
     // columns of the slab: finalise dissolved ones, reset keys whose argmin row leaves
@@ -758,8 +886,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
     }
   }
   (void)fatal;
+  int64_t* const vo = RS ? sh->vout[grank] + cl0 : a.v + c0;
   for (int c = tid; c < W; c += kThreads)
-    if (c0 + c < a.n) a.v[c0 + c] = vloc[c];
+    if (c0 + c < a.n) vo[c] = vloc[c];
+  if constexpr (RS) {  // K10 over the slab: sum of C[match_col[j]][j] (core.cpp:76-90)
+    long long o = 0;
+    for (int c = tid; c < W; c += kThreads)
+      if (c0 + c < a.n) {
+        const int32_t i = M.ld(M.match_col(c0 + c));
+        if (i >= 0) o += Cb[static_cast<int64_t>(i) * pitch + cl0 + c];
+      }
+#pragma unroll
+    for (int q = 16; q > 0; q >>= 1) o += __shfl_xor_sync(0xffffffffu, o, q);
+    if (lane == 0 && o) atomicAdd(&ctrl->obj, static_cast<unsigned long long>(o));
+  }
 #if KMB_SOLVER_FINE
   if (leader)
     printf("k_solve leader fine (cycles/round over %lld rounds): relax %lld, sync %lld, absorb %lld, other %lld\n",
@@ -778,6 +918,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
   }
 }
 
+template <class Barrier, bool DSM>
+__global__ void __launch_bounds__(kThreads, 1) k_solve(SolverArgs a) {
+  solve_body<Barrier, DSM ? 1 : 0>(a, nullptr);
+}
+
+// column-sharded ranks with a replicated row side (RMem); `sh` in device memory
+__global__ void __launch_bounds__(kThreads, 1) k_solve_sharded(SolverArgs a, const ShardDevArgs* sh) {
+  solve_body<GridBarrier, 2>(a, sh);
+}
+
 // ---- full-frontier scan microbenchmark ------------------------------------------
 // The engine's reduced-cost scan (relax_slab) with every row in the frontier:
 // one pass over the whole n x n matrix per launch, keys written out so the pass
@@ -789,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan_all(SolverArgs a, uint64_t
   const int W = a.W, c0 = blockIdx.x * W;
   for (int c = threadIdx.x; c < W; c += kThreads) skey[c] = KMB_KEY_INF;
   __syncthreads();
-  relax_slab<GMem, kScanBatch>(a, GMem{&a}, 0, 0, a.n, c0, W, skey);
+  relax_slab<GMem, kScanBatch>(a.C, a.pitch, GMem{&a}, 0, 0, a.n, c0, W, skey);
   __syncthreads();
   for (int c = threadIdx.x; c < W; c += kThreads)
     if (c0 + c < a.n) keys_out[c0 + c] = skey[c];
@@ -878,5 +1028,19 @@ cudaError_t launch_objective(const int32_t* C, int64_t pitch, int n, const int32
 }
 
 int solver_threads() { return kThreads; }
+
+size_t shard_rep_bytes(int n, int G) { return shard_rep_o32(n, G) + 4ull * 7 * n; }
+
+cudaError_t launch_solver_sharded(const SolverArgs& a, const ShardDevArgs* sh_dev, int grid, cudaStream_t st) {
+  const size_t smem = solver_smem_bytes(a.W);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_solve_sharded, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  void* params[] = {const_cast<SolverArgs*>(&a), const_cast<ShardDevArgs**>(&sh_dev)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_solve_sharded), dim3(grid), dim3(kThreads),
+                                     params, smem, st);
+}
 
 }  // namespace kmb
