@@ -209,10 +209,20 @@ int main() {
       const SolveResult a = solve_km_b200(inst, &d1);
       const SolveResult b = solve_km(inst, &d2);
       CHECK(a.objective == b.objective && d1.u == d2.u && d1.v == d2.v);
-      // lossless B = N through the device quantization: the wide engine's duals
-      DualPotentials e0, f0;
+      // B = N: B * N overflows int64 for costs this wide, so quantize_costs
+      // rejects it — the drop-in the same way, with the same message
       BatchedKMConfig c0;
       c0.B = head;
+      std::string m1, m2;
+      try { solve_batched_km_b200(inst, c0); } catch (const std::invalid_argument& e) { m1 = e.what(); }
+      try { solve_batched_km(inst, c0); } catch (const std::invalid_argument& e) { m2 = e.what(); }
+      CHECK(m1 == m2 && m1 == "quantize_costs: B * max cost overflows");
+      // B = N with N = 2^31 (N * N fits): lossless, chat = C beyond the 32-bit
+      // engines' range, solved on the wide engine
+      for (int64_t& x : inst.cost) x = static_cast<int64_t>(rng() % (int64_t{1} << 31));
+      inst.cost[1] = int64_t{1} << 31;
+      c0.B = int64_t{1} << 31;
+      DualPotentials e0, f0;
       const SolveResult g = solve_batched_km_b200(inst, c0, &e0);
       const SolveResult h = solve_batched_km(inst, c0, &f0);
       CHECK(g.exact && h.exact && g.objective == h.objective && e0.u == f0.u && e0.v == f0.v);
