@@ -187,6 +187,10 @@ __device__ __forceinline__ int cta_solve(const BatchArgs& a, const int32_t* Cm, 
   __syncthreads();
 
   while (nfree > 0) {
+    if (rounds > 4 * n * n + 64) {  // a valid search ends in n epochs of <= 2n + 1 rounds
+      status = -2;
+      break;
+    }
     ++rounds;
     // ---- relax rows[head, nrows) for column j (hungarian.cpp:164-172) ----
     if (!dirty_round) {

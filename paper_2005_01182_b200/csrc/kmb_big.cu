@@ -242,6 +242,10 @@ __global__ void __launch_bounds__(kT, 1) k_big(BigArgs a) {
     long long clk[6] = {0, 0, 0, 0, 0, 0}, clk_last = clock64();  // relax, dirty, min, absorb, epoch, sync
 #endif
     while (nfree > 0) {
+      if (rounds > 4 * n * n + 64) {  // a valid search ends in n epochs of <= 2n + 1 rounds
+        status = -2;
+        break;
+      }
       ++rounds;
       // ---- relax (hungarian.cpp:164-172) ----
       if (!dirty_round) {

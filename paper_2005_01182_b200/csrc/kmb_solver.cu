@@ -655,6 +655,13 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
     KMB_FINE(0);
     __syncthreads();
     KMB_FINE(1);
+    // a valid search ends within n epochs of at most 2n + 1 rounds each; every
+    // CTA counts the same rounds, so all of them stop together if it does not
+    if (rounds_total > 4ll * a.n * a.n + 64) {
+      if (leader) ctrl->status = -2;
+      fatal = true;
+      break;
+    }
     if (rounds_total == 0 && a.seed == 1)  // column reduction, hungarian.cpp:328-333
       for (int c = tid; c < W; c += kThreads)
         if (c0 + c < a.n) vloc[c] = key_val(skey[c]);
@@ -994,7 +1001,8 @@ cudaError_t launch_solver(const SolverArgs& a, int G, bool cluster, cudaStream_t
   // search state in the cluster's distributed shared memory when G is a power
   // of two (element i -> CTA i mod G) and it fits
   static const bool no_dsm = getenv("KMB_NO_DSM") != nullptr;  // A/B switch
-  const bool dsm = !no_dsm && (G & (G - 1)) == 0 && smem + dsm_bytes(a.n, G) <= 200 * 1024;
+  // (the DSMEM claim words hold the column in 13 bits: n <= 8192)
+  const bool dsm = !no_dsm && a.n <= 8192 && (G & (G - 1)) == 0 && smem + dsm_bytes(a.n, G) <= 200 * 1024;
   auto kern = dsm ? k_solve<ClusterBarrier, true> : k_solve<ClusterBarrier, false>;
   const size_t csmem = smem + (dsm ? dsm_bytes(a.n, G) : 0);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -201,6 +201,10 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   __syncwarp();
 
   while (nfree > 0) {
+    if (rounds > 4 * n * n + 64) {  // a valid search ends in n epochs of <= 2n + 1 rounds
+      status = -2;
+      break;
+    }
     ++rounds;
     // ---- relax rows[head, nrows)  (hungarian.cpp:164-172) ----
     int r = head;

@@ -248,6 +248,10 @@ __global__ void __launch_bounds__(T) k_wide(WideArgs a) {
     __syncthreads();
 
     while (nfree > 0) {
+      if (rounds > 4ll * n * n + 64) {  // a valid search ends in n epochs of <= 2n + 1 rounds
+        status = -2;
+        break;
+      }
       ++rounds;
       // ---- relax the rows reached last round (hungarian.cpp:164-172) ----
       for (int j = t; j < n; j += T) {
