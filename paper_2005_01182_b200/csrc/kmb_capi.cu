@@ -14,6 +14,7 @@
 
 #include "kmb.h"
 #include "kmb_internal.h"
+#include "kmb_stage.h"
 
 namespace {
 
@@ -99,6 +100,8 @@ struct kmb_context {
   std::unique_ptr<kmb::Exchange> exchange;
   // device-resident column-sharded solve (replicas, IPC mappings)
   kmb::ShardDevPtr shard_dev;
+  // pageable host buffers: pinned staging ring + copy threads (kmb_stage.h)
+  std::unique_ptr<kmb::HostStager> stager;
   // chunked host-input pipeline of the batch engines
   static constexpr int kAux = 4, kMaxChunks = 64;
   cudaStream_t aux[kAux] = {};
@@ -149,6 +152,7 @@ void kmb_destroy(kmb_context* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   c->shard_dev.reset();
+  c->stager.reset();
   for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
                     &c->obj, &c->bcost, &c->bpad, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
@@ -344,16 +348,38 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.status = status_base + lo;
     return kmb::launch_warp_batch(a, c->sm_count, static_cast<int>(c->warps_per_sm), s, &grid);
   };
+  // Pageable host memory (numpy arrays, std::vectors): the costs are staged
+  // through pinned slots by the copy threads, and results bound for pageable
+  // arrays land in a pinned buffer first (a D2H into pageable memory blocks
+  // the host until the stream reaches it, which would serialise the chunks).
+  const bool page_in = host_in && !async_status && !kmb::is_pinned_host(costs);
+  int32_t* orow = row_to_col;
+  int64_t *ou = u, *ov = v, *otot = total_cost;
+  const bool pg_row = row_to_col && dr2c != row_to_col && !kmb::is_pinned_host(row_to_col);
+  const bool pg_u = u && du != u && !kmb::is_pinned_host(u);
+  const bool pg_v = v && dv != v && !kmb::is_pinned_host(v);
+  const bool pg_tot = total_cost && dtot != total_cost && !kmb::is_pinned_host(total_cost);
+  if (page_in || pg_row || pg_u || pg_v || pg_tot) {
+    if (!c->stager) c->stager = std::make_unique<kmb::HostStager>();
+  }
+  if (pg_row || pg_u || pg_v || pg_tot) {
+    unsigned char* pb = nullptr;
+    KMB_CUDA(c->stager->out_buffer(nb * 20 + static_cast<size_t>(batch) * 8, &pb));
+    if (pg_u) ou = reinterpret_cast<int64_t*>(pb);
+    if (pg_v) ov = reinterpret_cast<int64_t*>(pb + nb * 8);
+    if (pg_tot) otot = reinterpret_cast<int64_t*>(pb + nb * 16);
+    if (pg_row) orow = reinterpret_cast<int32_t*>(pb + nb * 16 + static_cast<size_t>(batch) * 8);
+  }
   // results of instances [lo, lo + cnt) to the caller's host buffers
   auto results_out = [&](int lo, int cnt, cudaStream_t s) -> cudaError_t {
     const size_t ro = static_cast<size_t>(lo) * n, rn = static_cast<size_t>(cnt) * n;
     cudaError_t e = cudaSuccess;
     if (dr2c != row_to_col && row_to_col)
-      e = cudaMemcpyAsync(row_to_col + ro, dr2c + ro, rn * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && du != u && u) e = cudaMemcpyAsync(u + ro, du + ro, rn * 8, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && dv != v && v) e = cudaMemcpyAsync(v + ro, dv + ro, rn * 8, cudaMemcpyDeviceToHost, s);
+      e = cudaMemcpyAsync(orow + ro, dr2c + ro, rn * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && du != u && u) e = cudaMemcpyAsync(ou + ro, du + ro, rn * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dv != v && v) e = cudaMemcpyAsync(ov + ro, dv + ro, rn * 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && dtot != total_cost && total_cost)
-      e = cudaMemcpyAsync(total_cost + lo, dtot + lo, static_cast<size_t>(cnt) * 8, cudaMemcpyDeviceToHost, s);
+      e = cudaMemcpyAsync(otot + lo, dtot + lo, static_cast<size_t>(cnt) * 8, cudaMemcpyDeviceToHost, s);
     return e;
   };
   int used = engine;
@@ -368,7 +394,8 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   }
   KMB_CUDA(cudaEventRecord(c->ev0, st));
   if (!pipelined) {
-    if (host_in) KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
+    if (page_in) KMB_CUDA(c->stager->h2d(c->bcost.p, costs, cbytes, st));
+    else if (host_in) KMB_CUDA(cudaMemcpyAsync(c->bcost.p, costs, cbytes, cudaMemcpyHostToDevice, st));
     if (repack) {  // rows padded to np (in-bounds, aligned vector loads): pad once
       KMB_CUDA(c->bpad.ensure(nb * np * 4));
       KMB_CUDA(cudaMemcpy2DAsync(c->bpad.p, np * 4, dcost, n * 4, n * 4, nb, cudaMemcpyDeviceToDevice, st));
@@ -393,14 +420,20 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     // auxiliary stream once its copy has landed (solves of successive chunks
     // may overlap each other; the D2H engine runs beside the H2D one)
     KMB_CUDA(cudaStreamWaitEvent(c->cin, c->ev0, 0));
-    for (size_t k = 0; k < sched.size(); ++k) {
+    auto copy_in = [&](size_t k) -> cudaError_t {
       const int lo = sched[k].first, cnt = sched[k].second;
-      const size_t off = static_cast<size_t>(lo) * n * n;
-      KMB_CUDA(cudaMemcpyAsync(c->bcost.as<int32_t>() + off, costs + off,
-                               static_cast<size_t>(cnt) * n * n * 4, cudaMemcpyHostToDevice, c->cin));
-      KMB_CUDA(cudaEventRecord(c->in_ev[k], c->cin));
-    }
+      const size_t off = static_cast<size_t>(lo) * n * n, len = static_cast<size_t>(cnt) * n * n * 4;
+      cudaError_t e = page_in ? c->stager->h2d(c->bcost.as<int32_t>() + off, costs + off, len, c->cin)
+                              : cudaMemcpyAsync(c->bcost.as<int32_t>() + off, costs + off, len,
+                                                cudaMemcpyHostToDevice, c->cin);
+      return e == cudaSuccess ? cudaEventRecord(c->in_ev[k], c->cin) : e;
+    };
+    // pinned input: every copy enqueued up front; pageable: the host stages
+    // chunk k + 1 while chunk k's copy and solve run
+    if (!page_in)
+      for (size_t k = 0; k < sched.size(); ++k) KMB_CUDA(copy_in(k));
     for (size_t k = 0; k < sched.size(); ++k) {
+      if (page_in) KMB_CUDA(copy_in(k));
       const int lo = sched[k].first, cnt = sched[k].second;
       cudaStream_t s2 = c->aux[k % kmb_context::kAux];
       KMB_CUDA(cudaStreamWaitEvent(s2, c->in_ev[k], 0));
@@ -427,6 +460,10 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, who);
   }
+  if (pg_u) c->stager->memcpy_par(u, ou, nb * 8);
+  if (pg_v) c->stager->memcpy_par(v, ov, nb * 8);
+  if (pg_row) c->stager->memcpy_par(row_to_col, orow, nb * 4);
+  if (pg_tot) std::memcpy(total_cost, otot, static_cast<size_t>(batch) * 8);
   const int64_t* h = c->hsum;
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
