@@ -634,6 +634,12 @@ static int prepare_grid(kmb_context* c, const int32_t* cost, int32_t n, int64_t 
   // prefetching the rows each round appends pays when they come from HBM (c5:
   // 121.7 -> 117.2 ms); on an L2-resident matrix it only adds traffic (c4: +5%)
   a.prefetch_rows = static_cast<double>(pitch) * n * 4 > 96.0 * (1 << 20) ? 1 : 0;
+#ifndef KMB_SLAB_CACHE
+#define KMB_SLAB_CACHE 1
+#endif
+  // the grid engine keeps the rows' roots and its slab's matches in shared
+  // memory (4 (n + W) bytes; one CTA per SM), the cluster engine does not
+  a.slab_cache = (KMB_SLAB_CACHE && !cluster && n <= 40960) ? 1 : 0;
   a.u = c->u.as<int64_t>();
   a.v = c->v.as<int64_t>();
   a.match_row = c->mrow.as<int32_t>();

@@ -50,7 +50,8 @@ struct Ctrl {
 // memory (the kernel reads it through a pointer).
 constexpr int KMB_MAX_RANKS = 8;
 struct ShardDevArgs {
-  int32_t R, rank_base, Gr, pad_;
+  int32_t R, rank_base, Gr;
+  int32_t sys;                         // 1: ranks on several GPUs (system-scope barrier)
   int64_t slab_pitch;
   const int32_t* slab[KMB_MAX_RANKS];  // rank r's cost slab (its own HBM)
   unsigned char* rep[KMB_MAX_RANKS];   // replica bases (peer-mapped for other GPUs)
@@ -66,6 +67,7 @@ struct SolverArgs {
   int32_t seed;       // 0: u = v = 0 (solve_km), 1: reductions (solve_batched_km)
   int32_t continue_bfs;
   int32_t prefetch_rows;  // L2 bulk prefetch of appended rows (matrix larger than L2)
+  int32_t slab_cache;     // grid / sharded engines: row roots + slab matches in shared memory
   unsigned long long deadline_ns;  // %globaltimer deadline, 0 = none
   int64_t* u;
   int64_t* v;

@@ -156,6 +156,7 @@ int run(kmb_context* c, ShardDevState& s, int32_t seed, int32_t* row_to_col, int
   A.R = s.R;
   A.rank_base = s.local ? 0 : s.rank;
   A.Gr = p.Gr;
+  A.sys = s.local ? 0 : 1;
   A.slab_pitch = s.local ? static_cast<int64_t>(p.Gt) * p.W : p.slab_cols();
   for (int r = 0; r < s.R; ++r) {
     A.rep[r] = s.peer[r];
@@ -173,7 +174,10 @@ int run(kmb_context* c, ShardDevState& s, int32_t seed, int32_t* row_to_col, int
   a.n = n;
   a.W = p.W;
   a.seed = seed;
-  a.prefetch_rows = 0;
+  // prefetch appended rows into L2 when this rank's slab exceeds it (as the
+  // single-GPU engine does)
+  a.prefetch_rows = static_cast<double>(A.slab_pitch) * n * 4 > 96.0 * (1 << 20) ? 1 : 0;
+  a.slab_cache = n <= 40960 ? 1 : 0;
   a.claim = h.claim;
   a.ctrl = h.ctrl;
   if (s.local || s.rank == 0) DEV_CUDA(cudaMemsetAsync(h.ctrl, 0, sizeof(Ctrl), st));

@@ -48,6 +48,9 @@
 #ifndef KMB_SOLVER_FINE
 #define KMB_SOLVER_FINE 0
 #endif
+#ifndef KMB_POLL_RELAXED  // grid barrier: relaxed polls + one acquire (1) or acquire polls (0)
+#define KMB_POLL_RELAXED 0
+#endif
 #ifndef KMB_SOLVER_PREFETCH  // L2 bulk prefetch of rows appended by the absorb
 #define KMB_SOLVER_PREFETCH 1
 #endif
@@ -56,6 +59,20 @@
 #endif
 
 namespace kmb {
+
+// list_w entry: the dual shift D at which the row was reached (low 32 bits;
+// 0 <= D <= max cost < 2^29) and the row's tree root (high 32 bits), so every
+// CTA's relax learns the roots of the rows it scans from a word it loads anyway
+// and keeps them in shared memory: the absorb then finds a parent's root
+// without an L2 round trip (grid engine)
+__device__ __forceinline__ int64_t lw_pack(int64_t D, int32_t root) {
+  return static_cast<int64_t>((static_cast<uint64_t>(static_cast<uint32_t>(root)) << 32) |
+                              static_cast<uint32_t>(D));
+}
+__device__ __forceinline__ int64_t lw_d(int64_t x) { return static_cast<int64_t>(static_cast<uint32_t>(x)); }
+__device__ __forceinline__ int32_t lw_root(int64_t x) {
+  return static_cast<int32_t>(static_cast<uint64_t>(x) >> 32);
+}
 
 constexpr int kThreads = 512;
 #ifndef KMB_SOLVER_RB
@@ -252,7 +269,7 @@ __global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
       else if (hi >= (1 << 29)) atomicMax(&a.ctrl->status, 3);  // KMB_ERANGE
       a.u[i] = u0;
       a.list_row[0][i] = i;
-      a.list_w[0][i] = 0;  // reached at D = 0: w = u - 0
+      a.list_w[0][i] = static_cast<int64_t>(i) << 32;  // reached at D = 0, its own root
       a.root_row[i] = i;
       a.claim[i] = KMB_KEY_INF;
       a.match_row[i] = -1;
@@ -269,7 +286,8 @@ __global__ void __launch_bounds__(256) k_init_rows(SolverArgs a) {
 // bits (S < 32) and a xor-shuffle tree merges them before the shared atomics.
 template <class Mem, int kRelaxBatch = kSolveBatch>
 __device__ __forceinline__ void relax_slab(const int32_t* C, int64_t pitch, const Mem& M, int p,
-                                           int head, int tail, int c0, int W, uint64_t* skey) {
+                                           int head, int tail, int c0, int W, uint64_t* skey,
+                                           int32_t* sroot = nullptr) {
   const int S = W >> 2;
   const int R = kThreads / S > 0 ? kThreads / S : 1;
   const int tid = threadIdx.x;
@@ -297,8 +315,11 @@ __device__ __forceinline__ void relax_slab(const int32_t* C, int64_t pitch, cons
 #pragma unroll
         for (int k = 0; k < kRelaxBatch; ++k) {
           c[k] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[k]) * pitch));
-          b[k] = row_bias(M.ld(M.u(i[k])) - dr[k]);  // w = u - D at reach
+          b[k] = row_bias(M.ld(M.u(i[k])) - lw_d(dr[k]));  // w = u - D at reach
         }
+        if (sroot && s == 0)
+#pragma unroll
+          for (int k = 0; k < kRelaxBatch; ++k) sroot[i[k]] = lw_root(dr[k]);
 #pragma unroll
         for (int k = 0; k < kRelaxBatch; ++k) {
           best0 = umin64(best0, pack_key(static_cast<uint32_t>(c[k].x) + b[k], i[k]));
@@ -311,7 +332,8 @@ __device__ __forceinline__ void relax_slab(const int32_t* C, int64_t pitch, cons
         const int i = M.ld(M.list_row(p, r));
         const int64_t drr = M.ld(M.list_w(p, r));
         const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * pitch));
-        const uint32_t b = row_bias(M.ld(M.u(i)) - drr);
+        const uint32_t b = row_bias(M.ld(M.u(i)) - lw_d(drr));
+        if (sroot && s == 0) sroot[i] = lw_root(drr);
         best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
         best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
         best2 = umin64(best2, pack_key(static_cast<uint32_t>(c.z) + b, i));
@@ -378,7 +400,7 @@ __device__ __forceinline__ void relax_sel(const int32_t* C, int64_t pitch, const
 #pragma unroll
       for (int q = 0; q < kRelaxBatch; ++q) {
         c[q] = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i[q]) * pitch));
-        b[q] = row_bias(M.ld(M.u(i[q])) - dr[q]);
+        b[q] = row_bias(M.ld(M.u(i[q])) - lw_d(dr[q]));
       }
 #pragma unroll
       for (int q = 0; q < kRelaxBatch; ++q) {
@@ -392,7 +414,7 @@ __device__ __forceinline__ void relax_sel(const int32_t* C, int64_t pitch, const
       const int i = M.ld(M.list_row(p, r));
       const int64_t drr = M.ld(M.list_w(p, r));
       const int4 c = ld_stream(reinterpret_cast<const int4*>(base + static_cast<int64_t>(i) * pitch));
-      const uint32_t b = row_bias(M.ld(M.u(i)) - drr);
+      const uint32_t b = row_bias(M.ld(M.u(i)) - lw_d(drr));
       best0 = umin64(best0, pack_key(static_cast<uint32_t>(c.x) + b, i));
       best1 = umin64(best1, pack_key(static_cast<uint32_t>(c.y) + b, i));
       best2 = umin64(best2, pack_key(static_cast<uint32_t>(c.z) + b, i));
@@ -435,6 +457,11 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
   int64_t* dcol = vloc + W;
   unsigned char* rch = reinterpret_cast<unsigned char*>(dcol + W);
   int32_t* dsegs = reinterpret_cast<int32_t*>(rch + W);  // dirty segments (W/4)
+  // grid / sharded engines: the roots of the rows this CTA relaxed (n) and the
+  // matches of its slab columns (W), so the absorb reads no global state
+  const bool cache = !DSM && a.slab_cache;
+  int32_t* sroot = cache ? dsegs + (W >> 2) : nullptr;
+  int32_t* smatch = cache ? sroot + a.n : nullptr;
   __shared__ SlabSmem sm;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -529,7 +556,7 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
         else if (hi >= (1 << 29)) atomicMax(&ctrl->status, 3);  // KMB_ERANGE
         sh->rowmin[static_cast<int64_t>(grank) * a.n + i] = lo;
         *M.list_row(0, i).local() = i;
-        *M.list_w(0, i).local() = 0;
+        *M.list_w(0, i).local() = static_cast<int64_t>(i) << 32;
         *M.root_row(i).local() = i;
         *M.match_row(i).local() = -1;
         *M.match_col(i).local() = -1;
@@ -559,17 +586,24 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
         unsigned long long* w = &ctrl->cbar[(kb + 1) % 3];
         const unsigned long long add = 1ull | (static_cast<unsigned long long>(sm.my_rows) << 16) |
                                        (static_cast<unsigned long long>(sm.my_frees) << 40);
+        // KMB_POLL_RELAXED: poll relaxed, then one acquire load of the
+        // completed word (it reads the last arrival's add, so it synchronises
+        // with every arrival's release; the word cannot be cleared in between:
+        // that happens after the next barrier).  Otherwise every poll is an
+        // acquire (an L1 invalidation each, but no extra round trip at the end).
         unsigned long long v;
-        if constexpr (RS) {
+        if (RS && sh->sys) {  // ranks on several GPUs: system scope
           asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(w), "l"(add) : "memory");
           do {
-            v = ld_acquire_sys_u64(w);
+            v = KMB_POLL_RELAXED ? ld_relaxed_sys_u64(w) : ld_acquire_sys_u64(w);
           } while ((v & 0xFFFFull) < static_cast<unsigned long long>(G));
+          if (KMB_POLL_RELAXED) v = ld_acquire_sys_u64(w);
         } else {
           asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(w), "l"(add) : "memory");
           do {
-            v = ld_acquire_u64(w);
+            v = KMB_POLL_RELAXED ? ld_relaxed_u64(w) : ld_acquire_u64(w);
           } while ((v & 0xFFFFull) < static_cast<unsigned long long>(G));
+          if (KMB_POLL_RELAXED) v = ld_acquire_u64(w);
         }
         sm.tot_rows = static_cast<int32_t>((v >> 16) & 0xFFFFFFull);
         sm.tot_frees = static_cast<int32_t>(v >> 40);
@@ -601,6 +635,7 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
     vloc[c] = 0;  // seed 0: v = 0
     skey[c] = KMB_KEY_INF;
     rch[c] = (c0 + c < a.n) ? 0 : 1;  // padding columns never count
+    if (cache) smatch[c] = -1;
   }
   __syncthreads();
   int64_t dual_steps = 0, rows_scanned = 0, seg_rows = 0;
@@ -649,7 +684,7 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
       if (sm.ndseg > 0) relax_sel(Cb, pitch, M, p, head, tail, cl0, dsegs, sm.ndseg, skey);
       seg_rows += static_cast<int64_t>(tail - head) * sm.ndseg;
     } else {
-      relax_slab(Cb, pitch, M, p, head, tail, cl0, W, skey);
+      relax_slab(Cb, pitch, M, p, head, tail, cl0, W, skey, sroot);
       rows_scanned += tail - head;
     }
     KMB_FINE(0);
@@ -674,14 +709,14 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
       for (int cb = 0; cb < W; cb += kThreads) {
         const int c = cb + tid;
         bool newrow = false, newfree = false;
-        int32_t i2 = -1, col = c0 + c;
+        int32_t i2 = -1, col = c0 + c, root = 0;
         if (c < W && !rch[c] && key_val(skey[c]) - vloc[c] == Dn) {
           rch[c] = 1;
           dcol[c] = Dn;
           const int32_t par = key_row(skey[c]);
           *M.tree_par(col) = par;
-          const int32_t root = M.ld(M.root_row(par));
-          i2 = M.ld(M.match_col(col));
+          root = cache ? sroot[par] : M.ld(M.root_row(par));
+          i2 = cache ? smatch[c] : M.ld(M.match_col(col));
           if (i2 < 0) {
             newfree = true;
             M.claim_min(root, M.ckey(epoch, col));
@@ -691,10 +726,13 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
 #if KMB_SOLVER_PREFETCH
             // every CTA scans this row next round: start pulling it into L2 now,
             // so the barrier and the list reads hide the DRAM latency
+            // (sharded: this rank's slab row; a rank cannot prefetch into a
+            // peer GPU's L2)
             if (a.prefetch_rows)
-              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.C + static_cast<int64_t>(i2) * a.pitch),
-                         "r"(static_cast<uint32_t>(a.pitch * 4))
-                         : "memory");
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                               (RS ? sh->slab[grank] : a.C) + static_cast<int64_t>(i2) * pitch),
+                           "r"(static_cast<uint32_t>((RS ? static_cast<int64_t>(Gr) * W : pitch) * 4))
+                           : "memory");
 #endif
           }
         }
@@ -710,7 +748,7 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
           if (newrow) {
             const int pos = tail + base + __popc(rowmask & ((1u << lane) - 1));
             *M.list_row(p, pos) = i2;
-            *M.list_w(p, pos) = Dn;
+            *M.list_w(p, pos) = lw_pack(Dn, root);
           }
         }
         const unsigned fmask = __ballot_sync(0xffffffffu, newfree);
@@ -785,7 +823,7 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
     // round re-relaxes survivors over dirty segments only, so every survivor
     // must already be in the keys); a key whose argmin is one of them that gets
     // dissolved is reset below like any other.
-    relax_slab(Cb, pitch, M, p, head, tail, cl0, W, skey);
+    relax_slab(Cb, pitch, M, p, head, tail, cl0, W, skey, sroot);
     rows_scanned += tail - head;
     __syncthreads();
     // columns of the slab: finalise dissolved ones, reset keys whose argmin row leaves
@@ -828,7 +866,7 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
         // appended this round, may read u before or after this write: either
         // way every key it could set has this dissolved row as argmin and is
         // reset by that CTA's column pass.)
-        *M.u(i) = M.ld(M.u(i)) - dr + D;
+        *M.u(i) = M.ld(M.u(i)) - lw_d(dr) + D;
       } else {
         const int pos = atomicAdd(sc, 1);
         if (kCounted) atomicAdd(&sm.my_rows, 1);
@@ -865,6 +903,8 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
     ++epoch;
     head = 0;
     tail = got_rows();  // survivors
+    if (cache)  // the augmenting paths just flipped some of this slab's matches
+      for (int c = tid; c < W; c += kThreads) smatch[c] = c0 + c < a.n ? M.ld(M.match_col(c0 + c)) : -1;
     dirty_round = true;
     nfound = 0;
     if (ldcg(&ctrl->matched) == a.n) break;
@@ -876,7 +916,7 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
   if (stopped) {  // time budget: write back the surviving trees' lazy duals
     for (int r = gtid; r < tail; r += gthreads) {
       const int32_t i = M.ld(M.list_row(p, r));
-      *M.u(i) = M.ld(M.u(i)) - M.ld(M.list_w(p, r)) + D;
+      *M.u(i) = M.ld(M.u(i)) - lw_d(M.ld(M.list_w(p, r))) + D;
     }
     for (int c = tid; c < W; c += kThreads)
       if (rch[c] && c0 + c < a.n) vloc[c] -= D - dcol[c];
@@ -986,7 +1026,7 @@ cudaError_t launch_solver_init(const SolverArgs& a, cudaStream_t st) {
 cudaError_t launch_solver(const SolverArgs& a, int G, bool cluster, cudaStream_t st) {
   cudaError_t e = launch_solver_init(a, st);
   if (e != cudaSuccess) return e;
-  const size_t smem = solver_smem_bytes(a.W);
+  const size_t smem = solver_smem_bytes(a.W) + (a.slab_cache ? 4ull * (a.n + a.W) : 0);
   if (!cluster) {
     auto kern = k_solve<GridBarrier, false>;
     if (smem > 48 * 1024) {
@@ -1040,7 +1080,7 @@ int solver_threads() { return kThreads; }
 size_t shard_rep_bytes(int n, int G) { return shard_rep_o32(n, G) + 4ull * 7 * n; }
 
 cudaError_t launch_solver_sharded(const SolverArgs& a, const ShardDevArgs* sh_dev, int grid, cudaStream_t st) {
-  const size_t smem = solver_smem_bytes(a.W);
+  const size_t smem = solver_smem_bytes(a.W) + (a.slab_cache ? 4ull * (a.n + a.W) : 0);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_solve_sharded, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
