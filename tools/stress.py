@@ -1,7 +1,10 @@
 """Randomised stress: engines x sizes x value ranges x seeds against the
 reference (duals, total cost) and against themselves (determinism: the same
 matching and round count twice).  Usage: python tools/stress.py [seconds]
-(BATCH=1: random batches through every batch engine instead)."""
+(BATCH=1: random batches through every batch engine instead; WIDE=1: int64
+costs up to validate_instance's headroom through kmb_solve_i64 / the wide
+engine; SHARD=1: the device-exchange column-sharded engine with 1-8 ranks as
+CTA groups, against the reference and the grid engine's matching)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -19,7 +22,7 @@ while time.time() - t0 < budget:
         cb = rng.integers(0, hi, size=(b, n, n)).astype(np.int32)
         seed = int(rng.choice([KMB_SEED_BATCHED, KMB_SEED_KM]))
         refs = [O.ref_solve_batched_km(x) if seed == KMB_SEED_BATCHED else O.ref_solve_km(x) for x in cb]
-        for eng in ([2, 3, 4, 6] if n <= 256 else []) + [8, 0]:
+        for eng in ([4, 6] if n <= 256 else []) + [8, 0]:
             s.set_option(OPT_ENGINE, eng)
             r = s.solve_batch(cb, seed)
             ok = all(np.array_equal(r.u[t], refs[t].u) and np.array_equal(r.v[t], refs[t].v)
@@ -28,6 +31,37 @@ while time.time() - t0 < budget:
             if not ok:
                 bad += 1
                 print(f"MISMATCH batch b={b} n={n} hi={hi} seed={seed} engine={eng}", flush=True)
+        continue
+    if os.environ.get("WIDE"):
+        n = int(rng.integers(1, 400))
+        head = ((1 << 62) // n) // (2 * n + 2)
+        hw = int(rng.choice([2**29, 2**35, head]))
+        c = rng.integers(0, min(hw, head), size=(n, n), dtype=np.int64)
+        c[rng.random((n, n)) < 0.3] = int(rng.integers(0, 100))
+        seed = int(rng.choice([KMB_SEED_BATCHED, KMB_SEED_KM]))
+        mx = max(int(c.max()), 1)
+        ref = (O.ref_solve_km(c) if seed == KMB_SEED_KM else
+               O.ref_solve_batched_km(c) if mx * mx < 2**63 else O.kmo_solve_batched(c))
+        r = s.solve(c, seed)
+        cases += 1
+        if not (np.array_equal(r.u, ref.u) and np.array_equal(r.v, ref.v) and r.total_cost == ref.total_cost):
+            bad += 1
+            print(f"MISMATCH wide n={n} max={mx} seed={seed} engine={r.stats['engine']}", flush=True)
+        continue
+    if os.environ.get("SHARD"):
+        n = int(rng.choice([rng.integers(1, 64), rng.integers(64, 700), rng.integers(700, 3000)]))
+        c = rng.integers(0, hi, size=(n, n)).astype(np.int32)
+        seed = int(rng.choice([KMB_SEED_BATCHED, KMB_SEED_KM]))
+        ref = O.ref_solve_batched_km(c) if seed == KMB_SEED_BATCHED else O.ref_solve_km(c)
+        s.set_option(OPT_ENGINE, 1)
+        g = s.solve(c, seed)
+        for R in (1, 2, 3, 5, 8):
+            r = s.solve_sharded_local(c, R, seed)
+            cases += 1
+            if not (np.array_equal(r.u, ref.u) and np.array_equal(r.v, ref.v) and r.total_cost == ref.total_cost
+                    and np.array_equal(r.row_to_col, g.row_to_col)):
+                bad += 1
+                print(f"MISMATCH sharded n={n} hi={hi} seed={seed} ranks={R}", flush=True)
         continue
     n = int(rng.choice([rng.integers(1, 64), rng.integers(64, 300), rng.integers(300, 1500), rng.integers(1500, 3000)]))
     c = rng.integers(0, hi, size=(n, n)).astype(np.int32)
