@@ -141,6 +141,17 @@ int alloc_state(ShardDevState& s, int n, int R, int rank, bool local, int max_ct
   return KMB_OK;
 }
 
+// GPU ranks: every rank reaches this host vote before launching, so a rank
+// that failed locally (bad arguments, staging) makes every rank return an
+// error instead of leaving the others' kernels waiting at the first barrier.
+// Returns 0 when every rank is ready.
+int vote(Exchange* ex, bool ok) {
+  if (!ex || ex->nranks <= 1) return ok ? 0 : -1;
+  int64_t x = ok ? 0 : -1;
+  if (ex->allreduce_min(&x, 1) != 0) return -2;
+  return x < 0 ? -1 : 0;
+}
+
 // Run the kernel over this process's ranks; slab pointers already staged.
 int run(kmb_context* c, ShardDevState& s, int32_t seed, int32_t* row_to_col, int64_t* u, int64_t* v,
         int64_t* total_cost, kmb_stats* stats, const char* who, Exchange* ex) {
@@ -169,7 +180,7 @@ int run(kmb_context* c, ShardDevState& s, int32_t seed, int32_t* row_to_col, int
     }
   }
   A.rowmin = h.rowmin;
-  DEV_CUDA(cudaMemcpyAsync(s.args_dev, &A, sizeof(A), cudaMemcpyHostToDevice, st));
+  const bool staged = cudaMemcpyAsync(s.args_dev, &A, sizeof(A), cudaMemcpyHostToDevice, st) == cudaSuccess;
   SolverArgs a{};
   a.n = n;
   a.W = p.W;
@@ -180,12 +191,15 @@ int run(kmb_context* c, ShardDevState& s, int32_t seed, int32_t* row_to_col, int
   a.slab_cache = n <= 40960 ? 1 : 0;
   a.claim = h.claim;
   a.ctrl = h.ctrl;
-  if (s.local || s.rank == 0) DEV_CUDA(cudaMemsetAsync(h.ctrl, 0, sizeof(Ctrl), st));
-  DEV_CUDA(cudaStreamSynchronize(st));
-  // GPU ranks: rank 0's reset of the home block precedes every launch
-  if (ex && ex->nranks > 1) {
-    int64_t x = 0;
-    if (ex->allreduce_min(&x, 1) != 0) return dfail(KMB_ECUDA, std::string(who) + ": host barrier failed");
+  bool ready = staged && (!(s.local || s.rank == 0) || cudaMemsetAsync(h.ctrl, 0, sizeof(Ctrl), st) == cudaSuccess);
+  ready = ready && cudaStreamSynchronize(st) == cudaSuccess;
+  // GPU ranks: rank 0's reset of the home block precedes every launch, and
+  // nobody launches unless everybody is ready
+  if (int vr = vote(ex, ready)) {
+    cudaGetLastError();
+    return dfail(KMB_ECUDA, std::string(who) + (vr == -2 ? ": host barrier failed"
+                                                : ready ? ": another rank failed before the solve"
+                                                        : ": staging the solve failed"));
   }
   DEV_CUDA(cudaEventRecord(s.e0, st));
   DEV_CUDA(launch_solver_sharded(a, s.args_dev, s.local ? p.Gt : p.Gr, st));
@@ -221,6 +235,8 @@ int run(kmb_context* c, ShardDevState& s, int32_t seed, int32_t* row_to_col, int
   if (hc.status == KMB_ENEGATIVE) return dfail(KMB_ENEGATIVE, std::string(who) + ": costs must be nonnegative");
   if (hc.status == KMB_ERANGE)
     return dfail(KMB_ERANGE, std::string(who) + ": cost exceeds the device range [0, 2^29)");
+  if (hc.status == -3)
+    return dfail(KMB_ECUDA, std::string(who) + ": a rank did not reach the barrier within 20 s");
   if (hc.status != 0) return dfail(KMB_EINTERNAL, std::string(who) + ": engine invariant violated");
   if (total_cost) *total_cost = static_cast<int64_t>(hc.obj);
   if (stats) {
@@ -334,29 +350,41 @@ int kmb_solve_sharded_dev_i32(kmb_context* c, const int32_t* slab, int32_t n, in
   auto& sp = kmb::context_shard_dev(c);
   if (!sp || sp->local) return kmb::dfail(KMB_EINVAL, std::string(who) + ": call kmb_shard_dev_open first");
   kmb::ShardDevState& s = *sp;
+  auto& ex = kmb::context_exchange(c);
+  if (s.R > 1 && !ex) return kmb::dfail(KMB_EINVAL, std::string(who) + ": call kmb_shard_init_* first");
+  // a rank-local argument error is voted on, so the other ranks return too
   for (int r = 0; r < s.R; ++r)
-    if (!s.peer[r]) return kmb::dfail(KMB_EINVAL, std::string(who) + ": call kmb_shard_dev_connect first");
+    if (!s.peer[r]) {
+      kmb::vote(ex.get(), false);
+      return kmb::dfail(KMB_EINVAL, std::string(who) + ": call kmb_shard_dev_connect first");
+    }
   const int64_t w = s.plan.slab_cols();
   const int64_t want = std::max<int64_t>(0, std::min<int64_t>(w, n - w * s.rank));
   if (n != s.n || col_begin != w * s.rank || ncols != want || !slab || ld < ncols ||
-      (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED))
+      (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED)) {
+    kmb::vote(ex.get(), false);
     return kmb::dfail(KMB_EINVAL, std::string(who) + ": bad arguments (rank r holds columns [r * slab_cols, ...))");
-  auto& ex = kmb::context_exchange(c);
-  if (s.R > 1 && !ex) return kmb::dfail(KMB_EINVAL, std::string(who) + ": call kmb_shard_init_* first");
+  }
   cudaSetDevice(kmb::context_device(c));
+  // staging failures are voted on in run()'s pre-launch barrier like any other
   const size_t need = static_cast<size_t>(n) * w * 4;
+  cudaError_t e = cudaSuccess;
   if (s.slab_bytes < need) {
     if (s.slab) cudaFree(s.slab);
     s.slab = nullptr;
     s.slab_bytes = 0;
-    DEV_CUDA(cudaMalloc(&s.slab, need));
-    s.slab_bytes = need;
+    e = cudaMalloc(&s.slab, need);
+    if (e == cudaSuccess) s.slab_bytes = need;
   }
   cudaStream_t st = kmb::context_stream(c);
-  DEV_CUDA(cudaMemsetAsync(s.slab, 0, need, st));
-  if (ncols > 0)
-    DEV_CUDA(cudaMemcpy2DAsync(s.slab, w * 4, slab, ld * 4, static_cast<size_t>(ncols) * 4, n,
-                               cudaMemcpyDefault, st));
+  if (e == cudaSuccess) e = cudaMemsetAsync(s.slab, 0, need, st);
+  if (e == cudaSuccess && ncols > 0)
+    e = cudaMemcpy2DAsync(s.slab, w * 4, slab, ld * 4, static_cast<size_t>(ncols) * 4, n, cudaMemcpyDefault, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    kmb::vote(ex.get(), false);
+    return kmb::dfail(KMB_ECUDA, std::string(who) + ": staging the slab: " + cudaGetErrorString(e));
+  }
   return kmb::run(c, s, seed, row_to_col, u, v_slab, total_cost, stats, who, ex.get());
 }
 

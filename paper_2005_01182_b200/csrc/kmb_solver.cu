@@ -90,6 +90,7 @@ struct SlabSmem {
   int64_t m;
   int32_t append_base;
   int32_t ndseg;              // dirty segments after an epoch end
+  int32_t abort;              // sharded ranks on GPUs: a barrier timed out
   int32_t my_rows, my_frees;  // this CTA's appends since the last barrier
   int32_t tot_rows, tot_frees;  // everyone's, delivered by the counting barrier
 };
@@ -579,7 +580,10 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
   // it — one L2 round trip less per barrier.  Other engines read the counters.
   // The sharded engine's ranks may be GPUs: system-scope release / acquire.
   constexpr bool kCounted = std::is_same_v<Barrier, GridBarrier> && !DSM;
-  auto gsync = [&]() {
+  if (tid == 0) sm.abort = 0;
+  // returns false when the sharded ranks' barrier timed out (then every CTA
+  // that waited leaves the solve; the host reports the status)
+  auto gsync = [&]() -> bool {
     if constexpr (kCounted) {
       __syncthreads();
       if (tid == 0) {
@@ -593,9 +597,18 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
         // acquire (an L1 invalidation each, but no extra round trip at the end).
         unsigned long long v;
         if (RS && sh->sys) {  // ranks on several GPUs: system scope
+          // a rank whose kernel never started (or died) must not leave the
+          // others spinning: after 20 s without the barrier completing every
+          // waiting CTA gives up and the solve reports an error
           asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(w), "l"(add) : "memory");
+          const unsigned long long t_wait = globaltimer_ns();
           do {
             v = KMB_POLL_RELAXED ? ld_relaxed_sys_u64(w) : ld_acquire_sys_u64(w);
+            if ((v & 0xFFFFull) < static_cast<unsigned long long>(G) &&
+                globaltimer_ns() - t_wait > 20000000000ull) {
+              sm.abort = 1;
+              break;
+            }
           } while ((v & 0xFFFFull) < static_cast<unsigned long long>(G));
           if (KMB_POLL_RELAXED) v = ld_acquire_sys_u64(w);
         } else {
@@ -619,16 +632,21 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
       *M.fcnt((kb + 2) % 3) = 0;
       if constexpr (kCounted) ctrl->cbar[(kb + 2) % 3] = 0;
     }
+    if (RS && sm.abort) {
+      if (tid == 0) atomicExch(&ctrl->status, -3);
+      return false;
+    }
+    return true;
   };
   if constexpr (RS) {
-    gsync();  // every rank's row minima and replica in place
+    if (!gsync()) return;  // every rank's row minima and replica in place
     const int lt = lbr * kThreads + tid, nlt = Gr * kThreads;
     for (int i = lt; i < a.n; i += nlt) {
       int32_t lo = 0x7fffffff;
       for (int r = 0; r < sh->R; ++r) lo = min(lo, ldcg(sh->rowmin + static_cast<int64_t>(r) * a.n + i));
       *M.u(i).local() = a.seed == 1 ? lo : 0;  // hungarian.cpp:323-327
     }
-    gsync();
+    if (!gsync()) return;
   }
   if (ldcg(&ctrl->status) != 0) return;  // invalid input (k_init_rows), all CTAs agree
   for (int c = tid; c < W; c += kThreads) {
@@ -782,7 +800,10 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
       if (lane == 0) *M.partial(gb) = x;
     }
     KMB_STAGE(0);
-    gsync();  // ---------------------------------------------------- B1
+    if (!gsync()) {  // ---------------------------------------------- B1
+      fatal = true;
+      break;
+    }
     KMB_STAGE(1);
     int added = got_rows();
     int fadded = got_frees();
@@ -808,7 +829,10 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
       ++dual_steps;
       absorb_at(D);
       KMB_STAGE(2);
-      gsync();  // ------------------------------------------------ B2 (dual steps only)
+      if (!gsync()) {  // ------------------------------------------ B2 (dual steps only)
+        fatal = true;
+        break;
+      }
       KMB_STAGE(3);
       added = got_rows();
       fadded = got_frees();
@@ -897,7 +921,10 @@ __device__ __forceinline__ void solve_body(const SolverArgs& a, const ShardDevAr
       if (deadline && globaltimer_ns() > deadline) ctrl->stop = 1;
     }
     KMB_STAGE(4);
-    gsync();  // ---------------------------------------------------- B3
+    if (!gsync()) {  // ---------------------------------------------- B3
+      fatal = true;
+      break;
+    }
     KMB_STAGE(5);
     p ^= 1;
     ++epoch;

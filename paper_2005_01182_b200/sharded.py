@@ -107,3 +107,46 @@ def solve_sharded(solver: Solver, slab: np.ndarray, n: int, col_begin: int, seed
                                    v.ctypes.data_as(C.c_void_p), C.byref(tot), C.byref(st))
     solver._check(rc)
     return r2c, u, v[:ncols], tot.value, _stats_dict(st)
+
+
+# ---- device-side exchange (kmb_shard_dev_*, csrc/kmb_shard_dev.cu) --------------
+
+def open_device_exchange(solver: Solver, n: int, group=None) -> int:
+    """Collective setup of the device-exchange protocol for an n x n instance:
+    each rank allocates its window, the 64-byte CUDA IPC handles are allgathered
+    through the process group and every rank maps its peers' windows.  Needs
+    ``init_exchange`` too (two host barriers per solve).  Returns slab_cols:
+    rank r holds columns [r * slab_cols, min(n, (r + 1) * slab_cols))."""
+    import torch
+    import torch.distributed as dist
+    lib = solver._lib
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    cols = C.c_int32()
+    mine = (C.c_uint8 * 64)()
+    solver._check(lib.kmb_shard_dev_open(solver._h, n, world, rank, C.byref(cols), mine))
+    outs = [torch.empty(64, dtype=torch.uint8) for _ in range(world)]
+    dist.all_gather(outs, torch.tensor(list(bytes(mine)), dtype=torch.uint8), group=group)
+    allh = (C.c_uint8 * (64 * world))(*torch.cat(outs).tolist())
+    solver._check(lib.kmb_shard_dev_connect(solver._h, allh))
+    return cols.value
+
+
+def solve_sharded_device(solver: Solver, slab, n: int, col_begin: int, seed: int = 1):
+    """Collective solve with the exchange on the device (after
+    ``open_device_exchange``): every rank passes its n x ncols column slab
+    (host or device array).  Returns (row_to_col[n], u[n], v_slab[ncols],
+    total_cost, stats)."""
+    lib = solver._lib
+    s = np.ascontiguousarray(slab, dtype=np.int32) if isinstance(slab, np.ndarray) else slab
+    ncols = s.shape[1]
+    r2c = np.full(n, -1, np.int32)
+    u = np.zeros(n, np.int64)
+    v = np.zeros(max(ncols, 1), np.int64)
+    tot = C.c_int64()
+    st = Stats()
+    ptr = s.ctypes.data if isinstance(s, np.ndarray) else s.data_ptr()
+    rc = lib.kmb_solve_sharded_dev_i32(solver._h, C.c_void_p(ptr), n, ncols, col_begin, ncols, seed,
+                                       r2c.ctypes.data_as(C.c_void_p), u.ctypes.data_as(C.c_void_p),
+                                       v.ctypes.data_as(C.c_void_p), C.byref(tot), C.byref(st))
+    solver._check(rc)
+    return r2c, u, v[:ncols], tot.value, _stats_dict(st)

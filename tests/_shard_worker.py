@@ -65,6 +65,20 @@ def run(rank, world, port, mode, outdir):
             C.c_void_p(r2c.ctypes.data), C.c_void_p(u.ctypes.data), C.c_void_p(v.ctypes.data),
             C.c_void_p(out.ctypes.data), C.c_int32(int(op) if rank == 1 else 0), C.c_int32(int(at)))
         results.append(rc)
+    elif mode == "dev":  # the device-exchange protocol through the Python helpers (one rank)
+        from paper_2005_01182_b200 import Solver
+        from paper_2005_01182_b200.sharded import init_exchange, open_device_exchange, solve_sharded_device
+        s = Solver(0)
+        init_exchange(s, "group")
+        for c in make_cases():
+            n = c.shape[0]
+            cols = open_device_exchange(s, n)
+            for seed in (1, 0):
+                cb = rank * cols
+                nc = max(0, min(cols, n - cb))
+                slab = np.ascontiguousarray(c[:, cb:cb + nc])
+                r2c, u, v, tot, st = solve_sharded_device(s, slab, n, cb, seed)
+                results.append((0, r2c, u, v, tot, st["dual_steps"], cb))
     else:  # "gpu"/"nccl": the CUDA slab kernels; exchange through this gloo group
         # (ranks share cuda:0) or through NCCL (one rank per GPU)
         from paper_2005_01182_b200 import Solver

@@ -151,6 +151,15 @@ def test_sharded_device_exchange_gpu_rank_path_world1(solver):
 
 
 @pytest.mark.gpu
+def test_sharded_device_exchange_python_helpers_world1():
+    """sharded.open_device_exchange / solve_sharded_device under
+    torch.distributed (IPC handle allgather, host barriers through the group)
+    with the one rank a test box's GPU can hold: the device-exchange kernels of
+    several ranks must not share a GPU as separate launches."""
+    _check(_run(1, "dev"))
+
+
+@pytest.mark.gpu
 def test_sharded_device_exchange_errors(solver):
     c = np.ones((9, 9), np.int32)
     c[4, 4] = -1
