@@ -16,9 +16,8 @@
 //
 // Layout: thread t owns CPT columns in groups of V contiguous ones, group g at
 // columns V·(t + g·T) .. V·(t + g·T) + V - 1, so a row is read with one V-wide
-// vector load per group (LDG.64 / LDG.128: a lone SM is issue-bound, and
-// scalar loads issued V times more load instructions); per-column key / v / Dc
-// in registers; per-row state, the row lists,
+// load per group (V = 2 at two columns per thread, see launch_nt); per-column
+// key / v / Dc in registers; per-row state, the row lists,
 // parents, matching, 32-bit tree claims and the dirty-column list in shared
 // memory (14n words: 224 KB at n = 4096).
 #include <cuda_runtime.h>
@@ -491,7 +490,12 @@ int big_max_n() { return 4096; }
 #define KMB_BIG_CARVE 1
 #endif
 
-template <int CPT, int NT, int V = (CPT >= 4 ? 4 : CPT)>
+// Row-load width: LDG.E.64 at two columns per thread (n <= 1024: c2 8.60 ->
+// 8.45 ms, n = 700 2.62 -> 2.53); scalar above, where a thread's V-wide groups
+// put stride-V bank conflicts on every per-column shared array of the absorb
+// and the epoch end (c4 on this engine: V = 4 171 ms, V = 2 150, V = 1 140;
+// n = 3072: 36.7 / 34.9 / 33.7 ms; tools/ab_raw.py, round 2)
+template <int CPT, int NT, int V = (CPT == 2 ? 2 : 1)>
 static cudaError_t launch_nt(const BigArgs& a, int sm_count, size_t smem, cudaStream_t st) {
   const void* k = reinterpret_cast<const void*>(k_big<CPT, NT, V>);
   // carveout: the shared memory of the CTAs per SM this batch needs (+1 KiB

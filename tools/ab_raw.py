@@ -11,9 +11,14 @@ if len(sys.argv) > 2 and sys.argv[1] == "--child":
     lib = C.CDLL(sys.argv[2])
     h = C.c_void_p()
     assert lib.kmb_create(0, C.byref(h)) == 0
+    lib.kmb_set_option(h, 3, C.c_int64(int(os.environ.get("ENGINE", "0"))))
     out = {"lib": os.path.basename(sys.argv[2])}
     for key in os.environ.get("CFGS", "c4,c5").split(","):
-        c = W.CONFIGS[key].make(); n = c.shape[0]
+        if key.startswith("u"):  # uN: uniform U{0..1e6} instance of size N
+            import numpy as np
+            n = int(key[1:]); c = np.random.default_rng(n).integers(0, 10**6, (n, n)).astype(np.int32)
+        else:
+            c = W.CONFIGS[key].make(); n = c.shape[0]
         d = torch.from_numpy(c).cuda()
         r2c = torch.empty(n, dtype=torch.int32, device="cuda"); u = torch.empty(n, dtype=torch.int64, device="cuda")
         v = torch.empty_like(u); tot = torch.empty(1, dtype=torch.int64, device="cuda")
