@@ -64,7 +64,9 @@ enum kmb_status {
 
 enum kmb_option {
   KMB_OPT_MAX_CTAS = 1,     /* grid engine: upper bound on CTAs (0 = #SMs)      */
-  KMB_OPT_CONTINUE_BFS = 2, /* 1: exhaust the tight closure before augmenting   */
+  /* 2 (continue the BFS past a free column, ABI 1) was removed: the
+     incremental-epoch engines never read it, and a CPU model of them measured
+     more rounds with it (config 1: 185 -> 236; config 3: 368 -> 379) */
   KMB_OPT_ENGINE = 3,       /* 0 auto: single instances CTA n<=256, single-CTA
                                n<=3072, cluster n<=5120, grid beyond; batches
                                warp or CTA (n<=256, by residency), single-CTA

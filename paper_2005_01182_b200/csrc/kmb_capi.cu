@@ -78,7 +78,6 @@ struct kmb_context {
   int64_t max_ctas = 0;
   int64_t warps_per_sm = 0;  // warp engine residency bound (0 = occupancy limit)
   int64_t pipeline = 0;      // host-input batches: chunk schedule (0 = tapered auto)
-  int continue_bfs = 0;
   int engine = 0;
   int64_t last_batch = 0;  // instances of the last batch solve (kmb_last_instance_stats)
   // grid-engine workspace
@@ -183,7 +182,6 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
   if (!c) return fail(KMB_EINVAL, "kmb_set_option: NULL context");
   switch (option) {
     case KMB_OPT_MAX_CTAS: c->max_ctas = value; return KMB_OK;
-    case KMB_OPT_CONTINUE_BFS: c->continue_bfs = value ? 1 : 0; return KMB_OK;
     case KMB_OPT_WARPS_PER_SM: c->warps_per_sm = value; return KMB_OK;
     case KMB_OPT_PIPELINE:
       if (value < -(kmb_context::kMaxChunks / 2) || value > kmb_context::kMaxChunks)
@@ -323,7 +321,6 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
       a.batch = cnt;
       a.n = n;
       a.seed = seed;
-      a.continue_bfs = c->continue_bfs;
       a.row_to_col = dr2c + ro;
       a.u = du + ro;
       a.v = dv + ro;
@@ -339,7 +336,6 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.n = n;
     a.pitch = np;
     a.seed = seed;
-    a.continue_bfs = c->continue_bfs;
     a.row_to_col = dr2c + ro;
     a.u = du + ro;
     a.v = dv + ro;
@@ -630,7 +626,6 @@ static int prepare_grid(kmb_context* c, const int32_t* cost, int32_t n, int64_t 
   a.n = n;
   a.W = W;
   a.seed = seed;
-  a.continue_bfs = c->continue_bfs;
   // prefetching the rows each round appends pays when they come from HBM (c5:
   // 121.7 -> 117.2 ms); on an L2-resident matrix it only adds traffic (c4: +5%)
   a.prefetch_rows = static_cast<double>(pitch) * n * 4 > 96.0 * (1 << 20) ? 1 : 0;

@@ -65,7 +65,6 @@ struct SolverArgs {
   int32_t n;
   int32_t W;          // column slab per CTA (power of two >= 4); G*W >= n
   int32_t seed;       // 0: u = v = 0 (solve_km), 1: reductions (solve_batched_km)
-  int32_t continue_bfs;
   int32_t prefetch_rows;  // L2 bulk prefetch of appended rows (matrix larger than L2)
   int32_t slab_cache;     // grid / sharded engines: row roots + slab matches in shared memory
   unsigned long long deadline_ns;  // %globaltimer deadline, 0 = none
@@ -99,7 +98,6 @@ struct BatchArgs {
   int32_t batch;
   int32_t n;
   int32_t seed;
-  int32_t continue_bfs;
   int32_t* row_to_col;   // batch x n
   int64_t* u;            // batch x n
   int64_t* v;            // batch x n
@@ -123,7 +121,6 @@ struct WarpArgs {
   int32_t n;
   int32_t pitch;
   int32_t seed;
-  int32_t continue_bfs;
   int32_t* row_to_col;   // batch x n
   int64_t* u;            // batch x n
   int64_t* v;            // batch x n

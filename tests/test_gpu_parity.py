@@ -20,7 +20,7 @@ import pytest
 import oracle as O
 from paper_2005_01182_b200 import KMB_SEED_BATCHED, KMB_SEED_KM, KmbError
 from paper_2005_01182_b200 import workloads as W
-from paper_2005_01182_b200.api import OPT_CONTINUE_BFS, OPT_ENGINE, OPT_MAX_CTAS
+from paper_2005_01182_b200.api import OPT_ENGINE, OPT_MAX_CTAS
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
@@ -156,16 +156,12 @@ def test_cta_counts(solver, maxg):
     check_against(r, ref, c)
 
 
-@pytest.mark.parametrize("cont", [0, 1])
-def test_continue_bfs_same_duals(solver, cont):
-    c = W.CONFIGS["c1"].make()
-    ref = O.ref_solve_batched_km(c)
-    solver.set_option(OPT_CONTINUE_BFS, cont)
-    try:
-        r = solver.solve(c, KMB_SEED_BATCHED)
-    finally:
-        solver.set_option(OPT_CONTINUE_BFS, 0)
-    check_against(r, ref, c)
+def test_removed_options_rejected(solver):
+    """Options 2 (continue BFS) and 5 (16-bit warp mode) of ABI 1 were removed:
+    setting them is an error, not a silent no-op."""
+    for opt in (2, 5):
+        with pytest.raises(KmbError, match="unknown option"):
+            solver.set_option(opt, 1)
 
 
 def test_matching_equals_mirror(solver):

@@ -6,7 +6,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from paper_2005_01182_b200 import Solver, workloads as W
-from paper_2005_01182_b200.api import OPT_CONTINUE_BFS
 
 B, N = 4096, 128
 c = W.CONFIGS["c3"].make()
@@ -35,11 +34,8 @@ def timed(call, steps=20):
 
 
 out = {}
-for opt in (0, 1):
-    s.set_option(OPT_CONTINUE_BFS, opt)
-    out[f"async_continue_bfs_{opt}_ms"] = timed(lambda: s.solve_batch_async(dc, B, N, 1, r2c, u, v, tot, status))
-    out[f"tot_fnv_{opt}"] = W.fnv1a64(tot.cpu().numpy())
-s.set_option(OPT_CONTINUE_BFS, 0)
+out["async_ms"] = timed(lambda: s.solve_batch_async(dc, B, N, 1, r2c, u, v, tot, status))
+out["tot_fnv"] = W.fnv1a64(tot.cpu().numpy())
 hc = torch.from_numpy(c).pin_memory()
 hr = [torch.empty((B, N), dtype=torch.int32).pin_memory(), torch.empty((B, N), dtype=torch.int64).pin_memory(),
       torch.empty((B, N), dtype=torch.int64).pin_memory(), torch.empty(B, dtype=torch.int64).pin_memory()]

@@ -10,7 +10,7 @@ from paper_2005_01182_b200 import workloads as W
 INF = np.iinfo(np.int64).max
 
 
-def solve(C, seed=1):
+def solve(C, seed=1, continue_bfs=False):
     n = C.shape[0]
     C = C.astype(np.int64)
     u = C.min(1) if seed == 1 else np.zeros(n, np.int64)
@@ -22,7 +22,8 @@ def solve(C, seed=1):
     w = u.copy(); root = np.arange(n); tree_par = np.full(n, -1)
     rows = list(range(n)); head = 0; D = 0; first = seed == 1; nfree = n; ep = 0
     stats = dict(epochs=0, relaxed=0, rerelax_full=0, dirty=0, resolved=0, epochs_all_resolved=0,
-                 rerelax_rows_needed=0)
+                 rerelax_rows_needed=0, rounds=0)
+    pending = []  # continue_bfs: free columns found earlier in this epoch
     claim_ep = np.full(n, -1); claim_col = np.zeros(n, np.int64)
     dirty_cols = None
 
@@ -41,6 +42,7 @@ def solve(C, seed=1):
             k2v[j2] = xv[better2]; k2r[j2] = i
 
     while nfree > 0:
+        stats["rounds"] += 1
         if dirty_cols is not None:
             # epoch start: survivors over the dirty columns only (key1 and key2 from scratch)
             if len(dirty_cols):
@@ -55,7 +57,7 @@ def solve(C, seed=1):
             v = k1v.copy(); first = False
         s = np.where(rcol, INF, k1v - v)
         m = s.min()
-        if m > D:
+        if m > D and not pending:
             D = m
         tight = np.nonzero(~rcol & (k1v - v == D))[0]
         found = []
@@ -68,6 +70,17 @@ def solve(C, seed=1):
                 found.append(j)
             else:
                 w[i2] = u[i2] - D; root[i2] = rt; rows.append(i2)
+        if continue_bfs:
+            nrow_before = head
+            pending += found
+            # keep growing while the tight closure still adds rows
+            if len(rows) > head or (found and m <= D):
+                if len(rows) > head:
+                    continue
+            found = pending
+            pending = []
+            if not found:
+                continue
         if not found:
             continue
         relax(rows[head:]); stats["relaxed"] += len(rows) - head; head = len(rows)
@@ -121,6 +134,16 @@ def solve(C, seed=1):
     tot = int(C[np.arange(n), match_row].sum())
     return tot, u, v, stats
 
+
+if __name__ == "__main__" and os.environ.get("CFG"):
+    import oracle as O
+    c = W.CONFIGS[os.environ["CFG"]].make()
+    for cb in (False, True):
+        tot, u, v, st = solve(c, 1, cb)
+        ref = O.ref_solve_batched_km(c) if c.shape[0] <= 1024 else None
+        ok = ref is None or (tot == ref.total_cost and np.array_equal(u, ref.u))
+        print("continue_bfs", cb, "ok", ok, {k: st[k] for k in ("rounds", "epochs", "relaxed", "rerelax_full")})
+    sys.exit(0)
 
 if __name__ == "__main__":
     import oracle as O
