@@ -235,12 +235,19 @@ def cpu_baselines_single() -> dict:
         r = O.kmo_solve_km_seeded(mats["c5"])
         return time.perf_counter() - t0, int(r.total_cost)
 
+    def run_c3_one_core():  # config 3 on 1 core as well as on all of them
+        c3 = _gen_c3_isolated(0, 512)
+        _, w = O.ref_solve_many_i32(c3, mode=1, nthreads=1)
+        return c3.shape[0] / w
+
     workers = max(2, min(len(jobs) + 1, (os.cpu_count() or 2) - 1))
     t0 = time.perf_counter()
     with ThreadPoolExecutor(workers) as ex:
         f5 = ex.submit(run_c5)
+        f3 = ex.submit(run_c3_one_core)
         res = list(ex.map(run, sorted(jobs, key=lambda j: j[0] != "c4")))  # long jobs first
         c5_s, c5_tot = f5.result()
+        c3_rate = f3.result()
     out = {}
     for key in ("c1", "c2", "c4"):
         d = {"n": int(mats[key].shape[0]), "cores": 1, "kind": "reference"}
@@ -254,6 +261,8 @@ def cpu_baselines_single() -> dict:
                  "note": "seeded e-maxx restatement (oracle/km_oracle.c, duals equal to the "
                          "reference's, tests/test_oracle.py); the reference solve_batched_km "
                          "is estimated at ~1 h here (SURVEY 8(c)); timed once"}
+    out["c3_one_core"] = {"value": c3_rate, "unit": "solves/s", "cores": 1, "kind": "reference",
+                          "sample": "the first 512 config-3 instances, solve_batched_km at lossless B"}
     out["wall_s"] = time.perf_counter() - t0
     out["cpu"] = cpu_model()
     out["host_threads"] = os.cpu_count()

@@ -16,6 +16,7 @@
 #include "ot/core.hpp"
 #include "ot/datasets.hpp"
 #include "ot/hungarian.hpp"
+#include "ot/io.hpp"
 #include "ot/netsimplex.hpp"
 #include "kmb_ot.hpp"
 #include "oracle.hpp"    // the reference's exhaustive oracles (proj/tests/oracle.hpp)
@@ -205,6 +206,41 @@ int main() {
     for (const Flow::Entry& e : br.flow.entries())
       CHECK(bd.u[e.i] + bd.v[e.j] == q.chat[static_cast<size_t>(e.i) * unit.n + e.j]);
     std::printf("criterion 9: km / batched km certificates at n = 200\n");
+  }
+  // the dense text format (io.cpp:57-75) feeding the B200 plugins: save, load
+  // back through the reference's own loader, solve through run_suite beside
+  // the reference solvers, point-cloud form too (io.cpp:77-110:
+  // costs materialised by the loader, then solved)
+  {
+    const std::string dense = "/tmp/kmb_harness_dense.txt", pts = "/tmp/kmb_harness_points.txt";
+    save_instance_dense(insts[2], dense);
+    PointCloudDistribution a, b;
+    a.dim = b.dim = 2;
+    std::mt19937 prng(11);
+    std::uniform_real_distribution<double> ud(0.0, 1.0);
+    for (int k = 0; k < 64; ++k) {
+      for (PointCloudDistribution* d : {&a, &b}) {
+        d->coords.push_back(ud(prng));
+        d->coords.push_back(ud(prng));
+        d->weights.push_back(1);
+      }
+    }
+    save_instance_points(a, b, 1e6, pts);
+    for (const std::string& path : {dense, pts}) {
+      const OTInstance inst = load_instance(path);
+      const int64_t B = std::max<int64_t>(inst.max_cost(), 1);
+      CalibrationEntry ce;
+      ce.B = B;
+      const std::vector<SolverSpec> roster = {make_solver("km"), km_b200_spec(),
+                                              make_solver("batched_km", &ce), batched_km_b200_spec(B)};
+      const std::vector<BenchRecord> recs = run_suite({inst}, roster, cfg);
+      CHECK(recs.size() == 4);
+      for (const BenchRecord& r : recs) {
+        std::printf("%-24s %-16s obj=%.0f exact=%.0f conv=%d\n", r.instance.c_str(), r.solver.c_str(),
+                    r.objective, r.exact_objective, r.converged ? 1 : 0);
+        CHECK(r.applicable && r.converged && r.objective == r.exact_objective);
+      }
+    }
   }
   std::printf("harness: %d failed\n", g_fail);
   return g_fail ? 1 : 0;
