@@ -415,7 +415,8 @@ def extras_single(solver) -> dict:
     committed reference golden."""
     import torch
     from paper_2005_01182_b200 import workloads as W
-    names = {6: "CTA", 8: "single-CTA (512 threads)", 5: "cluster (DSMEM state)", 1: "grid"}
+    names = {6: "CTA", 8: "single-CTA (512 threads)", 5: "cluster (DSMEM state)", 1: "grid",
+             11: "replicated cluster (16 CTAs, row state per CTA)"}
     golden = _golden()
     out = {}
     for key in ("c1", "c2", "c4"):

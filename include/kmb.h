@@ -68,13 +68,16 @@ enum kmb_option {
      incremental-epoch engines never read it, and a CPU model of them measured
      more rounds with it (config 1: 185 -> 236; config 3: 368 -> 379) */
   KMB_OPT_ENGINE = 3,       /* 0 auto: single instances CTA n<=256, single-CTA
-                               n<=3072, cluster n<=5120, grid beyond; batches
-                               warp or CTA (n<=256, by residency), single-CTA
-                               (n<=4096);
+                               n<=1792, replicated cluster n<=4608, grid beyond;
+                               batches warp or CTA (n<=256, by residency),
+                               single-CTA (n<=4096);
                                1 grid (persistent), 4 warp (n <= 256),
                                5 cluster (grid engine on one <=16-CTA cluster),
                                6 CTA (n <= 256),
-                               8 single-CTA (one 512-thread CTA, n <= 4096);
+                               8 single-CTA (one 512-thread CTA, n <= 4096),
+                               11 replicated cluster (one <=16-CTA cluster per
+                               instance, row state replicated per CTA,
+                               n <= 5120; KMB_OPT_MAX_CTAS = cluster size);
                                stats->engine 7 = column-sharded (host
                                exchange), 9 = wide (int64 costs,
                                kmb_solve_i64), 10 = column-sharded (device

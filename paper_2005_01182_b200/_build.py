@@ -21,7 +21,7 @@ GEN_SO = os.path.join(PKG, "libkmb_gen.so")
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["kmb_solver.cu", "kmb_batch.cu", "kmb_warp.cu", "kmb_shard.cu", "kmb_costs.cu",
-              "kmb_auction.cu", "kmb_big.cu", "kmb_wide.cu", "kmb_shard_dev.cu", "kmb_capi.cu"]
+              "kmb_auction.cu", "kmb_big.cu", "kmb_cluster.cu", "kmb_wide.cu", "kmb_shard_dev.cu", "kmb_capi.cu"]
 CU_HEADERS = ["kmb_common.cuh", "kmb_internal.h", "kmb_launch.h", "kmb_shard_proto.h", "kmb_stage.h"]
 
 

@@ -189,8 +189,8 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
       c->pipeline = value;
       return KMB_OK;
     case KMB_OPT_ENGINE:
-      if (value < 0 || value > 8 || value == 2 || value == 3 || value == 7)
-        return fail(KMB_EINVAL, "kmb_set_option: engine must be 0, 1, 4, 5, 6 or 8");
+      if (value < 0 || value > 11 || value == 2 || value == 3 || value == 7 || value == 9 || value == 10)
+        return fail(KMB_EINVAL, "kmb_set_option: engine must be 0, 1, 4, 5, 6, 8 or 11");
       c->engine = static_cast<int>(value);
       return KMB_OK;
     default: return fail(KMB_EINVAL, "kmb_set_option: unknown option");
@@ -297,6 +297,24 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // instances [lo, lo + cnt) on engine eng, stream s
   auto launch = [&](int lo, int cnt, int eng, cudaStream_t s) -> cudaError_t {
     const size_t ro = static_cast<size_t>(lo) * n;
+    if (eng == 11) {  // replicated cluster engine: one <=16-CTA cluster per instance
+      kmb::BigArgs a{};
+      a.C = dcost + ro * n;
+      a.ld = n;
+      a.inst_stride = static_cast<int64_t>(n) * n;
+      a.batch = cnt;
+      a.n = n;
+      a.seed = seed;
+      a.deadline_ns = time_budget_s > 0.0 ? static_cast<int64_t>(time_budget_s * 1e9) : 0;
+      a.row_to_col = dr2c + ro;
+      a.u = du + ro;
+      a.v = dv + ro;
+      a.total_cost = dtot + lo;
+      a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
+      a.status = status_base + lo;
+      const int G = c->max_ctas > 0 ? static_cast<int>(std::min<int64_t>(c->max_ctas, 16)) : 16;
+      return kmb::launch_cluster(a, G, c->sm_count, s);
+    }
     if (eng == 8) {
       kmb::BigArgs a{};
       a.C = src + ro * np;
@@ -492,8 +510,10 @@ int kmb_solve_batch_i32(kmb_context* c, const int32_t* costs, int32_t batch, int
   if (n > kmb::big_max_n())
     return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > " + std::to_string(kmb::big_max_n()) +
                                 " (use kmb_solve_i32 per instance)");
-  if (n > kmb::warp_max_n() && c->engine != 0 && c->engine != 8)
-    return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > 256 needs the single-CTA engine (8)");
+  if (n > kmb::warp_max_n() && c->engine != 0 && c->engine != 8 && c->engine != 11)
+    return fail(KMB_EINVAL, "kmb_solve_batch_i32: n > 256 needs the single-CTA (8) or cluster (11) engine");
+  if (c->engine == 11 && n > kmb::cluster_max_n())
+    return fail(KMB_EINVAL, "kmb_solve_batch_i32: engine 11 takes n <= " + std::to_string(kmb::cluster_max_n()));
   KMB_CUDA(cudaSetDevice(c->device));
   return solve_batch_impl(c, costs, batch, n, seed, row_to_col, u, v, total_cost, stats, who,
                           c->engine);
@@ -668,17 +688,20 @@ int kmb_solve_i32(kmb_context* c, const int32_t* cost, int32_t n, int64_t ld, in
   int engine = c->engine;
   // auto (measured crossovers): one CTA per instance up to
   // n = 256 (no time budget there; c1 0.20 ms vs 0.55 for one warp), one
-  // 512-thread CTA up to n = 3072 (c2 8.9 ms vs 24 on a cluster), one
-  // thread-block cluster up to n = 5120 (c4: 129 ms vs 157 on one CTA, 160 on
-  // the grid), the whole-GPU grid beyond (n = 6144: 64 vs 78 ms uniform,
-  // 269 vs 298 geometric)
+  // 512-thread CTA up to n = 1792 (c2 8.5 ms vs 24 on a cluster), one
+  // thread-block cluster with replicated row state up to n = 4608, the
+  // whole-GPU grid beyond (n = 6144: 64 vs 78 ms uniform, 269 vs 298 geometric)
+  // round 2: the replicated cluster engine takes 1792 < n <= 4608 (c4 84 ms vs
+  // 130 on engine 5; uniform n = 3072 23 vs 34 ms on the single CTA, n = 4096 31
+  // vs 43 on engine 5; at n = 5120 it ties the grid engine)
   if (engine == 0)
-    engine = (n <= 256 && time_budget_s <= 0.0) ? 6 : n <= 3072 ? 8 : (n <= 5120 ? 5 : 1);
+    engine = (n <= 256 && time_budget_s <= 0.0) ? 6 : n <= 1792 ? 8 : (n <= 4608 ? 11 : 1);
   if (engine == 6 && n > kmb::batch_max_n()) engine = 1;
   if (engine == 4 && n > kmb::warp_max_n()) engine = 1;
   if (engine == 8 && n > kmb::big_max_n()) engine = 1;
-  if (engine == 4 || engine == 6 || engine == 8) {
-    if (time_budget_s > 0.0 && engine != 8)
+  if (engine == 11 && n > kmb::cluster_max_n()) engine = 1;
+  if (engine == 4 || engine == 6 || engine == 8 || engine == 11) {
+    if (time_budget_s > 0.0 && engine != 8 && engine != 11)
       return fail(KMB_EINVAL, "kmb_solve_i32: the per-instance engines have no time budget; use engine 1");
     const int32_t* src = cost;
     if (ld != n) {  // compact into the batch buffer

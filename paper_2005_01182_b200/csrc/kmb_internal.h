@@ -154,6 +154,10 @@ struct BigArgs {
 size_t big_smem_bytes(int n);
 int big_max_n();
 cudaError_t launch_big(const BigArgs& a, int sm_count, cudaStream_t st);
+// replicated cluster engine (kmb_cluster.cu): one <=16-CTA cluster per instance
+size_t cluster_smem_bytes(int n, int G);
+int cluster_max_n();
+cudaError_t launch_cluster(const BigArgs& a, int G, int sm_count, cudaStream_t st);
 // Gauss-Seidel auction (kmb_auction.cu)
 struct AuctionArgs {
   const int32_t* C;     // batch instances, row stride ld, instance stride inst_stride

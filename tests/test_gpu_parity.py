@@ -108,7 +108,7 @@ def test_known_constant(solver):  # :133-142: constant 6x6 cost 4 -> 24, one pha
     assert r.stats["dual_steps"] == 0
 
 
-@pytest.mark.parametrize("engine", [1, 4, 5, 6, 8])
+@pytest.mark.parametrize("engine", [1, 4, 5, 6, 8, 11])
 @pytest.mark.parametrize("seed", [KMB_SEED_KM, KMB_SEED_BATCHED])
 def test_random_small_vs_reference(solver, engine, seed):
     rng = np.random.default_rng(100 + 10 * engine + seed)
@@ -126,7 +126,7 @@ def test_random_small_vs_reference(solver, engine, seed):
         solver.set_option(OPT_ENGINE, 0)
 
 
-@pytest.mark.parametrize("engine", [1, 5, 8])
+@pytest.mark.parametrize("engine", [1, 5, 8, 11])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 13, 31, 33, 127, 129, 200, 255, 257, 300, 513, 1000, 1001,
                                1025, 2049, 3000])
 def test_ragged_sizes_grid(solver, n, engine):
@@ -156,6 +156,26 @@ def test_cta_counts(solver, maxg):
     check_against(r, ref, c)
 
 
+@pytest.mark.parametrize("G", [1, 2, 3, 5, 16])
+def test_cluster_engine_sizes(solver, G):
+    """The replicated cluster engine (11) at any cluster size (KMB_OPT_MAX_CTAS),
+    columns split unevenly, CTAs without columns, 1-4 columns per thread."""
+    rng = np.random.default_rng(40 + G)
+    solver.set_option(OPT_ENGINE, 11)
+    solver.set_option(OPT_MAX_CTAS, G)
+    try:
+        for n in (1, 17, 255, 600, 1500, 2100):
+            c = rng.integers(0, int(rng.choice([3, 1000, 10**6])), size=(n, n)).astype(np.int32)
+            for seed in (KMB_SEED_BATCHED, KMB_SEED_KM):
+                ref = O.ref_solve_batched_km(c) if seed == KMB_SEED_BATCHED else O.ref_solve_km(c)
+                r = solver.solve(c, seed)
+                assert r.stats["engine"] == 11
+                check_against(r, ref, c)
+    finally:
+        solver.set_option(OPT_ENGINE, 0)
+        solver.set_option(OPT_MAX_CTAS, 0)
+
+
 def test_removed_options_rejected(solver):
     """Options 2 (continue BFS) and 5 (16-bit warp mode) of ABI 1 were removed:
     setting them is an error, not a silent no-op."""
@@ -173,7 +193,7 @@ def test_matching_equals_mirror(solver):
         n = int(rng.integers(2, 300))
         c = rng.integers(0, 20, size=(n, n)).astype(np.int32)
         mi = O.mirror_solve_incr(c, 1)
-        engines = [1, 5, 8] + ([4, 6] if n <= 256 else [])
+        engines = [1, 5, 8, 11] + ([4, 6] if n <= 256 else [])
         for engine in engines:
             solver.set_option(OPT_ENGINE, engine)
             r = solver.solve(c, KMB_SEED_BATCHED)
@@ -208,7 +228,7 @@ def test_out_of_device_range_rejected(solver):
     check_against(solver.solve(c, KMB_SEED_BATCHED), ref, c)
 
 
-@pytest.mark.parametrize("engine", [1, 5, 8])
+@pytest.mark.parametrize("engine", [1, 5, 8, 11])
 def test_time_budget(solver, engine):
     c = W.CONFIGS["c2"].make()
     solver.set_option(OPT_ENGINE, engine)
@@ -313,7 +333,7 @@ def test_config3_all_instances_vs_reference(solver, engine):
             np.testing.assert_array_equal(r.row_to_col[t], O.ref_solve_batched_km(c[t]).row_to_col)
 
 
-@pytest.mark.parametrize("key,engine", [("c4", 0), ("c4", 1), ("c4", 5), ("c4", 8),
+@pytest.mark.parametrize("key,engine", [("c4", 0), ("c4", 1), ("c4", 5), ("c4", 8), ("c4", 11),
                                         ("c5", 0), ("c5", 5)])
 def test_large_config_golden(solver, key, engine):
     """Configs 4 and 5 on every engine that accepts them (0 = auto: cluster for

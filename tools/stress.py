@@ -67,7 +67,7 @@ while time.time() - t0 < budget:
     c = rng.integers(0, hi, size=(n, n)).astype(np.int32)
     seed = int(rng.choice([KMB_SEED_BATCHED, KMB_SEED_KM]))
     ref = O.ref_solve_batched_km(c) if seed == KMB_SEED_BATCHED else O.ref_solve_km(c)
-    engines = [1, 5] + ([4, 6] if n <= 256 else []) + ([8] if n <= 4096 else [])
+    engines = [1, 5] + ([4, 6] if n <= 256 else []) + ([8] if n <= 4096 else []) + ([11] if n <= 5120 else [])
     for eng in engines:
         s.set_option(OPT_ENGINE, eng)
         r1 = s.solve(c, seed)
