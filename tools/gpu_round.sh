@@ -21,7 +21,7 @@ if [[ $stages == *l* ]]; then
       --log-file $O/${tag}_launches.csv $B > $O/${tag}_ncu_launches.log 2>&1; echo "launches exit $?"
 fi
 if [[ $stages == *n* ]]; then
-  for spec in "c3 k_warp_batch 0" "c5 k_solve 0" "c4 k_solve 0" "c2 k_big 0" "c1 k_cta_batch 0"; do
+  for spec in "c3 k_warp_batch 0" "c5 k_solve 0" "c4 k_cluster 0" "c2 k_big 0" "c1 k_cta_batch 0"; do
     set -- $spec; cfg=$1; k=$2; eng=$3
     P="python tools/prof_run.py --config $cfg --iters 2 --engine $eng"
     timeout 600 $P > $O/${tag}_prof_${cfg}_plain.log 2>&1 && \
