@@ -230,8 +230,14 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // resident (1.00 ms at 4096 vs 1.7 for CTAs)
   const bool auto_engine = engine == 0 || engine == 1 || engine == 5;
   const int cap6 = auto_engine ? kmb::cta_batch_capacity(n, c->sm_count) : 0;
-  // n > 256: one 512-thread CTA per instance (single-CTA engine, n <= 4096)
-  auto pick = [&](int cnt) { return n > kmb::warp_max_n() ? 8 : (cnt <= cap6 ? 6 : 4); };
+  // n > 256: one 512-thread CTA per instance (single-CTA engine, n <= 4096),
+  // or, for up to #SMs / 32 instances with 1792 < n <= 4608, one replicated
+  // 16-CTA cluster each (4 x n = 3072: 43.6 -> 26.0 ms; at 9 clusters the
+  // single-CTA engine is ahead again: 9 x n = 2500 38.5 vs 40.9 ms)
+  auto pick = [&](int cnt) {
+    if (n <= kmb::warp_max_n()) return cnt <= cap6 ? 6 : 4;
+    return (n > 1792 && n <= 4608 && cnt * 32 <= c->sm_count) ? 11 : 8;
+  };
   if (auto_engine) engine = pick(batch);
   // Host input: stream the batch in chunks, each chunk's kernel starting as soon
   // as its H2D copy lands and its results leaving as soon as it ends, so the
