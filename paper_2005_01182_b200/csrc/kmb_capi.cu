@@ -537,8 +537,8 @@ int kmb_solve_batch_async_i32(kmb_context* c, const int32_t* costs, int32_t batc
   if (seed != KMB_SEED_KM && seed != KMB_SEED_BATCHED) return fail(KMB_EINVAL, std::string(who) + ": bad seed");
   if (n > kmb::big_max_n())
     return fail(KMB_EINVAL, std::string(who) + ": n > " + std::to_string(kmb::big_max_n()));
-  if (n > kmb::warp_max_n() && c->engine != 0 && c->engine != 8)
-    return fail(KMB_EINVAL, std::string(who) + ": n > 256 needs the single-CTA engine (8)");
+  if (n > kmb::warp_max_n() && c->engine != 0 && c->engine != 8 && c->engine != 11)
+    return fail(KMB_EINVAL, std::string(who) + ": n > 256 needs the single-CTA (8) or cluster (11) engine");
   KMB_CUDA(cudaSetDevice(c->device));
   for (const void* p : {static_cast<const void*>(costs), static_cast<const void*>(row_to_col),
                         static_cast<const void*>(u), static_cast<const void*>(v),

@@ -176,6 +176,28 @@ def test_cluster_engine_sizes(solver, G):
         solver.set_option(OPT_MAX_CTAS, 0)
 
 
+@pytest.mark.parametrize("G,b,n", [(4, 5, 300), (16, 23, 200), (2, 80, 97)])
+def test_cluster_engine_batches(solver, G, b, n):
+    """Engine 11 on batches: several clusters side by side and, past #SMs / G
+    clusters, several instances per cluster in turn (its per-instance state
+    reset); every instance against the reference."""
+    rng = np.random.default_rng(G * 1000 + b)
+    c = rng.integers(0, 10**5, size=(b, n, n)).astype(np.int32)
+    solver.set_option(OPT_ENGINE, 11)
+    solver.set_option(OPT_MAX_CTAS, G)
+    try:
+        r = solver.solve_batch(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_ENGINE, 0)
+        solver.set_option(OPT_MAX_CTAS, 0)
+    assert r.stats["engine"] == 11
+    for t in range(b):
+        ref = O.ref_solve_batched_km(c[t])
+        assert r.total_cost[t] == ref.total_cost
+        np.testing.assert_array_equal(r.u[t], ref.u)
+        np.testing.assert_array_equal(r.v[t], ref.v)
+
+
 def test_removed_options_rejected(solver):
     """Options 2 (continue BFS) and 5 (16-bit warp mode) of ABI 1 were removed:
     setting them is an error, not a silent no-op."""
