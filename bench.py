@@ -364,9 +364,14 @@ def extras_c5(solver, hbm_peak: float) -> dict:
     rd = 4.0 * n * (st.rows_scanned + 2 * n) + 16.0 * st.segment_rows
     eff = 4.0 * n * n * (st.phases + 2)
     prof = _profile("r02_ncu_solvers.json").get("c5_k_solve_grid", {})
+    dram = prof.get("dram_bytes")
     scan = {"bound": "latency", "kernel": "k_solve<GridBarrier>", "achieved": rd / t / 1e9,
             "peak": hbm_peak, "unit": "GB/s", "frac": rd / t / 1e9 / hbm_peak,
-            "traffic": prof.get("dram_bytes"),
+            "traffic": dram,
+            # SURVEY 8(d)1's kernel-level figure: ncu DRAM bytes of the in-situ
+            # solve over its ncu duration (profiles/r02_ncu_solvers.json)
+            "ncu_dram_gbs": (dram / prof["duration_ns"]) if dram and prof.get("duration_ns") else None,
+            "ncu_dram_frac": (dram / prof["duration_ns"] / hbm_peak) if dram and prof.get("duration_ns") else None,
             "note": "bytes the scans read (4n per relaxed row, 16 B per dirty row-segment, "
                     "2 reduction passes) / solve time; 15.5k dependent rounds bound it "
                     "(profiles/r02_ncu_solvers.json)"}
