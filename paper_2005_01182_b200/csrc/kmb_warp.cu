@@ -110,6 +110,7 @@ struct Keys<false> {
   __device__ static int32_t val(K k) { return static_cast<int32_t>(static_cast<int64_t>(k >> 32) - KMB_BIAS); }
   __device__ static int32_t row(K k) { return static_cast<int32_t>(static_cast<uint32_t>(k)); }
   __device__ static K kmin(K a, K b) { return a < b ? a : b; }
+  __device__ static K from_wide(uint64_t k) { return k; }
 };
 template <>
 struct Keys<true> {
@@ -125,6 +126,11 @@ struct Keys<true> {
   __device__ static int32_t val(K k) { return static_cast<int32_t>(k >> 8) - NB; }
   __device__ static int32_t row(K k) { return static_cast<int32_t>(k & 0xffu); }
   __device__ static K kmin(K a, K b) { return min(a, b); }
+  // a wide key (c - w + 2^30, row) as a narrow one (c - w + 2^22, row)
+  __device__ static K from_wide(uint64_t k) {
+    if (k == Keys<false>::INF) return INF;
+    return (static_cast<uint32_t>(Keys<false>::val(k) + NB) << 8) | static_cast<uint32_t>(k & 0xffu);
+  }
 };
 
 struct WarpSmem {
@@ -138,7 +144,7 @@ struct WarpSmem {
 // RB: rows per relax batch; CACHE: matched rows and their u in registers
 template <int CPL, bool NARROW, int RB, bool CACHE>
 __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* Cm, int inst,
-                                              const WarpSmem& S, int lane) {
+                                              const WarpSmem& S, int lane, const uint64_t (&k0)[CPL]) {
   using KO = Keys<NARROW>;
   using K = typename KO::K;
   constexpr uint32_t FULL = 0xffffffffu;
@@ -169,7 +175,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   for (int q = 0; q < CPL; ++q) {
     v[q] = 0;
     dc[q] = 0;
-    key[q] = KO::INF;
+    key[q] = KO::from_wide(k0[q]);  // every row relaxed once by the validation pass
     if (c0 + q >= n) pad |= 1u << q;
   }
   uint32_t rch = pad;  // bit q: column c0+q reached (padding counts as reached)
@@ -181,9 +187,9 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     mi2[q] = -1;
     mu2[q] = 0;
   }
-  int nrows = n, head = 0, nfree = n;  // rows[0, nrows) reached; [head, nrows) to relax
+  int nrows = n, head = n, nfree = n;  // rows[0, nrows) reached; [head, nrows) to relax
   int32_t D = 0;
-  int epochs = 0, dual_steps = 0, rows_scanned = 0, rounds = 0;
+  int epochs = 0, dual_steps = 0, rows_scanned = n, rounds = 0;
   int status = 0;
   const long long t_start = clock64();
   long long cyc[4] = {0, 0, 0, 0};  // relax, min, absorb, epoch end
@@ -456,14 +462,21 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
     __syncwarp();
     // validation (core.cpp:144-145 + device range) and row reductions
     // (hungarian.cpp:323-327): the warp walks the rows, lanes across columns,
-    // 8 rows in flight (loads first, then the per-row reductions)
+    // IB rows in flight (loads first, then the per-row reductions)
+    // The same pass is the search's first relax (every row reached at D = 0
+    // with w = u0): the keys are folded here, in the wide (value, row) form
+    // the key width is picked from afterwards, so the matrix is read once less.
     int32_t lo_all = 0x7fffffff, hi_all = 0;
-    for (int i0 = 0; i0 < n; i0 += 8) {
-      RowVec<CPL> cv[8];
+    uint64_t k0[CPL];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) cv[k] = load_row<CPL>(Cm + static_cast<int64_t>(min(i0 + k, n - 1)) * np + c0);
+    for (int q = 0; q < CPL; ++q) k0[q] = Keys<false>::INF;
+    constexpr int IB = CPL >= 8 ? 4 : 8;  // rows in flight (8 columns a lane: fewer, spills)
+    for (int i0 = 0; i0 < n; i0 += IB) {
+      RowVec<CPL> cv[IB];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < IB; ++k) cv[k] = load_row<CPL>(Cm + static_cast<int64_t>(min(i0 + k, n - 1)) * np + c0);
+#pragma unroll
+      for (int k = 0; k < IB; ++k) {
         const int i = i0 + k;
         if (i >= n) break;  // warp-uniform
         int32_t lo = 0x7fffffff, hi = 0;
@@ -476,8 +489,11 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
         lo = __reduce_min_sync(FULL, lo);
         lo_all = min(lo_all, lo);
         hi_all = max(hi_all, hi);
+        const int32_t u0 = a.seed == 1 ? lo : 0;
+        const uint32_t tag = Keys<false>::tag(u0, i);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) k0[q] = Keys<false>::kmin(k0[q], Keys<false>::make(cv[k].x[q], tag, i));
         if (lane == (i & 31)) {
-          const int32_t u0 = a.seed == 1 ? lo : 0;
           S.u[i] = u0;
           S.w[i] = u0;
         }
@@ -487,8 +503,8 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
     int status = lo_all < 0 ? 2 : (hi_all >= (1 << 29) ? 3 : 0);
     __syncwarp();
     if (status == 0) {
-      status = hi_all < (1 << 21) ? solve_instance<CPL, true, RB, CK>(a, Cm, inst, S, lane)
-                                  : solve_instance<CPL, false, RB, CK>(a, Cm, inst, S, lane);
+      status = hi_all < (1 << 21) ? solve_instance<CPL, true, RB, CK>(a, Cm, inst, S, lane, k0)
+                                  : solve_instance<CPL, false, RB, CK>(a, Cm, inst, S, lane, k0);
     } else {
       for (int k = lane; k < n; k += 32) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
       if (lane == 0) a.total_cost[inst] = 0;
