@@ -111,6 +111,10 @@ struct Keys<false> {
   __device__ static int32_t row(K k) { return static_cast<int32_t>(static_cast<uint32_t>(k)); }
   __device__ static K kmin(K a, K b) { return a < b ? a : b; }
   __device__ static K from_wide(uint64_t k) { return k; }
+  // row-list entry: (row, tag); the row's byte offset is row * pitch bytes
+  __device__ static int2 ent(int32_t row, uint32_t tag, uint32_t) { return make_int2(row, static_cast<int32_t>(tag)); }
+  __device__ static int32_t erow(int2 e) { return e.x; }
+  __device__ static uint32_t eoff(int2 e, uint32_t pb) { return static_cast<uint32_t>(e.x) * pb; }
 };
 template <>
 struct Keys<true> {
@@ -131,6 +135,14 @@ struct Keys<true> {
     if (k == Keys<false>::INF) return INF;
     return (static_cast<uint32_t>(Keys<false>::val(k) + NB) << 8) | static_cast<uint32_t>(k & 0xffu);
   }
+  // row-list entry: (byte offset of the row, tag); the tag's low byte is the
+  // row, so the relax adds the offset to the lane's base and nothing else
+  // (5 address instructions per row -> 2, SASS)
+  __device__ static int2 ent(int32_t row, uint32_t tag, uint32_t pb) {
+    return make_int2(static_cast<int32_t>(static_cast<uint32_t>(row) * pb), static_cast<int32_t>(tag));
+  }
+  __device__ static int32_t erow(int2 e) { return e.y & 0xff; }
+  __device__ static uint32_t eoff(int2 e, uint32_t) { return static_cast<uint32_t>(e.x); }
 };
 
 struct WarpSmem {
@@ -150,8 +162,9 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   constexpr uint32_t FULL = 0xffffffffu;
   const int n = a.n;
   const uint32_t np = static_cast<uint32_t>(a.pitch);
+  const uint32_t pb = 4u * np;  // row pitch in bytes
   const int c0 = CPL * lane;
-  const int32_t* const lb = Cm + c0;  // this lane's columns of row 0
+  const char* const lb = reinterpret_cast<const char*>(Cm + c0);  // this lane's columns of row 0
   int32_t* const u = S.u;
   int32_t* const w = S.w;
   int32_t* const root_row = S.root_row;
@@ -163,7 +176,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   int2* spare = S.spare;
   int32_t* found = reinterpret_cast<int32_t*>(spare);  // idle row list during an epoch
 
-  for (int k = lane; k < n; k += 32) rows[k] = make_int2(k, static_cast<int32_t>(KO::tag(w[k], k)));
+  for (int k = lane; k < n; k += 32) rows[k] = KO::ent(k, KO::tag(w[k], k), pb);
   if (lane == 0) {
     S.ctr[0] = n;
     S.ctr[1] = 0;
@@ -171,12 +184,20 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   K key[CPL];
   int32_t v[CPL], dc[CPL];
   uint32_t pad = 0;
+  // Narrow keys: a reached (or padding) column's v carries -RBIG while it is
+  // reached, so its slack' = val - v sits near 2^29: never the minimum, never
+  // equal to D (< 2^22) - the min and the tight test need no reached mask.
+  // (Wide keys: slack' reaches 3 * 2^29, no headroom; they keep the mask.)
+  constexpr int32_t RBIG = NARROW ? (1 << 29) : 0;
 #pragma unroll
   for (int q = 0; q < CPL; ++q) {
     v[q] = 0;
     dc[q] = 0;
     key[q] = KO::from_wide(k0[q]);  // every row relaxed once by the validation pass
-    if (c0 + q >= n) pad |= 1u << q;
+    if (c0 + q >= n) {
+      pad |= 1u << q;
+      v[q] = -RBIG;
+    }
   }
   uint32_t rch = pad;  // bit q: column c0+q reached (padding counts as reached)
   // CACHE (low-occupancy build): each column's matched row and its u in
@@ -191,6 +212,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   int32_t D = 0;
   int epochs = 0, dual_steps = 0, rows_scanned = n, rounds = 0;
   int status = 0;
+  const int round_cap = 4 * n * n + 64;
   const long long t_start = clock64();
   long long cyc[4] = {0, 0, 0, 0};  // relax, min, absorb, epoch end
   long long tl = t_start;
@@ -207,11 +229,10 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   __syncwarp();
 
   while (nfree > 0) {
-    if (rounds > 4 * n * n + 64) {  // a valid search ends in n epochs of <= 2n + 1 rounds
+    if (++rounds > round_cap) {  // a valid search ends in n epochs of <= 2n + 1 rounds
       status = -2;
       break;
     }
-    ++rounds;
     // ---- relax rows[head, nrows)  (hungarian.cpp:164-172) ----
     int r = head;
     // RB rows in flight: entries, then all row loads, then the folds
@@ -221,19 +242,19 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
 #pragma unroll
       for (int k = 0; k < RB; ++k) e[k] = rows[r + k];
 #pragma unroll
-      for (int k = 0; k < RB; ++k) cv[k] = load_row<CPL>(lb + static_cast<uint32_t>(e[k].x) * np);
+      for (int k = 0; k < RB; ++k) cv[k] = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e[k], pb)));
 #pragma unroll
       for (int k = 0; k < RB; ++k)
 #pragma unroll
         for (int q = 0; q < CPL; ++q)
-          key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), e[k].x));
+          key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), KO::erow(e[k])));
     }
     if (nrows - r == 1) {
       const int2 e = rows[r];
-      const RowVec<CPL> cv = load_row<CPL>(lb + static_cast<uint32_t>(e.x) * np);
+      const RowVec<CPL> cv = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e, pb)));
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
-        key[q] = KO::kmin(key[q], KO::make(cv.x[q], static_cast<uint32_t>(e.y), e.x));
+        key[q] = KO::kmin(key[q], KO::make(cv.x[q], static_cast<uint32_t>(e.y), KO::erow(e)));
     } else if (r < nrows) {
       // 2..RB-1 rows: one batch with the last row repeated (the fold is
       // idempotent), so all loads are in flight together
@@ -242,12 +263,12 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
 #pragma unroll
       for (int k = 0; k < RB; ++k) e[k] = rows[min(r + k, nrows - 1)];
 #pragma unroll
-      for (int k = 0; k < RB; ++k) cv[k] = load_row<CPL>(lb + static_cast<uint32_t>(e[k].x) * np);
+      for (int k = 0; k < RB; ++k) cv[k] = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e[k], pb)));
 #pragma unroll
       for (int k = 0; k < RB; ++k)
 #pragma unroll
         for (int q = 0; q < CPL; ++q)
-          key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), e[k].x));
+          key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), KO::erow(e[k])));
     }
     r = nrows;
     rows_scanned += nrows - head;
@@ -264,11 +285,11 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       s[q] = KO::val(key[q]) - v[q];
-      if (!((rch >> q) & 1)) lm = min(lm, s[q]);
+      if (NARROW || !((rch >> q) & 1)) lm = min(lm, s[q]);
     }
     const int32_t m = __reduce_min_sync(FULL, lm);
     if (m > D) {
-      if (m == 0x7fffffff) {
+      if (NARROW ? m >= (RBIG >> 1) : m == 0x7fffffff) {
         status = -2;
         break;
       }
@@ -282,7 +303,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     uint32_t tm = 0;
 #pragma unroll
     for (int q = 0; q < CPL; ++q)
-      if (!((rch >> q) & 1) && s[q] == D) tm |= 1u << q;
+      if ((NARROW || !((rch >> q) & 1)) && s[q] == D) tm |= 1u << q;
     if (tm) {
       rch |= tm;
 #pragma unroll
@@ -290,6 +311,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
         if (!((tm >> q) & 1)) continue;
         const int col = c0 + q;
         dc[q] = D;
+        v[q] -= RBIG;
         const int32_t par = KO::row(key[q]);
         tree_par[col] = par;
         const int32_t root = root_row[par];
@@ -301,7 +323,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
           const int32_t w2 = (CACHE ? mu2[CACHE ? q : 0] : u[i2]) - D;
           w[i2] = w2;
           root_row[i2] = root;
-          rows[atomicAdd(S.ctr, 1)] = make_int2(i2, static_cast<int32_t>(KO::tag(w2, i2)));
+          rows[atomicAdd(S.ctr, 1)] = KO::ent(i2, KO::tag(w2, i2), pb);
         }
       }
     }
@@ -320,7 +342,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       const int col = c0 + q;
       if ((rch >> q) & 1) {
         if (wclaimed_in(claim[root_row[tree_par[col]]], epochs)) {
-          v[q] -= D - dc[q];
+          v[q] -= D - dc[q] - RBIG;
           rch &= ~(1u << q);
           key[q] = KO::INF;
         }
@@ -358,7 +380,8 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       int2 e = make_int2(0, 0);
       if (rr < nrows) {
         e = rows[rr];
-        if (wclaimed_in(claim[root_row[e.x]], epochs)) u[e.x] = w[e.x] + D;
+        const int32_t er = KO::erow(e);
+        if (wclaimed_in(claim[root_row[er]], epochs)) u[er] = w[er] + D;
         else keep = true;
       }
       const uint32_t km = __ballot_sync(FULL, keep);
@@ -399,7 +422,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   }
 #pragma unroll
   for (int q = 0; q < CPL; ++q)
-    if (c0 + q < n) a.v[static_cast<int64_t>(inst) * n + c0 + q] = v[q];
+    if (c0 + q < n) a.v[static_cast<int64_t>(inst) * n + c0 + q] = v[q] + (((rch >> q) & 1) ? RBIG : 0);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
   if (lane == 0) {
@@ -452,7 +475,11 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
 
   for (int inst = blockIdx.x * wpb + wib; inst < a.batch; inst += gridDim.x * wpb) {
     const unsigned long long t_inst0 = globaltimer_ns();
+#ifdef KMB_WARP_ALIAS  // diagnostics: instances share KMB_WARP_ALIAS matrices (L2 footprint probe; outputs of aliased instances repeat)
+    const int32_t* Cm = a.C + static_cast<int64_t>(inst % KMB_WARP_ALIAS) * n * np;
+#else
     const int32_t* Cm = a.C + static_cast<int64_t>(inst) * n * np;
+#endif
     for (int k = lane; k < n; k += 32) {
       S.match_row[k] = -1;
       S.match_col[k] = -1;
