@@ -618,8 +618,9 @@ def main():
     # roofline of the dominant kernel (k_warp_batch at 4096 instances): its
     # compulsory bytes are each instance's matrix read once (4 n^2 per instance);
     # it is latency-bound (~377 dependent rounds per instance), so the HBM
-    # fraction is low; ncu DRAM bytes of one launch (profiles/) show how often
-    # the matrices are re-fetched because 256 MiB does not fit the 126 MB L2
+    # fraction is low; ncu DRAM bytes of one launch (profiles/) show how much is
+    # re-fetched (the 16-bit resident copy of the rows, 128 MiB, fits the L2 far
+    # better than the 256 MiB of int32 matrices)
     alg_bytes = 4.0 * N * N * count
     achieved = alg_bytes / (step_ms * 1e-3) / 1e9
     kern = ENGINES.get(engine_used, ("", "?"))[1]
@@ -654,9 +655,11 @@ def main():
                          if prof else None,
                          "note": "algorithmic bytes = each instance's 4 n^2 matrix read once; "
                                  "the kernel is bound by ~377 dependent search rounds per "
-                                 "instance, not by HBM; traffic = ncu DRAM bytes of one launch "
-                                 "(profiles/r02_ncu_batch.json): the matrices are re-fetched "
-                                 "because 256 MiB exceeds the 126 MB L2"},
+                                 "instance (issue slots and the INT pipe next), not by HBM; "
+                                 "traffic = ncu DRAM bytes of one launch "
+                                 "(profiles/r02_ncu_batch.json): the int32 matrices once, the "
+                                 "16-bit resident copy written once (128 MiB) and what the L2 "
+                                 "re-fetches of it (12x the compulsory bytes before the copy)"},
             "reference_work_equivalent": {
                 "gbs": ref_eq, "note": "SURVEY 8(d)2: 4 n^2 per phase + 2 reduction passes per "
                                        "instance over the step time: the reference's per-phase "

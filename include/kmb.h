@@ -93,6 +93,16 @@ enum kmb_option {
                                on config 3, tools/e2e_probe.py);
                                k > 0: k equal chunks (<= 64);
                                k < 0: tapered from |k| equal chunks            */
+  ,
+  KMB_OPT_RESIDENT16 = 7    /* warp engine, 64 < n <= 256: keep a 16-bit copy of
+                               every row (offsets from the row minimum) in a
+                               workspace and relax from it - half the L2
+                               footprint and bytes per row; rows, and past
+                               ~n/16 of them whole instances, that do not fit
+                               16 bits stay int32.  0 = auto (by size: n > 128
+                               from 128 MiB of matrices, n <= 128 between
+                               192 and 448 MiB), 1 = always, -1 = never.
+                               Results are identical either way.               */
 };
 
 typedef struct kmb_stats {

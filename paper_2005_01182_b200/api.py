@@ -24,7 +24,7 @@ from . import _build
 KMB_SEED_KM = 0
 KMB_SEED_BATCHED = 1
 KMB_OK, KMB_EINVAL, KMB_ENEGATIVE, KMB_ERANGE = 0, 1, 2, 3  # include/kmb.h status codes
-OPT_MAX_CTAS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_PIPELINE = 1, 3, 4, 6
+OPT_MAX_CTAS, OPT_ENGINE, OPT_WARPS_PER_SM, OPT_PIPELINE, OPT_RESIDENT16 = 1, 3, 4, 6, 7
 
 # every symbol include/kmb.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("kmb_create", "kmb_destroy", "kmb_set_stream", "kmb_set_option", "kmb_solve_i32",

@@ -78,13 +78,14 @@ struct kmb_context {
   int64_t max_ctas = 0;
   int64_t warps_per_sm = 0;  // warp engine residency bound (0 = occupancy limit)
   int64_t pipeline = 0;      // host-input batches: chunk schedule (0 = tapered auto)
+  int64_t resident16 = 0;    // warp engine 16-bit resident copy (0 auto, 1 on, -1 off)
   int engine = 0;
   int64_t last_batch = 0;  // instances of the last batch solve (kmb_last_instance_stats)
   // grid-engine workspace
   DevBuf cost, u, v, mrow, mcol, tpar, root, claim, lrow0, lrow1, lw0, lw1, found, partial,
       ctrl, obj;
   // batch workspace
-  DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus;
+  DevBuf bcost, bpad, br2c, bu, bv, btot, bstat, bstatus, b16;
   // cost construction workspace (host-resident points / output)
   DevBuf pa, pb, pout, pbad;
   // auction workspace
@@ -155,7 +156,7 @@ void kmb_destroy(kmb_context* c) {
   for (DevBuf* b : {&c->cost, &c->u, &c->v, &c->mrow, &c->mcol, &c->tpar, &c->root, &c->claim,
                     &c->lrow0, &c->lrow1, &c->lw0, &c->lw1, &c->found, &c->partial, &c->ctrl,
                     &c->obj, &c->bcost, &c->bpad, &c->br2c, &c->bu, &c->bv, &c->btot, &c->bstat,
-                    &c->bstatus, &c->pa, &c->pb, &c->pout, &c->pbad, &c->aprice, &c->ar2c, &c->atot,
+                    &c->bstatus, &c->b16, &c->pa, &c->pb, &c->pout, &c->pbad, &c->aprice, &c->ar2c, &c->atot,
                     &c->abids, &c->acomp, &c->aeps, &c->amin, &c->amax, &c->bsum, &c->w64in, &c->wchat,
                     &c->wnar, &c->wmm, &c->wr2c, &c->wu, &c->wv, &c->wtot, &c->wws64, &c->wws32})
     b->release();
@@ -183,6 +184,10 @@ int kmb_set_option(kmb_context* c, int option, int64_t value) {
   switch (option) {
     case KMB_OPT_MAX_CTAS: c->max_ctas = value; return KMB_OK;
     case KMB_OPT_WARPS_PER_SM: c->warps_per_sm = value; return KMB_OK;
+    case KMB_OPT_RESIDENT16:
+      if (value < -1 || value > 1) return fail(KMB_EINVAL, "kmb_set_option: resident16 must be -1, 0 or 1");
+      c->resident16 = value;
+      return KMB_OK;
     case KMB_OPT_PIPELINE:
       if (value < -(kmb_context::kMaxChunks / 2) || value > kmb_context::kMaxChunks)
         return fail(KMB_EINVAL, "kmb_set_option: pipeline chunk count out of range");
@@ -297,6 +302,27 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // stream-ordered calls write the statuses straight into the caller's buffer
   int32_t* const status_base = async_status ? async_status : c->bstatus.as<int32_t>();
   const int32_t* src = dcost;  // vector-load engines: rows padded to np
+  // warp engine: 16-bit resident copy of the rows (KMB_OPT_RESIDENT16)
+  uint16_t* c16 = nullptr;
+  if (warp_eng && n > 64) {
+    const size_t mat_bytes = nb * np * 4;
+    // auto (measured on one B200, ms without / with the copy):
+    //  n > 128 (8 columns a lane): from 128 MiB of matrices up - n = 256 x 700
+    //    1.75 / 1.69, x 1,024 2.16 / 1.79, x 4,096 5.58 / 4.37; n = 200 x 2,000
+    //    2.27 / 1.62; n = 160 x 4,096 2.38 / 1.79;
+    //  n <= 128: between 1.5 x the L2 and 448 MiB - config 3 (64 KiB matrices)
+    //    x 2,560 0.721 / 0.747, x 3,072 0.785 / 0.772, x 3,584 0.856 / 0.821,
+    //    x 4,096 0.956 / 0.899, x 6,000 1.452 / 1.370, x 8,192 1.753 / 1.790
+    //    (instances that start later pack while the others search); uniform
+    //    U{0..50000} x 4,096 0.603 / 0.592, x 8,192 1.092 / 1.194.
+    // Instances whose rows do not fit 16 bits fall back per instance.
+    const size_t mib = static_cast<size_t>(1) << 20;
+    const bool auto16 = n > 128 ? mat_bytes >= 128 * mib : (mat_bytes >= 192 * mib && mat_bytes < 448 * mib);
+    if (c->resident16 > 0 || (c->resident16 == 0 && auto16)) {
+      KMB_CUDA(c->b16.ensure(nb * np * 2));
+      c16 = c->b16.as<uint16_t>();
+    }
+  }
   int grid = 0;
   // the chunks of a pipelined call size their carveout for the largest chunk
   const int carve_batch = sched.empty() ? 0 : sched[0].second;
@@ -366,6 +392,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.total_cost = dtot + lo;
     a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
     a.status = status_base + lo;
+    a.C16 = c16 ? c16 + ro * np : nullptr;
     return kmb::launch_warp_batch(a, c->sm_count, static_cast<int>(c->warps_per_sm), s, &grid);
   };
   // Pageable host memory (numpy arrays, std::vectors): the costs are staged

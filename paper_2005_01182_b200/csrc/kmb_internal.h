@@ -127,6 +127,9 @@ struct WarpArgs {
   int64_t* total_cost;   // batch
   int64_t* stats;        // batch x KMB_ISTATS (may be null)
   int32_t* status;       // batch
+  // optional workspace, batch x n x pitch uint16 (n > 64 only): the kernel keeps
+  // a 16-bit copy of every row (offsets from the row minimum) and relaxes from it
+  uint16_t* C16;
 };
 int warp_max_n();
 int cta_batch_capacity(int n, int sm_count);  // CTA/L2 engine: instances resident at once

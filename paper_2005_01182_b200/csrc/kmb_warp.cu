@@ -40,6 +40,14 @@ namespace {
 //   ptxas folds early rows of a longer batch before its later loads issue);
 //   low-occupancy build 8 (2048 / 1536 batches .639 / .571 ms vs .664 / .598 at 5)
 constexpr int kRB7 = 5, kRB4 = 8;
+// rows per relax batch over the 16-bit resident copy (two registers a row)
+#ifndef KMB_WARP_RB16_7
+#define KMB_WARP_RB16_7 6
+#endif
+#ifndef KMB_WARP_RB16_4
+#define KMB_WARP_RB16_4 8
+#endif
+constexpr int kRB16_7 = KMB_WARP_RB16_7, kRB16_4 = KMB_WARP_RB16_4;
 // KMB_WARP_STAGE_CLOCKS (diagnostics): per-stage clock64 accounting
 // (kmb_last_instance_stats columns 5-8); costs ~3%, off in production
 #ifndef KMB_WARP_STAGE_CLOCKS
@@ -80,6 +88,33 @@ __device__ __forceinline__ RowVec<CPL> load_row(const int32_t* p) {
   return r;
 }
 
+// 16-bit resident rows: CPL offsets from the row minimum (same warp-width
+// pitch, 2 * CPL bytes a lane), returned already in key position (d << 8) -
+// one PRMT each.  Plain (coherent) loads: the copy is written by this kernel.
+template <int CPL>
+struct RowVec16 {
+  uint32_t x[CPL / 2];
+};
+template <int CPL>
+__device__ __forceinline__ RowVec16<CPL> load_row16(const char* p) {
+  static_assert(CPL == 4 || CPL == 8, "16-bit rows need 4 or 8 columns per lane");
+  RowVec16<CPL> r;
+  if constexpr (CPL == 8) {
+    const uint4 t = *reinterpret_cast<const uint4*>(p);
+    r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
+  } else {
+    const uint2 t = *reinterpret_cast<const uint2*>(p);
+    r.x[0] = t.x; r.x[1] = t.y;
+  }
+  return r;
+}
+// Key-position offsets (d << 8) + tag of the two halves of a packed word: one
+// PRMT each, and the caller's min takes the add (VIADDMNMX).  Doing the unpack
+// on the FMA pipe instead (mul.lo / mad.hi by powers of two; ptxas keeps a
+// LEA.HI) was measured slower: 0.913 vs 0.899 ms on config 3.
+__device__ __forceinline__ uint32_t lo16_key(uint32_t x, uint32_t tag) { return __byte_perm(x, 0u, 0x4104) + tag; }
+__device__ __forceinline__ uint32_t hi16_key(uint32_t x, uint32_t tag) { return __byte_perm(x, 0u, 0x4324) + tag; }
+
 }  // namespace
 
 // Per-warp shared state (n <= 256), in 32-bit words: two row lists of (row,
@@ -87,7 +122,9 @@ __device__ __forceinline__ RowVec<CPL> load_row(const int32_t* p) {
 // u, w, root_row, match_row, match_col, tree_par, claim (7n).  Kept small: what
 // the CTAs per SM do not take of the unified cache is L1 for the streamed
 // matrices.
-__host__ __device__ constexpr int warp_state_words(int n) { return 11 * n; }
+// (+ n with the 16-bit resident copy: each row's minimum, bit 31 = the row does
+// not fit 16 bits and is relaxed from the int32 matrix)
+__host__ __device__ constexpr int warp_state_words(int n, bool u16) { return (u16 ? 12 : 11) * n; }
 
 // Column keys.  Wide: ((c - w + 2^30) << 32) | row (any n, costs < 2^29).
 // Narrow (n <= 256, costs < 2^21): ((c - w + 2^22) << 8) | row in 32 bits, so a
@@ -149,14 +186,18 @@ struct WarpSmem {
   int32_t *u, *w, *root_row, *match_row, *match_col, *tree_par;
   int32_t* ctr;  // [0] rows tail, [1] free columns found this epoch
   uint32_t* claim;
+  int32_t* rminw;      // 16-bit mode only
   int2 *rows, *spare;  // (row, tag)
 };
 
 // One instance, whole warp.  Returns the status (0 ok, -2 internal).
 // RB: rows per relax batch; CACHE: matched rows and their u in registers
-template <int CPL, bool NARROW, int RB, bool CACHE>
+// U16 (narrow keys only): relax from the 16-bit resident copy C16m
+template <int CPL, bool NARROW, int RB, bool CACHE, bool U16 = false, int RB16 = 8>
 __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* Cm, int inst,
-                                              const WarpSmem& S, int lane, const uint64_t (&k0)[CPL]) {
+                                              const WarpSmem& S, int lane, const uint64_t (&k0)[CPL],
+                                              const uint16_t* C16m = nullptr) {
+  static_assert(!U16 || NARROW, "the 16-bit copy goes with narrow keys");
   using KO = Keys<NARROW>;
   using K = typename KO::K;
   constexpr uint32_t FULL = 0xffffffffu;
@@ -165,6 +206,22 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   const uint32_t pb = 4u * np;  // row pitch in bytes
   const int c0 = CPL * lane;
   const char* const lb = reinterpret_cast<const char*>(Cm + c0);  // this lane's columns of row 0
+  const char* const lb16 = reinterpret_cast<const char*>(C16m + c0);
+  // Row-list entry of row i reached with w.  16-bit mode: the byte offset is
+  // the row's in the 16-bit copy and the tag folds the row minimum in,
+  // key = (d << 8) + tag' with d = C - rowmin; a row that does not fit 16 bits
+  // keeps its int32 offset with bit 31 set and the plain tag.
+  auto mk_ent = [&](int32_t i, int32_t wi) {
+    if constexpr (U16) {
+      const int32_t rm = S.rminw[i];
+      const uint32_t t = KO::tag(wi, i);
+      if (rm < 0) return make_int2(static_cast<int32_t>((static_cast<uint32_t>(i) * pb) | 0x80000000u), static_cast<int32_t>(t));
+      return make_int2(static_cast<int32_t>(static_cast<uint32_t>(i) * (pb >> 1)),
+                       static_cast<int32_t>(t + (static_cast<uint32_t>(rm) << 8)));
+    } else {
+      return KO::ent(i, KO::tag(wi, i), pb);
+    }
+  };
   int32_t* const u = S.u;
   int32_t* const w = S.w;
   int32_t* const root_row = S.root_row;
@@ -176,7 +233,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   int2* spare = S.spare;
   int32_t* found = reinterpret_cast<int32_t*>(spare);  // idle row list during an epoch
 
-  for (int k = lane; k < n; k += 32) rows[k] = KO::ent(k, KO::tag(w[k], k), pb);
+  for (int k = lane; k < n; k += 32) rows[k] = mk_ent(k, w[k]);
   if (lane == 0) {
     S.ctr[0] = n;
     S.ctr[1] = 0;
@@ -235,40 +292,106 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     }
     // ---- relax rows[head, nrows)  (hungarian.cpp:164-172) ----
     int r = head;
-    // RB rows in flight: entries, then all row loads, then the folds
-    for (; r + RB - 1 < nrows; r += RB) {
-      int2 e[RB];
-      RowVec<CPL> cv[RB];
+    if constexpr (U16) {
+      // one row folded from the 16-bit copy (tag' in e.y) or, bit 31 of the
+      // offset set, from the int32 matrix (plain tag)
+      auto fold16 = [&](int2 e, const RowVec16<CPL>& cv) {
 #pragma unroll
-      for (int k = 0; k < RB; ++k) e[k] = rows[r + k];
+        for (int h = 0; h < CPL / 2; ++h) {
+          key[2 * h] = KO::kmin(key[2 * h], lo16_key(cv.x[h], static_cast<uint32_t>(e.y)));
+          key[2 * h + 1] = KO::kmin(key[2 * h + 1], hi16_key(cv.x[h], static_cast<uint32_t>(e.y)));
+        }
+      };
+      auto fold_any = [&](int2 e) {  // rare rows (warp-uniform branch)
+        if (e.x < 0) {
+          const RowVec<CPL> c32 = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + (static_cast<uint32_t>(e.x) & 0x7fffffffu)));
 #pragma unroll
-      for (int k = 0; k < RB; ++k) cv[k] = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e[k], pb)));
+          for (int q = 0; q < CPL; ++q) key[q] = KO::kmin(key[q], KO::make(c32.x[q], static_cast<uint32_t>(e.y), 0));
+        } else {
+          fold16(e, load_row16<CPL>(lb16 + static_cast<uint32_t>(e.x)));
+        }
+      };
+      // RB16 rows in flight: entries, then all row loads, then the folds
+      for (; r + RB16 <= nrows; r += RB16) {
+        int2 e[RB16];
+        int32_t anyw = 0;
 #pragma unroll
-      for (int k = 0; k < RB; ++k)
+        for (int k = 0; k < RB16; ++k) {
+          e[k] = rows[r + k];
+          anyw |= e[k].x;
+        }
+        if (anyw >= 0) {
+          RowVec16<CPL> cv[RB16];
+#pragma unroll
+          for (int k = 0; k < RB16; ++k) cv[k] = load_row16<CPL>(lb16 + static_cast<uint32_t>(e[k].x));
+#pragma unroll
+          for (int k = 0; k < RB16; ++k) fold16(e[k], cv[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < RB16; ++k) fold_any(e[k]);
+        }
+      }
+      if (nrows - r == 1) {
+        fold_any(rows[r]);
+      } else {
+        // 2..RB16-1 rows: batches of TB with the last row repeated (the fold is idempotent)
+        constexpr int TB = 4;
+        for (; r < nrows; r += TB) {
+          int2 e[TB];
+          int32_t anyw = 0;
+#pragma unroll
+          for (int k = 0; k < TB; ++k) {
+            e[k] = rows[min(r + k, nrows - 1)];
+            anyw |= e[k].x;
+          }
+          if (anyw >= 0) {
+            RowVec16<CPL> cv[TB];
+#pragma unroll
+            for (int k = 0; k < TB; ++k) cv[k] = load_row16<CPL>(lb16 + static_cast<uint32_t>(e[k].x));
+#pragma unroll
+            for (int k = 0; k < TB; ++k) fold16(e[k], cv[k]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < TB; ++k) fold_any(e[k]);
+          }
+        }
+      }
+    } else {
+      // RB rows in flight: entries, then all row loads, then the folds
+      for (; r + RB - 1 < nrows; r += RB) {
+        int2 e[RB];
+        RowVec<CPL> cv[RB];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) e[k] = rows[r + k];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) cv[k] = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e[k], pb)));
+#pragma unroll
+        for (int k = 0; k < RB; ++k)
+#pragma unroll
+          for (int q = 0; q < CPL; ++q)
+            key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), KO::erow(e[k])));
+      }
+      if (nrows - r == 1) {
+        const int2 e = rows[r];
+        const RowVec<CPL> cv = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e, pb)));
 #pragma unroll
         for (int q = 0; q < CPL; ++q)
-          key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), KO::erow(e[k])));
-    }
-    if (nrows - r == 1) {
-      const int2 e = rows[r];
-      const RowVec<CPL> cv = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e, pb)));
+          key[q] = KO::kmin(key[q], KO::make(cv.x[q], static_cast<uint32_t>(e.y), KO::erow(e)));
+      } else if (r < nrows) {
+        // 2..RB-1 rows: one batch with the last row repeated (the fold is
+        // idempotent), so all loads are in flight together
+        int2 e[RB];
+        RowVec<CPL> cv[RB];
 #pragma unroll
-      for (int q = 0; q < CPL; ++q)
-        key[q] = KO::kmin(key[q], KO::make(cv.x[q], static_cast<uint32_t>(e.y), KO::erow(e)));
-    } else if (r < nrows) {
-      // 2..RB-1 rows: one batch with the last row repeated (the fold is
-      // idempotent), so all loads are in flight together
-      int2 e[RB];
-      RowVec<CPL> cv[RB];
+        for (int k = 0; k < RB; ++k) e[k] = rows[min(r + k, nrows - 1)];
 #pragma unroll
-      for (int k = 0; k < RB; ++k) e[k] = rows[min(r + k, nrows - 1)];
+        for (int k = 0; k < RB; ++k) cv[k] = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e[k], pb)));
 #pragma unroll
-      for (int k = 0; k < RB; ++k) cv[k] = load_row<CPL>(reinterpret_cast<const int32_t*>(lb + KO::eoff(e[k], pb)));
+        for (int k = 0; k < RB; ++k)
 #pragma unroll
-      for (int k = 0; k < RB; ++k)
-#pragma unroll
-        for (int q = 0; q < CPL; ++q)
-          key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), KO::erow(e[k])));
+          for (int q = 0; q < CPL; ++q)
+            key[q] = KO::kmin(key[q], KO::make(cv[k].x[q], static_cast<uint32_t>(e[k].y), KO::erow(e[k])));
+      }
     }
     r = nrows;
     rows_scanned += nrows - head;
@@ -323,7 +446,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
           const int32_t w2 = (CACHE ? mu2[CACHE ? q : 0] : u[i2]) - D;
           w[i2] = w2;
           root_row[i2] = root;
-          rows[atomicAdd(S.ctr, 1)] = KO::ent(i2, KO::tag(w2, i2), pb);
+          rows[atomicAdd(S.ctr, 1)] = mk_ent(i2, w2);
         }
       }
     }
@@ -447,7 +570,13 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
 template <int CPL, int MINB = 7>
 __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
   constexpr int RB = CPL > 4 ? 4 : (MINB >= 7 ? kRB7 : kRB4);
+  constexpr int RB16 = CPL > 4 ? 4 : (MINB >= 7 ? kRB16_7 : kRB16_4);
   constexpr bool CK = MINB < 7;
+  // 16-bit resident copy (a.C16): written by the validation pass, read by every
+  // later relax - half the bytes per row and half the L2 footprint of a batch
+  // that does not fit the L2 as int32
+  constexpr bool kU16able = CPL == 4 || CPL == 8;
+  const bool use16 = kU16able && a.C16 != nullptr;
   extern __shared__ __align__(16) unsigned char dyn[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;  // warp in block
@@ -456,7 +585,7 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
   constexpr uint32_t FULL = 0xffffffffu;
 
   // carve this warp's slice: [2 counters | state]
-  const size_t wbytes = static_cast<size_t>(warp_state_words(n)) * 4 + 16;
+  const size_t wbytes = static_cast<size_t>(warp_state_words(n, use16)) * 4 + 16;
   unsigned char* base = dyn + wib * ((wbytes + 15) & ~static_cast<size_t>(15));
   int32_t* ctr = reinterpret_cast<int32_t*>(base);
   int32_t* st = reinterpret_cast<int32_t*>(base + 16);
@@ -470,6 +599,7 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
   S.match_col = S.match_row + n;
   S.tree_par = S.match_col + n;
   S.claim = reinterpret_cast<uint32_t*>(S.tree_par + n);
+  S.rminw = reinterpret_cast<int32_t*>(S.claim + n);  // 16-bit mode only
   S.ctr = ctr;
   const int c0 = CPL * lane;
 
@@ -493,6 +623,12 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
     // The same pass is the search's first relax (every row reached at D = 0
     // with w = u0): the keys are folded here, in the wide (value, row) form
     // the key width is picked from afterwards, so the matrix is read once less.
+    uint16_t* const C16m = use16 ? a.C16 + static_cast<int64_t>(inst) * n * np : nullptr;
+    // per instance: packing stops (and the solve reads int32 rows) once more
+    // than ~n/16 rows have a range beyond 16 bits - such rows are relaxed from
+    // the int32 matrix anyway, one at a time
+    bool pack = use16;
+    int nwide = 0;
     int32_t lo_all = 0x7fffffff, hi_all = 0;
     uint64_t k0[CPL];
 #pragma unroll
@@ -524,14 +660,42 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
           S.u[i] = u0;
           S.w[i] = u0;
         }
+        if constexpr (kU16able) {
+          if (pack) {  // d = C - rowmin, saturated; a saturated valid column marks the row
+            uint32_t d[CPL];
+            bool sat = false;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+              const uint32_t x = static_cast<uint32_t>(cv[k].x[q]) - static_cast<uint32_t>(lo);
+              d[q] = x >= 65535u ? 65535u : x;
+              sat |= (c0 + q < n) && x >= 65535u;
+            }
+            sat = __any_sync(FULL, sat);
+            uint16_t* out = C16m + static_cast<int64_t>(i) * np + c0;
+            if constexpr (CPL == 8) {
+              *reinterpret_cast<uint4*>(out) = make_uint4(d[0] | (d[1] << 16), d[2] | (d[3] << 16),
+                                                          d[4] | (d[5] << 16), d[6] | (d[7] << 16));
+            } else {
+              *reinterpret_cast<uint2*>(out) = make_uint2(d[0] | (d[1] << 16), d[2] | (d[3] << 16));
+            }
+            if (lane == (i & 31)) S.rminw[i] = sat ? (lo | static_cast<int32_t>(0x80000000u)) : lo;
+            nwide += sat;
+          }
+        }
       }
+      if (nwide * 16 > n + 16) pack = false;
     }
     hi_all = __reduce_max_sync(FULL, hi_all);
     int status = lo_all < 0 ? 2 : (hi_all >= (1 << 29) ? 3 : 0);
     __syncwarp();
     if (status == 0) {
-      status = hi_all < (1 << 21) ? solve_instance<CPL, true, RB, CK>(a, Cm, inst, S, lane, k0)
-                                  : solve_instance<CPL, false, RB, CK>(a, Cm, inst, S, lane, k0);
+      if (hi_all >= (1 << 21)) {
+        status = solve_instance<CPL, false, RB, CK>(a, Cm, inst, S, lane, k0);
+      } else if (kU16able && pack) {
+        if constexpr (kU16able) status = solve_instance<CPL, true, RB, CK, true, RB16>(a, Cm, inst, S, lane, k0, C16m);
+      } else {
+        status = solve_instance<CPL, true, RB, CK>(a, Cm, inst, S, lane, k0);
+      }
     } else {
       for (int k = lane; k < n; k += 32) a.row_to_col[static_cast<int64_t>(inst) * n + k] = -1;
       if (lane == 0) a.total_cost[inst] = 0;
@@ -549,8 +713,8 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
 
 int warp_max_n() { return 256; }
 
-size_t warp_smem_per_warp(int n) {
-  return (static_cast<size_t>(warp_state_words(n)) * 4 + 16 + 15) & ~static_cast<size_t>(15);
+size_t warp_smem_per_warp(int n, bool u16) {
+  return (static_cast<size_t>(warp_state_words(n, u16)) * 4 + 16 + 15) & ~static_cast<size_t>(15);
 }
 
 template <int CPL, int MINB = 7>
@@ -563,7 +727,7 @@ static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, int warps_
       return launch_t<CPL, 4>(a, sm_count, wpb, warps_per_sm, st, grid_out);
   }
   auto kern = k_warp_batch<CPL, MINB>;
-  const size_t smem = warp_smem_per_warp(a.n) * wpb;
+  const size_t smem = warp_smem_per_warp(a.n, (CPL == 4 || CPL == 8) && a.C16 != nullptr) * wpb;
   // Shared-memory carveout: just the state of the CTAs per SM this launch
   // needs (all instances resident in one wave, at most the register limit),
   // +1 KiB reserved per CTA; the rest of the unified cache is L1, which keeps

@@ -10,7 +10,12 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     key = os.environ.get("CFG", "c3"); eng = int(os.environ.get("ENGINE", "0"))
     s = Solver(0)
     if eng: s.set_option(OPT_ENGINE, eng)
-    c = W.CONFIGS[key].make()
+    if os.environ.get("RES16"): s.set_option(7, int(os.environ["RES16"]))
+    if key.startswith("u"):  # uNxB[xH]: B uniform U{0..H} (100000) instances of size N
+        nn, bb, *hi = map(int, key[1:].split("x"))
+        c = np.random.default_rng(1).integers(0, (hi[0] if hi else 100000) + 1, size=(bb, nn, nn), dtype=np.int32)
+    else:
+        c = W.CONFIGS[key].make(batch=int(os.environ["MAKE_BATCH"])) if os.environ.get("MAKE_BATCH") else W.CONFIGS[key].make()
     if c.ndim == 2: c = c[None]
     if os.environ.get("BATCH"): c = np.ascontiguousarray(c[:int(os.environ["BATCH"])])
     b, n, _ = c.shape

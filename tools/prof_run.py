@@ -17,6 +17,7 @@ s = Solver(0)
 s.set_option(OPT_ENGINE, a.engine)
 from paper_2005_01182_b200.api import OPT_MAX_CTAS
 s.set_option(OPT_MAX_CTAS, a.maxg)
+if os.environ.get("RES16"): s.set_option(7, int(os.environ["RES16"]))
 c = W.CONFIGS[a.config].make(batch=a.batch) if a.config == "c3" else W.CONFIGS[a.config].make()
 dc = torch.from_numpy(c).cuda()
 if a.config == "c3":
