@@ -145,6 +145,8 @@ struct Keys<false> {
     return (static_cast<uint64_t>(static_cast<uint32_t>(c) + tag) << 32) | static_cast<uint32_t>(row);
   }
   __device__ static int32_t val(K k) { return static_cast<int32_t>(static_cast<int64_t>(k >> 32) - KMB_BIAS); }
+  static constexpr int32_t VOFF = 0;  // the search keeps v + VOFF per column
+  __device__ static int32_t slack(K k, int32_t vq) { return val(k) - vq; }
   __device__ static int32_t row(K k) { return static_cast<int32_t>(static_cast<uint32_t>(k)); }
   __device__ static K kmin(K a, K b) { return a < b ? a : b; }
   __device__ static K from_wide(uint64_t k) { return k; }
@@ -165,6 +167,8 @@ struct Keys<true> {
     return (static_cast<uint32_t>(c) << 8) + tag;
   }
   __device__ static int32_t val(K k) { return static_cast<int32_t>(k >> 8) - NB; }
+  static constexpr int32_t VOFF = NB;  // v is kept with the key bias added: slack' is one shift-subtract
+  __device__ static int32_t slack(K k, int32_t vq) { return static_cast<int32_t>(k >> 8) - vq; }
   __device__ static int32_t row(K k) { return static_cast<int32_t>(k & 0xffu); }
   __device__ static K kmin(K a, K b) { return min(a, b); }
   // a wide key (c - w + 2^30, row) as a narrow one (c - w + 2^22, row)
@@ -248,12 +252,12 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   constexpr int32_t RBIG = NARROW ? (1 << 29) : 0;
 #pragma unroll
   for (int q = 0; q < CPL; ++q) {
-    v[q] = 0;
+    v[q] = KO::VOFF;
     dc[q] = 0;
     key[q] = KO::from_wide(k0[q]);  // every row relaxed once by the validation pass
     if (c0 + q >= n) {
       pad |= 1u << q;
-      v[q] = -RBIG;
+      v[q] = KO::VOFF - RBIG;
     }
   }
   uint32_t rch = pad;  // bit q: column c0+q reached (padding counts as reached)
@@ -400,14 +404,14 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     if (epochs == 0 && rounds == 1 && a.seed == 1) {  // column reduction, :328-333
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
-        if (!((pad >> q) & 1)) v[q] = KO::val(key[q]);
+        if (!((pad >> q) & 1)) v[q] = KO::val(key[q]) + KO::VOFF;
     }
     // ---- min unreached slack' (hungarian.cpp:203-206) ----
     int32_t s[CPL];
     int32_t lm = 0x7fffffff;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
-      s[q] = KO::val(key[q]) - v[q];
+      s[q] = KO::slack(key[q], v[q]);
       if (NARROW || !((rch >> q) & 1)) lm = min(lm, s[q]);
     }
     const int32_t m = __reduce_min_sync(FULL, lm);
@@ -423,15 +427,18 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     // ---- absorb zero-slack columns (hungarian.cpp:186-199) ----
     // Usually one column per round turns tight: only its lane branches in, and
     // appends go through warp-private shared counters (no per-column ballots).
+    // (narrow keys: a lane holds a tight column exactly when its minimum is D)
     uint32_t tm = 0;
+    if constexpr (!NARROW) {
 #pragma unroll
-    for (int q = 0; q < CPL; ++q)
-      if ((NARROW || !((rch >> q) & 1)) && s[q] == D) tm |= 1u << q;
-    if (tm) {
-      rch |= tm;
+      for (int q = 0; q < CPL; ++q)
+        if (!((rch >> q) & 1) && s[q] == D) tm |= 1u << q;
+    }
+    if (NARROW ? lm == D : tm != 0) {
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
-        if (!((tm >> q) & 1)) continue;
+        if (NARROW ? s[q] != D : !((tm >> q) & 1)) continue;
+        rch |= 1u << q;
         const int col = c0 + q;
         dc[q] = D;
         v[q] -= RBIG;
@@ -545,7 +552,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   }
 #pragma unroll
   for (int q = 0; q < CPL; ++q)
-    if (c0 + q < n) a.v[static_cast<int64_t>(inst) * n + c0 + q] = v[q] + (((rch >> q) & 1) ? RBIG : 0);
+    if (c0 + q < n) a.v[static_cast<int64_t>(inst) * n + c0 + q] = v[q] - KO::VOFF + (((rch >> q) & 1) ? RBIG : 0);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
   if (lane == 0) {
