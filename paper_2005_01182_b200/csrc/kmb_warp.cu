@@ -109,11 +109,11 @@ __device__ __forceinline__ RowVec16<CPL> load_row16(const char* p) {
   return r;
 }
 // Key-position offsets (d << 8) + tag of the two halves of a packed word: one
-// PRMT each, and the caller's min takes the add (VIADDMNMX).  Doing the unpack
+// PRMT each; the caller's fused add-min (VIADDMNMX) takes the tag.  Doing the unpack
 // on the FMA pipe instead (mul.lo / mad.hi by powers of two; ptxas keeps a
 // LEA.HI) was measured slower: 0.913 vs 0.899 ms on config 3.
-__device__ __forceinline__ uint32_t lo16_key(uint32_t x, uint32_t tag) { return __byte_perm(x, 0u, 0x4104) + tag; }
-__device__ __forceinline__ uint32_t hi16_key(uint32_t x, uint32_t tag) { return __byte_perm(x, 0u, 0x4324) + tag; }
+__device__ __forceinline__ uint32_t lo16_key(uint32_t x) { return __byte_perm(x, 0u, 0x4104); }
+__device__ __forceinline__ uint32_t hi16_key(uint32_t x) { return __byte_perm(x, 0u, 0x4324); }
 
 }  // namespace
 
@@ -302,8 +302,9 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       auto fold16 = [&](int2 e, const RowVec16<CPL>& cv) {
 #pragma unroll
         for (int h = 0; h < CPL / 2; ++h) {
-          key[2 * h] = KO::kmin(key[2 * h], lo16_key(cv.x[h], static_cast<uint32_t>(e.y)));
-          key[2 * h + 1] = KO::kmin(key[2 * h + 1], hi16_key(cv.x[h], static_cast<uint32_t>(e.y)));
+          // min((d << 8) + tag', key): the DPX add-min, one VIADDMNMX per column
+          key[2 * h] = __viaddmin_u32(lo16_key(cv.x[h]), static_cast<uint32_t>(e.y), key[2 * h]);
+          key[2 * h + 1] = __viaddmin_u32(hi16_key(cv.x[h]), static_cast<uint32_t>(e.y), key[2 * h + 1]);
         }
       };
       auto fold_any = [&](int2 e) {  // rare rows (warp-uniform branch)
@@ -434,6 +435,9 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       for (int q = 0; q < CPL; ++q)
         if (!((rch >> q) & 1) && s[q] == D) tm |= 1u << q;
     }
+    // (Numbering the slots in the single tight lane of the usual round and
+    // broadcasting the totals - a ballot and two shuffles instead of the shared
+    // atomics and the counter reads - was measured slower: 0.864 -> 0.910 ms.)
     if (NARROW ? lm == D : tm != 0) {
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
