@@ -260,6 +260,11 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       v[q] = KO::VOFF - RBIG;
     }
   }
+  if (a.seed == 1) {  // column reduction, :328-333 (the keys already hold every row's u0-reduced costs)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+      if (!((pad >> q) & 1)) v[q] = KO::val(key[q]) + KO::VOFF;
+  }
   uint32_t rch = pad;  // bit q: column c0+q reached (padding counts as reached)
   // CACHE (low-occupancy build): each column's matched row and its u in
   // registers between epoch ends (both change only there)
@@ -273,6 +278,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   int32_t D = 0;
   int epochs = 0, dual_steps = 0, rows_scanned = n, rounds = 0;
   int status = 0;
+  bool stuck = false;
   const int round_cap = 4 * n * n + 64;
   const long long t_start = clock64();
   long long cyc[4] = {0, 0, 0, 0};  // relax, min, absorb, epoch end
@@ -290,7 +296,9 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   __syncwarp();
 
   while (nfree > 0) {
-    if (++rounds > round_cap) {  // a valid search ends in n epochs of <= 2n + 1 rounds
+    // a valid search ends in n epochs of <= 2n + 1 rounds and always has an
+    // unreached column while a row is free
+    if (++rounds > round_cap || stuck) {
       status = -2;
       break;
     }
@@ -402,11 +410,6 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
     rows_scanned += nrows - head;
     head = nrows;
     KMB_WSTAGE(0);
-    if (epochs == 0 && rounds == 1 && a.seed == 1) {  // column reduction, :328-333
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-        if (!((pad >> q) & 1)) v[q] = KO::val(key[q]) + KO::VOFF;
-    }
     // ---- min unreached slack' (hungarian.cpp:203-206) ----
     int32_t s[CPL];
     int32_t lm = 0x7fffffff;
@@ -416,12 +419,11 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
       if (NARROW || !((rch >> q) & 1)) lm = min(lm, s[q]);
     }
     const int32_t m = __reduce_min_sync(FULL, lm);
-    if (m > D) {
-      if (NARROW ? m >= (RBIG >> 1) : m == 0x7fffffff) {
-        status = -2;
-        break;
-      }
-      D = m;  // dual step (hungarian.cpp:207-215), applied lazily
+    // dual step (hungarian.cpp:207-215), applied lazily; no unreached column
+    // left (an engine fault) ends the search at the next loop head
+    stuck = NARROW ? m >= (RBIG >> 1) : m == 0x7fffffff;
+    if (m > D && !stuck) {
+      D = m;
       ++dual_steps;
     }
     KMB_WSTAGE(1);
