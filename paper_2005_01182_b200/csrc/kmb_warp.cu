@@ -124,7 +124,11 @@ __device__ __forceinline__ uint32_t hi16_key(uint32_t x) { return __byte_perm(x,
 // matrices.
 // (+ n with the 16-bit resident copy: each row's minimum, bit 31 = the row does
 // not fit 16 bits and is relaxed from the int32 matrix)
-__host__ __device__ constexpr int warp_state_words(int n, bool u16) { return (u16 ? 12 : 11) * n; }
+// The arrays are strided by the padded size 32 * CPL for n <= 128 (compile-time
+// offsets from one base register instead of multiplies by n on every round's
+// critical path), by n above (12 KB a warp would cost residency).
+__host__ __device__ constexpr int warp_state_stride(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n; }
+__host__ __device__ constexpr int warp_state_words(int n, bool u16) { return (u16 ? 12 : 11) * warp_state_stride(n); }
 
 // Column keys.  Wide: ((c - w + 2^30) << 32) | row (any n, costs < 2^29).
 // Narrow (n <= 256, costs < 2^21): ((c - w + 2^22) << 8) | row in 32 bits, so a
@@ -279,7 +283,7 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   int epochs = 0, dual_steps = 0, rows_scanned = n, rounds = 0;
   int status = 0;
   bool stuck = false;
-  const int round_cap = 4 * n * n + 64;
+  constexpr int round_cap = 4 * 256 * 256 + 64;  // n <= 256; an immediate (4 n^2 + 64 was recomputed every round)
   const long long t_start = clock64();
   long long cyc[4] = {0, 0, 0, 0};  // relax, min, absorb, epoch end
   long long tl = t_start;
@@ -603,16 +607,17 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
   int32_t* ctr = reinterpret_cast<int32_t*>(base);
   int32_t* st = reinterpret_cast<int32_t*>(base + 16);
   WarpSmem S;
+  const int sn = CPL <= 4 ? 32 * CPL : n;  // == warp_state_stride(n)
   S.rows = reinterpret_cast<int2*>(st);  // 8-byte aligned first
-  S.spare = S.rows + n;
-  S.u = reinterpret_cast<int32_t*>(S.spare + n);
-  S.w = S.u + n;
-  S.root_row = S.w + n;
-  S.match_row = S.root_row + n;
-  S.match_col = S.match_row + n;
-  S.tree_par = S.match_col + n;
-  S.claim = reinterpret_cast<uint32_t*>(S.tree_par + n);
-  S.rminw = reinterpret_cast<int32_t*>(S.claim + n);  // 16-bit mode only
+  S.spare = S.rows + sn;
+  S.u = reinterpret_cast<int32_t*>(S.spare + sn);
+  S.w = S.u + sn;
+  S.root_row = S.w + sn;
+  S.match_row = S.root_row + sn;
+  S.match_col = S.match_row + sn;
+  S.tree_par = S.match_col + sn;
+  S.claim = reinterpret_cast<uint32_t*>(S.tree_par + sn);
+  S.rminw = reinterpret_cast<int32_t*>(S.claim + sn);  // 16-bit mode only
   S.ctr = ctr;
   const int c0 = CPL * lane;
 
