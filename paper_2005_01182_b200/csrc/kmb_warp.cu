@@ -210,8 +210,8 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
   using K = typename KO::K;
   constexpr uint32_t FULL = 0xffffffffu;
   const int n = a.n;
-  const uint32_t np = static_cast<uint32_t>(a.pitch);
-  const uint32_t pb = 4u * np;  // row pitch in bytes
+  constexpr uint32_t np = 32u * CPL;  // == a.pitch (launch_warp_batch checks it)
+  constexpr uint32_t pb = 4u * np;    // row pitch in bytes
   const int c0 = CPL * lane;
   const char* const lb = reinterpret_cast<const char*>(Cm + c0);  // this lane's columns of row 0
   const char* const lb16 = reinterpret_cast<const char*>(C16m + c0);
@@ -598,7 +598,8 @@ __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;  // warp in block
   const int wpb = blockDim.x >> 5;
-  const int n = a.n, np = a.pitch;
+  const int n = a.n;
+  constexpr int np = 32 * CPL;  // == a.pitch (launch_warp_batch checks it)
   constexpr uint32_t FULL = 0xffffffffu;
 
   // carve this warp's slice: [2 counters | state]
