@@ -232,7 +232,9 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // auto: a batch (or pipeline chunk) that fits the CTA engine's residency in
   // one wave runs one CTA per instance (shorter rounds: 0.38 vs 0.47 ms for a
   // 512-instance config-3 shard); larger batches one warp per instance, all
-  // resident (1.00 ms at 4096 vs 1.7 for CTAs)
+  // resident (0.78 ms at 4096 vs 1.7 for CTAs).  The warp engine is ahead from
+  // ~11/12 of that residency on (config 3, warp / CTA: 1,024 0.479 / 0.469 ms,
+  // 1,184 0.473 / 0.493)
   const bool auto_engine = engine == 0 || engine == 1 || engine == 5;
   const int cap6 = auto_engine ? kmb::cta_batch_capacity(n, c->sm_count) : 0;
   // n > 256: one 512-thread CTA per instance (single-CTA engine, n <= 4096),
@@ -240,7 +242,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   // 16-CTA cluster each (4 x n = 3072: 43.6 -> 26.0 ms; at 9 clusters the
   // single-CTA engine is ahead again: 9 x n = 2500 38.5 vs 40.9 ms)
   auto pick = [&](int cnt) {
-    if (n <= kmb::warp_max_n()) return cnt <= cap6 ? 6 : 4;
+    if (n <= kmb::warp_max_n()) return cnt * 12 <= cap6 * 11 ? 6 : 4;
     return (n > 1792 && n <= 4608 && cnt * 32 <= c->sm_count) ? 11 : 8;
   };
   if (auto_engine) engine = pick(batch);
