@@ -1,7 +1,9 @@
 """Randomised stress: engines x sizes x value ranges x seeds against the
 reference (duals, total cost) and against themselves (determinism: the same
 matching and round count twice).  Usage: python tools/stress.py [seconds]
-(BATCH=1: random batches through every batch engine instead; WIDE=1: int64
+(BATCH=1: random batches through every batch engine instead; RES16=1: the warp
+engine relaxing from its 16-bit resident copy, value ranges around the 16-bit
+and narrow-key limits, rows and instances that do not fit; WIDE=1: int64
 costs up to validate_instance's headroom through kmb_solve_i64 / the wide
 engine; SHARD=1: the device-exchange column-sharded engine with 1-8 ranks as
 CTA groups, against the reference and the grid engine's matching)."""
@@ -17,6 +19,35 @@ rng = np.random.default_rng(int(os.environ.get("SEED", "12345")))
 t0 = time.time(); cases = 0; bad = 0
 while time.time() - t0 < budget:
     hi = int(rng.choice([2, 10, 1000, 10**6, 2**29 - 1]))
+    if os.environ.get("RES16"):
+        n = int(rng.integers(65, 257)); b = int(rng.integers(1, 24))
+        h16 = int(rng.choice([100, 30000, 65534, 65535, 65536, 65537, 70000, 10**6, 2**21 - 1, 2**21, 2**23]))
+        cb = rng.integers(0, h16 + 1, size=(b, n, n)).astype(np.int32)
+        if rng.random() < 0.5:  # a few rows (sometimes many) leave the 16-bit range
+            for t in range(b):
+                k = int(rng.choice([0, 1, 2, n // 16, n // 16 + 3, n // 4]))
+                if k:
+                    rr = rng.choice(n, size=k, replace=False)
+                    cb[t][rr, int(rng.integers(0, n))] += int(rng.choice([65535, 10**5, 10**6]))
+        if rng.random() < 0.3:
+            cb += int(rng.integers(0, 10**6))  # a common offset: the copy is relative to the row minimum
+        seed = int(rng.choice([KMB_SEED_BATCHED, KMB_SEED_KM]))
+        refs = [O.ref_solve_batched_km(x) if seed == KMB_SEED_BATCHED else O.ref_solve_km(x) for x in cb]
+        s.set_option(OPT_ENGINE, 4)
+        out = {}
+        for mode in (1, -1):
+            s.set_option(7, mode)
+            out[mode] = r = s.solve_batch(cb, seed)
+            ok = all(np.array_equal(r.u[t], refs[t].u) and np.array_equal(r.v[t], refs[t].v)
+                     and r.total_cost[t] == refs[t].total_cost for t in range(b))
+            cases += 1
+            if not ok:
+                bad += 1
+                print(f"MISMATCH res16={mode} b={b} n={n} hi={h16} seed={seed}", flush=True)
+        if not np.array_equal(out[1].row_to_col, out[-1].row_to_col):
+            bad += 1
+            print(f"MATCHING DIFFERS between modes b={b} n={n} hi={h16} seed={seed}", flush=True)
+        continue
     if os.environ.get("BATCH"):  # batch engines: warp (SMEM / L2), CTA (SMEM / L2), single-CTA
         n = int(rng.integers(1, 300)); b = int(rng.integers(1, 40))
         cb = rng.integers(0, hi, size=(b, n, n)).astype(np.int32)
