@@ -305,9 +305,11 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
   int32_t* const status_base = async_status ? async_status : c->bstatus.as<int32_t>();
   const int32_t* src = dcost;  // vector-load engines: rows padded to np
   // warp engine: 16-bit resident copy of the rows (KMB_OPT_RESIDENT16)
+  // decided per launch (a pipelined call's chunks are launches of their own)
   uint16_t* c16 = nullptr;
-  if (warp_eng && n > 64) {
-    const size_t mat_bytes = nb * np * 4;
+  auto want16 = [&](int cnt) {
+    if (n <= 64 || n > kmb::warp_max_n()) return false;
+    const size_t mat_bytes = static_cast<size_t>(cnt) * n * np * 4;
     // auto (measured on one B200, ms without / with the copy):
     //  n > 128 (8 columns a lane): from 128 MiB of matrices up - n = 256 x 700
     //    1.75 / 1.69, x 1,024 2.16 / 1.79, x 4,096 5.58 / 4.37; n = 200 x 2,000
@@ -320,7 +322,16 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     // Instances whose rows do not fit 16 bits fall back per instance.
     const size_t mib = static_cast<size_t>(1) << 20;
     const bool auto16 = n > 128 ? mat_bytes >= 128 * mib : (mat_bytes >= 192 * mib && mat_bytes < 448 * mib);
-    if (c->resident16 > 0 || (c->resident16 == 0 && auto16)) {
+    return c->resident16 > 0 || (c->resident16 == 0 && auto16);
+  };
+  {
+    bool any16 = false;  // does any launch of this call run the warp engine with the copy?
+    if (sched.empty()) {
+      any16 = warp_eng && want16(batch);
+    } else {
+      for (const auto& ch : sched) any16 = any16 || ((auto_engine ? pick(ch.second) : engine) == 4 && want16(ch.second));
+    }
+    if (any16) {
       KMB_CUDA(c->b16.ensure(nb * np * 2));
       c16 = c->b16.as<uint16_t>();
     }
@@ -394,7 +405,7 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     a.total_cost = dtot + lo;
     a.stats = c->bstat.as<int64_t>() + static_cast<size_t>(lo) * kmb::KMB_ISTATS;
     a.status = status_base + lo;
-    a.C16 = c16 ? c16 + ro * np : nullptr;
+    a.C16 = c16 && want16(cnt) ? c16 + ro * np : nullptr;
     return kmb::launch_warp_batch(a, c->sm_count, static_cast<int>(c->warps_per_sm), s, &grid);
   };
   // Pageable host memory (numpy arrays, std::vectors): the costs are staged

@@ -88,6 +88,28 @@ def test_resident16_same_assignment_as_int32(solver):
         np.testing.assert_array_equal(out[1].u[t], ref.u)
 
 
+def test_resident16_host_pipeline(solver):
+    """A host batch of >= 256 instances is solved in chunks as its copy lands;
+    each chunk packs into its own slice of the workspace."""
+    c = W.CONFIGS["c3"].make(batch=320)
+    solver.set_option(OPT_ENGINE, 4)
+    try:
+        out = {}
+        for mode in (-1, 1):
+            solver.set_option(OPT_RESIDENT16, mode)
+            out[mode] = solver.solve_batch(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_RESIDENT16, 0)
+        solver.set_option(OPT_ENGINE, 0)
+    for f in ("row_to_col", "u", "v", "total_cost"):
+        np.testing.assert_array_equal(getattr(out[-1], f), getattr(out[1], f))
+    for t in (0, 63, 64, 159, 160, 255, 256, 319):
+        ref = O.ref_solve_batched_km(c[t])
+        assert out[1].total_cost[t] == ref.total_cost
+        np.testing.assert_array_equal(out[1].u[t], ref.u)
+        np.testing.assert_array_equal(out[1].v[t], ref.v)
+
+
 def test_resident16_invalid_instances(warp16):
     """Negative and out-of-range entries are reported per instance; the others
     of the batch are solved."""
