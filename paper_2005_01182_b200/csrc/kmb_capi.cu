@@ -312,8 +312,8 @@ static int solve_batch_impl(kmb_context* c, const int32_t* costs, int32_t batch,
     const size_t mat_bytes = static_cast<size_t>(cnt) * n * np * 4;
     // auto (measured on one B200, ms without / with the copy):
     //  n > 128 (8 columns a lane): from 128 MiB of matrices up - n = 256 x 700
-    //    1.75 / 1.69, x 1,024 2.16 / 1.79, x 4,096 5.58 / 4.37; n = 200 x 2,000
-    //    2.27 / 1.62; n = 160 x 4,096 2.38 / 1.79;
+    //    1.22 / 1.11, x 1,024 1.49 / 1.22, x 4,096 5.63 / 2.89; n = 200 x 2,000
+    //    1.62 / 1.24; n = 160 x 4,096 2.43 / 1.60;
     //  n <= 128: between 1.5 x the L2 and 448 MiB - config 3 (64 KiB matrices)
     //    x 2,560 0.721 / 0.747, x 3,072 0.785 / 0.772, x 3,584 0.856 / 0.821,
     //    x 4,096 0.956 / 0.899, x 6,000 1.452 / 1.370, x 8,192 1.753 / 1.790

@@ -50,6 +50,9 @@ constexpr int kRB7 = 5, kRB4 = 8;
 constexpr int kRB16_7 = KMB_WARP_RB16_7, kRB16_4 = KMB_WARP_RB16_4;
 // KMB_WARP_STAGE_CLOCKS (diagnostics): per-stage clock64 accounting
 // (kmb_last_instance_stats columns 5-8); costs ~3%, off in production
+#ifndef KMB_WARP_ROOMY8
+#define KMB_WARP_ROOMY8 1
+#endif
 #ifndef KMB_WARP_STAGE_CLOCKS
 #define KMB_WARP_STAGE_CLOCKS 0
 #endif
@@ -586,8 +589,17 @@ __device__ __forceinline__ int solve_instance(const WarpArgs& a, const int32_t* 
 // warps per SM
 template <int CPL, int MINB = 7>
 __global__ void __launch_bounds__(128, MINB) k_warp_batch(WarpArgs a) {
-  constexpr int RB = CPL > 4 ? 4 : (MINB >= 7 ? kRB7 : kRB4);
-  constexpr int RB16 = CPL > 4 ? 4 : (MINB >= 7 ? kRB16_7 : kRB16_4);
+  // 8 columns a lane, 128-register build: 4 int32 rows / 8 16-bit rows per
+  // batch (n = 256 x 4,096, 16-bit rows: 3.26 ms at 4, 2.89 at 8, 3.01 at 10,
+  // 2.91 at 12; 6 int32 rows: n = 256 x 1,024 1.52 -> 1.62)
+#ifndef KMB_WARP_RB8L
+#define KMB_WARP_RB8L 4
+#endif
+#ifndef KMB_WARP_RB16_8L
+#define KMB_WARP_RB16_8L 8
+#endif
+  constexpr int RB = CPL > 4 ? (MINB >= 7 ? 4 : KMB_WARP_RB8L) : (MINB >= 7 ? kRB7 : kRB4);
+  constexpr int RB16 = CPL > 4 ? (MINB >= 7 ? 4 : KMB_WARP_RB16_8L) : (MINB >= 7 ? kRB16_7 : kRB16_4);
   constexpr bool CK = MINB < 7;
   // 16-bit resident copy (a.C16): written by the validation pass, read by every
   // later relax - half the bytes per row and half the L2 footprint of a batch
@@ -739,10 +751,15 @@ size_t warp_smem_per_warp(int n, bool u16) {
 template <int CPL, int MINB = 7>
 static cudaError_t launch_t(const WarpArgs& a, int sm_count, int wpb, int warps_per_sm,
                             cudaStream_t st, int* grid_out) {
-  if constexpr (MINB == 7 && CPL == 4) {
+  if constexpr (MINB == 7 && CPL >= 4) {
     // a batch that needs at most 4 CTAs (16 warps) per SM runs the 128-register
-    // instance (config-3 shards of <= 2,368 instances)
-    if (warps_per_sm == 0 && (a.batch + wpb - 1) / wpb <= 4 * sm_count)
+    // instance (config-3 shards of <= 2,368 instances); so does one whose
+    // per-warp state leaves room for no more than 4 CTAs anyway (n > ~190: the
+    // 72-register build of 8 columns a lane spills)
+    const size_t smem4 = warp_smem_per_warp(a.n, (CPL == 4 || CPL == 8) && a.C16 != nullptr) * wpb + 1024;
+    const bool few = (a.batch + wpb - 1) / wpb <= 4 * sm_count;
+    const bool roomy = CPL == 8 && KMB_WARP_ROOMY8 && 5 * smem4 > 227 * 1024;
+    if (warps_per_sm == 0 && (few || roomy))
       return launch_t<CPL, 4>(a, sm_count, wpb, warps_per_sm, st, grid_out);
   }
   auto kern = k_warp_batch<CPL, MINB>;

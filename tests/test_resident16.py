@@ -110,6 +110,30 @@ def test_resident16_host_pipeline(solver):
         np.testing.assert_array_equal(out[1].v[t], ref.v)
 
 
+def test_resident16_large_batch_8_columns_a_lane(solver):
+    """n > 128 with more instances than 16 warps per SM hold: the 72-register
+    build of the 8-columns-a-lane kernel (smaller batches run the 128-register
+    one), both row modes."""
+    rng = np.random.default_rng(11)
+    c = rng.integers(0, 3001, size=(2400, 136, 136), dtype=np.int32)
+    solver.set_option(OPT_ENGINE, 4)
+    try:
+        out = {}
+        for mode in (-1, 1):
+            solver.set_option(OPT_RESIDENT16, mode)
+            out[mode] = solver.solve_batch(c, KMB_SEED_BATCHED)
+    finally:
+        solver.set_option(OPT_RESIDENT16, 0)
+        solver.set_option(OPT_ENGINE, 0)
+    for f in ("row_to_col", "u", "v", "total_cost"):
+        np.testing.assert_array_equal(getattr(out[-1], f), getattr(out[1], f))
+    for t in range(0, 2400, 97):
+        ref = O.ref_solve_batched_km(c[t])
+        assert out[1].total_cost[t] == ref.total_cost
+        np.testing.assert_array_equal(out[1].u[t], ref.u)
+        np.testing.assert_array_equal(out[1].v[t], ref.v)
+
+
 def test_resident16_invalid_instances(warp16):
     """Negative and out-of-range entries are reported per instance; the others
     of the batch are solved."""
